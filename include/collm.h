@@ -1,0 +1,124 @@
+/* collm.h — C ABI of the B200 co-batched LoRA layer (CoLLM unified PEFT layer).
+ *
+ * The drop-in boundary for the reference's replica-step hot path.  The reference (coserve,
+ * /root/reference/pkg/src/coserve) is pure Python and binds no native code; the functions below are
+ * what its Python seam calls (via ctypes) in place of the stand-ins it uses
+ * today:
+ *
+ *   perf.true_infer_latency      perf.py:62-74     -> collm_lora_shrink + collm_gemm_lora (forward)
+ *   perf.true_train_latency      perf.py:77-89     -> forward + collm_lora_shrink (dH) +
+ *                                                     collm_gemm_lora (dX) + collm_lora_reduce
+ *   perf.train_step              perf.py:111-126   -> collm_lora_reduce(mode=ADAMW) (real update)
+ *   AdapterParams.perturbed      launcher.py:43-47 -> collm_lora_reduce(mode=ADAMW)
+ *   fedavg                       launcher.py:68-80 -> NCCL allreduce(avg) + collm_lora_apply(COPY)
+ *   domain.Batch / pop_up_to     domain.py:64-86, dispatcher.py:66-82
+ *                                                  -> collm_plan_segments + collm_expand_segments
+ *
+ * Conventions: plain C types, device pointers for tensors (bf16 = 2-byte bfloat16, row-major,
+ * leading dimensions in ELEMENTS), `stream` is a cudaStream_t passed as void*.  All launches are
+ * asynchronous on `stream`; nothing allocates or frees on the hot path (workspaces are
+ * caller-owned, sized by the *_workspace_bytes functions, zero-filled once before first use).
+ * Every function returns a collm_status; the message of the last failure on the calling thread is
+ * available from collm_last_error().  The error classes mirror the reference's exceptions:
+ * COLLM_EINVAL -> ConfigurationError (domain.py:15-16), COLLM_EINTERNAL -> InvariantViolation
+ * (domain.py:19-20), COLLM_ECUDA -> RuntimeError.  No function aborts the process.
+ */
+#ifndef COLLM_H_
+#define COLLM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  COLLM_OK = 0,
+  COLLM_EINVAL = 1,       /* bad shape / rank / segment table: ConfigurationError */
+  COLLM_EINTERNAL = 2,    /* internal invariant broken: InvariantViolation */
+  COLLM_ECUDA = 3,        /* CUDA runtime/driver error */
+  COLLM_EUNSUPPORTED = 4, /* not an sm_100 device, or a configuration this build does not cover */
+} collm_status;
+
+enum { COLLM_MODE_STORE_GRAD = 0, COLLM_MODE_ADAMW = 1, COLLM_MODE_COPY_ONLY = 2 };
+
+/* ---- library / device --------------------------------------------------------------------- */
+int collm_version(void);
+const char* collm_last_error(void);
+/* Fills compute capability and SM count; COLLM_EUNSUPPORTED unless sm_100. */
+int collm_device_info(int device, int* sm_major, int* sm_minor, int* num_sms);
+
+/* ---- K0: batch composition (host planning + device expansion) -------------------------------
+ * Segment table of the mixed batch: rows [seg_start[s], seg_start[s+1]) use adapter
+ * seg_adapter[s] (-1 = base model only).  Replaces domain.Batch (domain.py:64-86), which may not
+ * mix streams (domain.py:75-77).
+ *
+ * collm_plan_segments (HOST, pure CPU): per 128-row tile the distinct adapters in order of first
+ * appearance (tile_slot_ptr[n_tiles+1], slot_adapter[n_slots]) — the LoRA "slots" the GEMM folds
+ * into its accumulator — and the shrink work list: segments cut into <=16-row tiles
+ * (shrink_tiles[3*i] = row_start, n_rows, adapter).  Capacities are checked (COLLM_EINVAL). */
+int collm_plan_segments(const int32_t* seg_start, const int32_t* seg_adapter, int n_seg,
+                        int n_rows, int32_t* tile_slot_ptr, int32_t* slot_adapter, int slot_cap,
+                        int32_t* n_slots, int32_t* shrink_tiles, int shrink_tile_cap,
+                        int32_t* n_shrink_tiles);
+
+/* DEVICE: row_adapter[t], slot_of_row[t] (either may be NULL). */
+int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, int n_seg,
+                          int n_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
+                          int32_t* row_adapter, int32_t* slot_of_row, void* stream);
+
+/* ---- K1: LoRA shrink (SGMV) ------------------------------------------------------------------
+ * H[t, g.rank_off + j] = scale[a] * sum_{k in [g.k_lo, g.k_hi)} X[t,k] * A[a][g.rank_off + j, k]
+ * for each shrink tile (rows of one adapter a) and each rank group g (groups: n_groups x 4 ints
+ * rank_off, n_ranks (multiple of 8, <= 64), k_lo, k_hi).  Outputs (each optional): H32 fp32
+ * [T, ldh]; H16 bf16 [T, ldh]; Hslots bf16 [n_slots*128, ldh], row slot_of_row[t]*128 + t%128
+ * (the caller zero-fills Hslots first: rows of other adapters stay zero).  `ksplit` >= 1 splits K
+ * across CTAs with a deterministic ordered reduction through `workspace`. */
+size_t collm_shrink_workspace_bytes(int n_tiles, int n_groups, int ksplit);
+int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
+                      const int32_t* tiles, int n_tiles, const float* scale, const int32_t* groups,
+                      int n_groups, int ksplit, float* H32, void* H16, int ldh, void* Hslots,
+                      const int32_t* slot_of_row, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- K2 / K3: base projection on tcgen05 with the LoRA expand fused into the accumulator ------
+ * Y[M,N] = A[M,K] . B[N,K]^T + sum over the LoRA slots s of each 128-row tile of
+ *          Hslots[s*128 : s*128+128, hcol(n) : hcol(n)+lora_rank] . LB[a(s)*lb_rows_per_adapter + n,
+ *          0 : lora_rank]^T,
+ * hcol(n) = sub_h_col[i] for the sub-projection i with sub_n_start[i] <= n < sub_n_start[i+1].
+ * Pass tile_slot_ptr = NULL for a plain GEMM.  lora_rank a multiple of 16.  bn = 0 picks the
+ * N tile (128/256).  Requirements: K, N, lda, ldb, ldy, ldh, ld_lb multiples of 8; 16-byte aligned
+ * pointers; sub-projection boundaries multiples of the N tile.
+ * Forward: A = X, B = W [N,K], Hslots from collm_lora_shrink, LB = adapters' B [n_ad*N, r].
+ * Backward dX: A = dY, B = W^T [K_in, N], Hslots = s*dY.B_t [T_tr, R] with one slot per tile,
+ *              LB = A_t^T [K_in, R]. */
+int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int ldy, int M, int N,
+                    int K, const void* Hslots, int ldh, int h_rows, const void* LB, int ld_lb,
+                    int lb_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
+                    int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
+                    const int32_t* sub_h_col, int bn, void* stream);
+
+/* ---- K5: LoRA weight-gradient reduction with fused AdamW --------------------------------------
+ * C[p,q] = sum_t U[t, g.u_off+p] * V[t, g.v_off+q] for each group g (groups: n_groups x 8 ints
+ * u_off, P, v_off, Q, c_row_off, c_col_off, t_row_off, t_col_off; Q <= 64; P, Q multiples of 8).
+ * Element (p,q) of group g lives at fp32 index (c_row_off+p)*ldc + c_col_off+q of grad / master /
+ * m / v and of out_same (bf16), and at (t_row_off+q)*ld_trans + t_col_off+p of out_trans (bf16).
+ * mode STORE_GRAD: grad = C*grad_scale (+grad if accum_in).  mode ADAMW: the same gradient drives
+ * an AdamW step (adamw = {lr, beta1, beta2, eps, weight_decay, 1-beta1^step, 1-beta2^step},
+ * PyTorch semantics) on master/m/v and the bf16 copies are rewritten.  Deterministic. */
+size_t collm_reduce_workspace_bytes(const int32_t* groups, int n_groups, int tsplit);
+int collm_lora_reduce(const void* U, int ldu, const void* V, int ldv, int T,
+                      const int32_t* groups, int n_groups, int mode, int accum_in,
+                      float grad_scale, float* grad, int ldc, float* master, float* m, float* v,
+                      void* out_same, void* out_trans, int ld_trans, const float* adamw,
+                      int tsplit, void* workspace, size_t ws_bytes, void* stream);
+/* Elementwise update over the same group table from `grad` (mode ADAMW, e.g. after a cross-
+ * replica gradient allreduce) or master -> bf16 copies only (mode COPY_ONLY, after fedavg). */
+int collm_lora_apply(const int32_t* groups, int n_groups, int mode, float* grad, int ldc,
+                     float* master, float* m, float* v, void* out_same, void* out_trans,
+                     int ld_trans, const float* adamw, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COLLM_H_ */

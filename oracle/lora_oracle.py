@@ -1,0 +1,230 @@
+"""numpy restatement of the unified PEFT layer — TEST INFRASTRUCTURE ONLY (see __init__.py).
+
+Every function restates one step of the algorithm the device path implements, with the same
+bf16 rounding points (inputs, the rank-space intermediates H = s.X.A^T and dH = s.dY.B, and the
+bf16 working copies of the adapter) and exact (float64) arithmetic everywhere else, so the device
+result must agree up to fp32 summation order and one rounding of the outputs.
+
+Reference anchors (/root/reference):
+  * adapter layout  b_mat (d, r), a_mat (r, l), update = b_mat @ a_mat ... pkg/src/coserve/launcher.py:28-47
+  * LoRA on a frozen W_pre, FedAvg of B and A separately .................. PAPER.md:359-366
+  * fedavg semantics (identity for 1 client, AggregationError naming client) launcher.py:68-80
+  * batch composition (replaced: single-stream Batch) ...................... domain.py:64-86
+  * AdamW: the HF Trainer default optimizer; the paper keeps .backward() ... PAPER.md:578
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "bf16_round", "bf16_to_bits", "bits_to_f32", "build_rows", "expand_segments", "tile_slots",
+    "slot_of_row", "shrink_tiles", "lora_forward", "lora_backward", "adamw_step", "AdamWState",
+    "fedavg", "AggregationError", "projection_flops",
+]
+
+
+# --------------------------------------------------------------------------- bf16 helpers
+def bf16_to_bits(x: np.ndarray) -> np.ndarray:
+    """float32 -> bf16 bit pattern, round-to-nearest-even (NaN kept quiet)."""
+    f = np.ascontiguousarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    rounded = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    nan = np.isnan(f)
+    out = rounded.astype(np.uint16)
+    out[nan] = 0x7FC0
+    return out
+
+
+def bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Values of x rounded to bf16 (returned as float32)."""
+    return bits_to_f32(bf16_to_bits(np.asarray(x, dtype=np.float32)))
+
+
+# --------------------------------------------------------------------------- K0: rows/segments
+def build_rows(train, items):
+    """Row table of one mixed pass.
+
+    train: None or (adapter, n_rows).  items: iterable of (request_id, adapter, n_rows, role).
+    Rows = training rows first, then inference rows ordered by (adapter, request_id); segments are
+    maximal runs of equal (adapter, role).  Returns (seg_start, seg_adapter, seg_role, row_request,
+    row_pos) as python lists.
+    """
+    rows = []  # (adapter, role, request, pos)
+    if train is not None:
+        ad, n = train
+        rows += [(ad, 0, -1, i) for i in range(n)]
+    for rid, ad, n, role in sorted(items, key=lambda it: (it[1], it[0])):
+        rows += [(ad, int(role), rid, i) for i in range(n)]
+    seg_start, seg_adapter, seg_role = [0], [], []
+    for i, (ad, role, _, _) in enumerate(rows):
+        if i == 0 or (ad, role) != (rows[i - 1][0], rows[i - 1][1]):
+            if i:
+                seg_start.append(i)
+            seg_adapter.append(ad)
+            seg_role.append(role)
+    seg_start.append(len(rows))
+    return (seg_start, seg_adapter, seg_role, [r[2] for r in rows], [r[3] for r in rows])
+
+
+def expand_segments(seg_start, seg_adapter) -> np.ndarray:
+    out = np.empty(seg_start[-1], dtype=np.int32)
+    for s, a in enumerate(seg_adapter):
+        out[seg_start[s]:seg_start[s + 1]] = a
+    return out
+
+
+def tile_slots(row_adapter: np.ndarray, tile_m: int = 128):
+    """Distinct adapters (>= 0) of each tile_m-row tile, in order of first appearance."""
+    ptr, slots = [0], []
+    for m0 in range(0, len(row_adapter), tile_m):
+        seen = []
+        for a in row_adapter[m0:m0 + tile_m].tolist():
+            if a >= 0 and a not in seen:
+                seen.append(a)
+        slots += seen
+        ptr.append(len(slots))
+    return np.array(ptr, np.int32), np.array(slots, np.int32)
+
+
+def slot_of_row(row_adapter, tile_slot_ptr, slot_adapter, tile_m: int = 128) -> np.ndarray:
+    out = np.full(len(row_adapter), -1, np.int32)
+    for t, a in enumerate(row_adapter.tolist()):
+        if a < 0:
+            continue
+        m = t // tile_m
+        for s in range(tile_slot_ptr[m], tile_slot_ptr[m + 1]):
+            if slot_adapter[s] == a:
+                out[t] = s
+                break
+    return out
+
+
+def shrink_tiles(seg_start, seg_adapter, tile: int = 16) -> np.ndarray:
+    out = []
+    for s, a in enumerate(seg_adapter):
+        if a < 0:
+            continue
+        for r in range(seg_start[s], seg_start[s + 1], tile):
+            out.append((r, min(tile, seg_start[s + 1] - r), a))
+    return np.array(out, np.int32).reshape(-1, 3)
+
+
+# --------------------------------------------------------------------------- projection fwd/bwd
+def _sub_bounds(sub_sizes):
+    b = [0]
+    for n in sub_sizes:
+        b.append(b[-1] + n)
+    return b
+
+
+def lora_forward(X, W, A, B, scale, row_adapter, sub_sizes, r_pad):
+    """Forward of one (possibly fused) LoRA projection over the mixed rows.
+
+    X [T, K], W [N, K] (N = sum(sub_sizes)), A [n_ad, R, K] (R = n_sub * r_pad; rank rows of sub s
+    at s*r_pad), B [n_ad, N, r_pad], scale [n_ad]; all float32 holding bf16 values.
+      H16[t]     = bf16(scale[a] * X[t] . A[a]^T)                       (a = row_adapter[t] >= 0)
+      Y[t, n_s]  = X[t] . W[n_s]^T + H16[t, s*r_pad:(s+1)*r_pad] . B[a][n_s]^T
+    Returns Y (float64, before the output rounding) and H16 (float32 bf16 values; 0 for a < 0).
+    """
+    X64 = X.astype(np.float64)
+    T = X.shape[0]
+    bounds = _sub_bounds(sub_sizes)
+    R = len(sub_sizes) * r_pad
+    Y = X64 @ W.astype(np.float64).T
+    H16 = np.zeros((T, R), np.float32)
+    for a in np.unique(row_adapter):
+        if a < 0:
+            continue
+        rows = np.nonzero(row_adapter == a)[0]
+        H = float(scale[a]) * (X64[rows] @ A[a].astype(np.float64).T)
+        H16[rows] = bf16_round(H.astype(np.float32))
+        for s in range(len(sub_sizes)):
+            cols = slice(bounds[s], bounds[s + 1])
+            Y[np.ix_(rows, np.arange(bounds[s], bounds[s + 1]))] += (
+                H16[rows, s * r_pad:(s + 1) * r_pad].astype(np.float64)
+                @ B[a][cols].astype(np.float64).T)
+    return Y, H16
+
+
+def lora_backward(dY, X_tr, H16_tr, W, A_t, B_t, s, sub_sizes, r_pad):
+    """Backward of the training rows (all on adapter t, scale s) through one projection.
+
+      dH16[:, sub s] = bf16(s * dY[:, n_s] . B_t[n_s])
+      dX             = dY . W + dH16 . A_t
+      dB[n_s]        = dY[:, n_s]^T . H16_tr[:, sub s]            ([N, r_pad], B_t's layout)
+      dA^T           = X_tr^T . dH16                              ([K, R], A_t^T's layout)
+    (d/dW of the frozen base is not formed.)  Returns float64 dX, dB, dAT and float32 dH16.
+    """
+    bounds = _sub_bounds(sub_sizes)
+    dY64 = dY.astype(np.float64)
+    T = dY.shape[0]
+    R = len(sub_sizes) * r_pad
+    dH16 = np.zeros((T, R), np.float32)
+    dB = np.zeros((bounds[-1], r_pad))
+    for si in range(len(sub_sizes)):
+        ns = slice(bounds[si], bounds[si + 1])
+        rs = slice(si * r_pad, (si + 1) * r_pad)
+        dH = s * (dY64[:, ns] @ B_t[ns].astype(np.float64))
+        dH16[:, rs] = bf16_round(dH.astype(np.float32))
+        dB[ns] = dY64[:, ns].T @ H16_tr[:, rs].astype(np.float64)
+    dX = dY64 @ W.astype(np.float64) + dH16.astype(np.float64) @ A_t.astype(np.float64)
+    dAT = X_tr.astype(np.float64).T @ dH16.astype(np.float64)
+    return dX, dB, dAT, dH16
+
+
+def projection_flops(T, T_tr, K, N):
+    """Algorithmic tensor-pipe FLOPs of one projection per step: forward of all rows + dX of the
+    training rows (the frozen base has no dW) — SURVEY.md §8(d)."""
+    return 2 * K * N * (T + T_tr)
+
+
+# --------------------------------------------------------------------------- optimizer
+@dataclass
+class AdamWState:
+    m: np.ndarray
+    v: np.ndarray
+    step: int = 0
+
+
+def adamw_step(p, g, st: AdamWState, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.0):
+    """torch.optim.AdamW (single-tensor path) in float32: decoupled weight decay, bias-corrected."""
+    p = p.astype(np.float32).copy()
+    g = g.astype(np.float32)
+    st.step += 1
+    p *= np.float32(1.0 - lr * wd)
+    st.m = (st.m + (g - st.m) * np.float32(1.0 - beta1)).astype(np.float32)
+    st.v = (st.v * np.float32(beta2) + np.float32(1.0 - beta2) * g * g).astype(np.float32)
+    bc1 = 1.0 - beta1 ** st.step
+    bc2 = 1.0 - beta2 ** st.step
+    denom = np.sqrt(st.v) / np.float32(math.sqrt(bc2)) + np.float32(eps)
+    p -= np.float32(lr / bc1) * st.m / denom
+    return p
+
+
+# --------------------------------------------------------------------------- FedAvg
+class AggregationError(ValueError):
+    pass
+
+
+def fedavg(clients):
+    """Element-wise mean of B and of A, separately (launcher.py:68-80).  ``clients`` is a list of
+    (b_mat, a_mat).  One client returns that client's arrays unchanged (launcher.py:76-77); a
+    shape mismatch raises AggregationError naming the client index (launcher.py:73-75)."""
+    if not clients:
+        raise AggregationError("no adapters to aggregate")
+    b0, a0 = clients[0]
+    for idx, (b, a) in enumerate(clients):
+        if b.shape != b0.shape or a.shape != a0.shape:
+            raise AggregationError(f"client {idx} adapter dimensions do not match the first client")
+    if len(clients) == 1:
+        return b0, a0
+    return (np.mean(np.stack([c[0] for c in clients]), axis=0),
+            np.mean(np.stack([c[1] for c in clients]), axis=0))

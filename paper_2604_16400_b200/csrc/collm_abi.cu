@@ -1,0 +1,495 @@
+// collm_abi.cu — the C ABI (include/collm.h): argument validation, host-side planning, TMA
+// descriptor encoding and kernel launches.  Built with
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared -Xcompiler -fPIC
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/collm.h"
+#include "common.cuh"
+#include "gemm_lora.cuh"
+#include "reduce_adamw.cuh"
+#include "segments.cuh"
+#include "shrink.cuh"
+
+using namespace collm;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      return fail(COLLM_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e),     \
+                  __FILE__, __LINE__);                                              \
+  } while (0)
+
+#define CHECK_ARG(cond, ...)                        \
+  do {                                              \
+    if (!(cond)) return fail(COLLM_EINVAL, __VA_ARGS__); \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int num_sms_cached() {
+  static int n = -1;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (n < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  }
+  return n;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2D bf16 tensor map over a row-major [rows, cols] matrix with leading dimension ld (elements).
+int make_tmap(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld,
+              uint32_t box_cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(COLLM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMapSwizzle sw;
+  switch (box_cols * 2) {
+    case 128: sw = CU_TENSOR_MAP_SWIZZLE_128B; break;
+    case 64: sw = CU_TENSOR_MAP_SWIZZLE_64B; break;
+    case 32: sw = CU_TENSOR_MAP_SWIZZLE_32B; break;
+    default: return fail(COLLM_EINTERNAL, "unsupported TMA box width %u", box_cols);
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(COLLM_ECUDA, "cuTensorMapEncodeTiled failed (%d): cols=%llu rows=%llu ld=%llu",
+                (int)r, (unsigned long long)cols, (unsigned long long)rows,
+                (unsigned long long)ld);
+  return COLLM_OK;
+}
+
+template <int BN, int STAGES>
+int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& th,
+                const CUtensorMap& tlb, const GemmLoraParams& p, cudaStream_t stream) {
+  using L = GemmSmem<BN, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
+    configured = true;
+  }
+  const int tiles = p.num_m_tiles * p.num_n_tiles;
+  const int grid = std::min(tiles, num_sms_cached());
+  gemm_lora_kernel<BN, STAGES><<<grid, 256, L::kTotal, stream>>>(ta, tb, th, tlb, p);
+  CUDA_TRY(cudaGetLastError());
+  return COLLM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int collm_version(void) { return 1; }
+
+const char* collm_last_error(void) { return g_err; }
+
+int collm_device_info(int device, int* sm_major, int* sm_minor, int* num_sms) {
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (sm_major) *sm_major = prop.major;
+  if (sm_minor) *sm_minor = prop.minor;
+  if (num_sms) *num_sms = prop.multiProcessorCount;
+  if (prop.major != 10)
+    return fail(COLLM_EUNSUPPORTED, "collm is built for sm_100a; device %d is sm_%d%d", device,
+                prop.major, prop.minor);
+  return COLLM_OK;
+}
+
+// ------------------------------------------------------------------------------------ K0 host
+int collm_plan_segments(const int32_t* seg_start, const int32_t* seg_adapter, int n_seg,
+                        int n_rows, int32_t* tile_slot_ptr, int32_t* slot_adapter, int slot_cap,
+                        int32_t* n_slots, int32_t* shrink_tiles, int shrink_tile_cap,
+                        int32_t* n_shrink_tiles) {
+  CHECK_ARG(n_seg >= 1 && n_rows >= 1, "empty segment table (n_seg=%d, n_rows=%d)", n_seg, n_rows);
+  CHECK_ARG(seg_start[0] == 0 && seg_start[n_seg] == n_rows,
+            "segment table must cover rows [0, %d): starts at %d, ends at %d", n_rows,
+            seg_start[0], seg_start[n_seg]);
+  for (int s = 0; s < n_seg; ++s)
+    CHECK_ARG(seg_start[s + 1] > seg_start[s], "segment %d is empty or unsorted", s);
+  const int n_tiles = (n_rows + kGemmBM - 1) / kGemmBM;
+  int ns = 0;
+  int seg = 0;
+  for (int m = 0; m < n_tiles; ++m) {
+    if (tile_slot_ptr) tile_slot_ptr[m] = ns;
+    const int r0 = m * kGemmBM, r1 = std::min(n_rows, r0 + kGemmBM);
+    while (seg_start[seg + 1] <= r0) ++seg;
+    const int first = ns;
+    for (int s = seg; s < n_seg && seg_start[s] < r1; ++s) {
+      const int a = seg_adapter[s];
+      if (a < 0) continue;
+      bool dup = false;
+      for (int i = first; i < ns; ++i)
+        if (slot_adapter[i] == a) { dup = true; break; }
+      if (dup) continue;
+      CHECK_ARG(ns < slot_cap, "slot capacity %d exceeded", slot_cap);
+      slot_adapter[ns++] = a;
+    }
+  }
+  if (tile_slot_ptr) tile_slot_ptr[n_tiles] = ns;
+  if (n_slots) *n_slots = ns;
+  int nt = 0;
+  for (int s = 0; s < n_seg; ++s) {
+    if (seg_adapter[s] < 0) continue;
+    for (int r = seg_start[s]; r < seg_start[s + 1]; r += 16) {
+      CHECK_ARG(nt < shrink_tile_cap, "shrink tile capacity %d exceeded", shrink_tile_cap);
+      if (shrink_tiles) {
+        shrink_tiles[3 * nt + 0] = r;
+        shrink_tiles[3 * nt + 1] = std::min(16, seg_start[s + 1] - r);
+        shrink_tiles[3 * nt + 2] = seg_adapter[s];
+      }
+      ++nt;
+    }
+  }
+  if (n_shrink_tiles) *n_shrink_tiles = nt;
+  return COLLM_OK;
+}
+
+int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, int n_seg,
+                          int n_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
+                          int32_t* row_adapter, int32_t* slot_of_row, void* stream) {
+  CHECK_ARG(n_seg >= 1 && n_rows >= 1, "empty segment table");
+  CHECK_ARG(!slot_of_row || (tile_slot_ptr && slot_adapter), "slot_of_row needs the tile slots");
+  expand_segments_kernel<<<(n_rows + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      seg_start, seg_adapter, n_seg, n_rows, tile_slot_ptr, slot_adapter, row_adapter,
+      slot_of_row);
+  CUDA_TRY(cudaGetLastError());
+  return COLLM_OK;
+}
+
+// ------------------------------------------------------------------------------------ K1
+// Workspace layout shared by the split reductions: [kCounterCap int32 arrival counters][fp32
+// partials].  Counters sit at a fixed prefix so that any launch (whatever its split factor or
+// tile count) finds them zero — kernels restore them to zero, and partials never overlap them.
+constexpr size_t kCounterCap = 1 << 16;
+constexpr size_t kCounterBytes = kCounterCap * sizeof(int32_t);
+
+size_t collm_shrink_workspace_bytes(int n_tiles, int n_groups, int ksplit) {
+  if (ksplit <= 1) return 0;
+  return kCounterBytes + (size_t)ksplit * n_groups * n_tiles * 16 * 64 * sizeof(float);
+}
+
+int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
+                      const int32_t* tiles, int n_tiles, const float* scale, const int32_t* groups,
+                      int n_groups, int ksplit, float* H32, void* H16, int ldh, void* Hslots,
+                      const int32_t* slot_of_row, void* workspace, size_t ws_bytes,
+                      void* stream) {
+  CHECK_ARG(X && A && tiles && scale && groups, "null input");
+  CHECK_ARG(n_tiles >= 0, "n_tiles < 0");
+  if (n_tiles == 0) return COLLM_OK;
+  CHECK_ARG(n_groups >= 1 && n_groups <= kShrinkMaxGroups, "n_groups=%d out of [1,%d]", n_groups,
+            kShrinkMaxGroups);
+  CHECK_ARG(ksplit >= 1 && ksplit <= 64, "ksplit=%d out of [1,64]", ksplit);
+  CHECK_ARG(ldx % 8 == 0 && lda % 8 == 0 && a_stride % 8 == 0, "ldx/lda/a_stride must be x8");
+  CHECK_ARG(aligned16(X) && aligned16(A), "X/A must be 16-byte aligned");
+  CHECK_ARG(!Hslots || slot_of_row, "Hslots needs slot_of_row");
+  ShrinkParams p{};
+  p.X = (const bf16*)X;
+  p.ldx = ldx;
+  p.Amat = (const bf16*)A;
+  p.a_stride = a_stride;
+  p.lda = lda;
+  p.tiles = tiles;
+  p.n_tiles = n_tiles;
+  p.scale = scale;
+  p.n_groups = n_groups;
+  int max_ranks = 0;
+  for (int g = 0; g < n_groups; ++g) {
+    ShrinkGroup sg{groups[4 * g], groups[4 * g + 1], groups[4 * g + 2], groups[4 * g + 3]};
+    CHECK_ARG(sg.n_ranks > 0 && sg.n_ranks <= 64 && sg.n_ranks % 8 == 0,
+              "group %d: n_ranks=%d must be a multiple of 8 in [8,64]", g, sg.n_ranks);
+    CHECK_ARG(sg.k_lo >= 0 && sg.k_hi > sg.k_lo && sg.k_lo % 8 == 0 && sg.k_hi % 8 == 0,
+              "group %d: K range [%d,%d) must be non-empty and 8-aligned", g, sg.k_lo, sg.k_hi);
+    CHECK_ARG(sg.rank_off >= 0 && sg.rank_off + sg.n_ranks <= ldh,
+              "group %d: ranks [%d,%d) exceed ldh=%d", g, sg.rank_off, sg.rank_off + sg.n_ranks,
+              ldh);
+    p.groups[g] = sg;
+    max_ranks = std::max(max_ranks, sg.n_ranks);
+  }
+  p.ksplit = ksplit;
+  p.H32 = H32;
+  p.H16 = (bf16*)H16;
+  p.ldh = ldh;
+  p.Hslots = (bf16*)Hslots;
+  p.slot_of_row = slot_of_row;
+  if (ksplit > 1) {
+    const size_t need = collm_shrink_workspace_bytes(n_tiles, n_groups, ksplit);
+    CHECK_ARG(workspace && ws_bytes >= need, "shrink workspace too small: %zu < %zu", ws_bytes,
+              need);
+    CHECK_ARG((size_t)n_groups * n_tiles <= kCounterCap, "too many shrink tiles (%d)", n_tiles);
+    p.counters = (int32_t*)workspace;
+    p.partials = (float*)((char*)workspace + kCounterBytes);
+  }
+  dim3 grid(n_tiles, n_groups, ksplit);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (max_ranks <= 16)
+    lora_shrink_kernel<2><<<grid, kShrinkWarps * 32, 0, st>>>(p);
+  else if (max_ranks <= 32)
+    lora_shrink_kernel<4><<<grid, kShrinkWarps * 32, 0, st>>>(p);
+  else
+    lora_shrink_kernel<8><<<grid, kShrinkWarps * 32, 0, st>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  return COLLM_OK;
+}
+
+// ------------------------------------------------------------------------------------ K2/K3
+int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int ldy, int M, int N,
+                    int K, const void* Hslots, int ldh, int h_rows, const void* LB, int ld_lb,
+                    int lb_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
+                    int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
+                    const int32_t* sub_h_col, int bn, void* stream) {
+  CHECK_ARG(A && B && Y, "null operand");
+  CHECK_ARG(M >= 1 && N >= 1 && K >= 1, "empty GEMM M=%d N=%d K=%d", M, N, K);
+  CHECK_ARG(K % 8 == 0 && N % 8 == 0, "K=%d and N=%d must be multiples of 8", K, N);
+  CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0 && ldy % 8 == 0 && lda >= K && ldb >= K && ldy >= N,
+            "bad leading dimensions lda=%d ldb=%d ldy=%d", lda, ldb, ldy);
+  CHECK_ARG(aligned16(A) && aligned16(B) && aligned16(Y), "operands must be 16-byte aligned");
+  const bool lora = tile_slot_ptr != nullptr;
+  if (n_sub <= 0) n_sub = 1;
+  CHECK_ARG(n_sub <= kMaxSub, "n_sub=%d > %d", n_sub, kMaxSub);
+
+  // N tile: sub-projection boundaries must be tile aligned; prefer the better-filled wave
+  const int sms = num_sms_cached();
+  auto aligned_to = [&](int t) {
+    if (!lora || !sub_n_start) return true;
+    for (int i = 1; i < n_sub; ++i)
+      if (sub_n_start[i] % t) return false;
+    return true;
+  };
+  const int nm = (M + kGemmBM - 1) / kGemmBM;
+  if (bn == 0) {
+    auto eff = [&](int t) {
+      const int tiles = nm * ((N + t - 1) / t);
+      const int waves = (tiles + sms - 1) / sms;
+      // useful fraction: real columns / padded columns times SM occupancy of the waves
+      const double col_eff = (double)N / (((N + t - 1) / t) * t);
+      return col_eff * (double)tiles / (waves * sms) * (t == 256 ? 1.0 : 0.93);
+    };
+    const bool ok256 = aligned_to(256), ok128 = aligned_to(128);
+    if (ok256 && (!ok128 || eff(256) >= eff(128))) bn = 256;
+    else if (ok128) bn = 128;
+    else return fail(COLLM_EINVAL, "sub-projection boundaries are not multiples of 128");
+  }
+  CHECK_ARG(bn == 128 || bn == 256, "bn must be 0, 128 or 256");
+  CHECK_ARG(aligned_to(bn), "sub-projection boundaries are not multiples of bn=%d", bn);
+
+  GemmLoraParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.Y = (bf16*)Y;
+  p.ldy = ldy;
+  p.num_m_tiles = nm;
+  p.num_n_tiles = (N + bn - 1) / bn;
+  p.n_sub = n_sub;
+  p.sub_n_start[0] = 0;
+  for (int i = 0; i <= kMaxSub; ++i) p.sub_n_start[i] = (i == 0) ? 0 : N;
+  for (int i = 0; i < kMaxSub; ++i) p.sub_h_col[i] = 0;
+
+  CUtensorMap ta, tb, th, tlb;
+  int rc = make_tmap(&ta, A, K, M, lda, kGemmBK, kGemmBM);
+  if (rc) return rc;
+  rc = make_tmap(&tb, B, K, N, ldb, kGemmBK, bn);
+  if (rc) return rc;
+  if (lora) {
+    CHECK_ARG(Hslots && LB && slot_adapter, "LoRA GEMM needs Hslots, LB and slot_adapter");
+    CHECK_ARG(lora_rank > 0 && lora_rank % 16 == 0, "lora_rank=%d must be a multiple of 16",
+              lora_rank);
+    CHECK_ARG(ldh % 8 == 0 && ld_lb % 8 == 0 && aligned16(Hslots) && aligned16(LB),
+              "Hslots/LB must be 16-byte aligned with x8 leading dimensions");
+    CHECK_ARG(h_rows >= 1 && lb_rows >= 1, "empty Hslots/LB");
+    // widest TMA/UMMA chunk (64/32/16 columns = 128/64/32-byte swizzle) dividing the LoRA width
+    const int lrc = (lora_rank % 64 == 0) ? 64 : (lora_rank % 32 == 0) ? 32 : 16;
+    p.tile_slot_ptr = tile_slot_ptr;
+    p.slot_adapter = slot_adapter;
+    p.lora_rc = lrc;
+    p.lora_chunks = lora_rank / lrc;
+    p.lb_rows_per_adapter = lb_rows_per_adapter;
+    if (sub_n_start) {
+      CHECK_ARG(sub_n_start[0] == 0 && sub_n_start[n_sub] == N, "sub_n_start must span [0, N)");
+      for (int i = 0; i <= n_sub; ++i) p.sub_n_start[i] = sub_n_start[i];
+      for (int i = n_sub + 1; i <= kMaxSub; ++i) p.sub_n_start[i] = N;
+    }
+    for (int i = 0; i < n_sub; ++i) {
+      p.sub_h_col[i] = sub_h_col ? sub_h_col[i] : 0;
+      CHECK_ARG(p.sub_h_col[i] % 8 == 0 && p.sub_h_col[i] + lora_rank <= ldh,
+                "sub %d: H columns [%d,%d) exceed ldh=%d", i, p.sub_h_col[i],
+                p.sub_h_col[i] + lora_rank, ldh);
+    }
+    CHECK_ARG(lora_rank <= ld_lb, "lora_rank %d exceeds LB width %d", lora_rank, ld_lb);
+    rc = make_tmap(&th, Hslots, ldh, h_rows, ldh, lrc, kGemmBM);
+    if (rc) return rc;
+    rc = make_tmap(&tlb, LB, ld_lb, lb_rows, ld_lb, lrc, bn);
+    if (rc) return rc;
+  } else {
+    th = ta;
+    tlb = tb;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (bn == 256) return launch_gemm<256, 4>(ta, tb, th, tlb, p, st);
+  return launch_gemm<128, 6>(ta, tb, th, tlb, p, st);
+}
+
+// ------------------------------------------------------------------------------------ K5
+static int build_reduce_params(ReduceParams& p, const int32_t* groups, int n_groups, int& qmax) {
+  CHECK_ARG(groups && n_groups >= 1 && n_groups <= kReduceMaxGroups, "n_groups=%d out of [1,%d]",
+            n_groups, kReduceMaxGroups);
+  p.n_groups = n_groups;
+  int tiles = 0;
+  qmax = 0;
+  for (int g = 0; g < n_groups; ++g) {
+    const int32_t* r = groups + 8 * g;
+    ReduceGroup gr{r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], tiles};
+    CHECK_ARG(gr.P > 0 && gr.P % 8 == 0 && gr.Q > 0 && gr.Q % 8 == 0 && gr.Q <= 64,
+              "group %d: P=%d, Q=%d (need multiples of 8, Q <= 64)", g, gr.P, gr.Q);
+    CHECK_ARG(gr.u_off % 8 == 0 && gr.v_off % 8 == 0, "group %d: offsets must be x8", g);
+    p.groups[g] = gr;
+    tiles += (gr.P + 63) / 64;
+    qmax = std::max(qmax, gr.Q);
+  }
+  p.n_tiles = tiles;
+  return COLLM_OK;
+}
+
+size_t collm_reduce_workspace_bytes(const int32_t* groups, int n_groups, int tsplit) {
+  if (tsplit <= 1 || !groups) return 0;
+  int tiles = 0;
+  for (int g = 0; g < n_groups; ++g) tiles += (groups[8 * g + 1] + 63) / 64;
+  return kCounterBytes + (size_t)tsplit * tiles * 64 * 64 * sizeof(float);
+}
+
+static void fill_opt(ReduceParams& p, const float* adamw) {
+  if (adamw) {
+    p.opt.lr = adamw[0];
+    p.opt.beta1 = adamw[1];
+    p.opt.beta2 = adamw[2];
+    p.opt.eps = adamw[3];
+    p.opt.weight_decay = adamw[4];
+    p.opt.bc1 = adamw[5];
+    p.opt.bc2 = adamw[6];
+  }
+}
+
+int collm_lora_reduce(const void* U, int ldu, const void* V, int ldv, int T,
+                      const int32_t* groups, int n_groups, int mode, int accum_in,
+                      float grad_scale, float* grad, int ldc, float* master, float* m, float* v,
+                      void* out_same, void* out_trans, int ld_trans, const float* adamw,
+                      int tsplit, void* workspace, size_t ws_bytes, void* stream) {
+  CHECK_ARG(U && V, "null operand");
+  CHECK_ARG(T >= 1, "T=%d", T);
+  CHECK_ARG(ldu % 8 == 0 && ldv % 8 == 0 && aligned16(U) && aligned16(V),
+            "U/V must be 16-byte aligned with x8 leading dimensions");
+  CHECK_ARG(mode == COLLM_MODE_STORE_GRAD || mode == COLLM_MODE_ADAMW, "bad mode %d", mode);
+  CHECK_ARG(mode != COLLM_MODE_STORE_GRAD || grad, "STORE_GRAD needs grad");
+  CHECK_ARG(!accum_in || grad, "accum_in needs grad");
+  CHECK_ARG(mode != COLLM_MODE_ADAMW || (master && m && v && adamw), "ADAMW needs master/m/v");
+  CHECK_ARG(tsplit >= 1 && tsplit <= 128, "tsplit=%d", tsplit);
+  ReduceParams p{};
+  int qmax = 0;
+  int rc = build_reduce_params(p, groups, n_groups, qmax);
+  if (rc) return rc;
+  p.U = (const bf16*)U;
+  p.ldu = ldu;
+  p.V = (const bf16*)V;
+  p.ldv = ldv;
+  p.T = T;
+  p.tsplit = tsplit;
+  p.mode = mode;
+  p.accum_in = accum_in;
+  p.grad_scale = grad_scale;
+  p.grad = grad;
+  p.ldc = ldc;
+  p.master = master;
+  p.m = m;
+  p.v = v;
+  p.out_same = (bf16*)out_same;
+  p.out_trans = (bf16*)out_trans;
+  p.ld_trans = ld_trans;
+  fill_opt(p, adamw);
+  if (tsplit > 1) {
+    const size_t need = collm_reduce_workspace_bytes(groups, n_groups, tsplit);
+    CHECK_ARG(workspace && ws_bytes >= need, "reduce workspace too small: %zu < %zu", ws_bytes,
+              need);
+    CHECK_ARG((size_t)p.n_tiles <= kCounterCap, "too many reduce tiles (%d)", p.n_tiles);
+    p.counters = (int32_t*)workspace;
+    p.partials = (float*)((char*)workspace + kCounterBytes);
+  }
+  dim3 grid(p.n_tiles, tsplit);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (qmax <= 16) lora_reduce_kernel<16><<<grid, 128, 0, st>>>(p);
+  else if (qmax <= 32) lora_reduce_kernel<32><<<grid, 128, 0, st>>>(p);
+  else lora_reduce_kernel<64><<<grid, 128, 0, st>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  return COLLM_OK;
+}
+
+int collm_lora_apply(const int32_t* groups, int n_groups, int mode, float* grad, int ldc,
+                     float* master, float* m, float* v, void* out_same, void* out_trans,
+                     int ld_trans, const float* adamw, void* stream) {
+  CHECK_ARG(mode == COLLM_MODE_ADAMW || mode == COLLM_MODE_COPY_ONLY, "bad mode %d", mode);
+  CHECK_ARG(master, "null master");
+  CHECK_ARG(mode != COLLM_MODE_ADAMW || (grad && m && v && adamw), "ADAMW needs grad/m/v");
+  ReduceParams p{};
+  int qmax = 0;
+  int rc = build_reduce_params(p, groups, n_groups, qmax);
+  if (rc) return rc;
+  p.mode = mode;
+  p.accum_in = 1;
+  p.grad_scale = 1.f;
+  p.grad = grad;
+  p.ldc = ldc;
+  p.master = master;
+  p.m = m;
+  p.v = v;
+  p.out_same = (bf16*)out_same;
+  p.out_trans = (bf16*)out_trans;
+  p.ld_trans = ld_trans;
+  fill_opt(p, adamw);
+  long long total = 0;
+  for (int g = 0; g < n_groups; ++g) total += (long long)p.groups[g].P * p.groups[g].Q;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 4LL * num_sms_cached());
+  lora_apply_kernel<<<std::max(blocks, 1), 256, 0, (cudaStream_t)stream>>>(p, total);
+  CUDA_TRY(cudaGetLastError());
+  return COLLM_OK;
+}
+
+}  // extern "C"

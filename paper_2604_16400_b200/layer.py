@@ -1,0 +1,306 @@
+"""The unified PEFT projection: one LoRA-augmented linear layer serving a mixed row batch.
+
+``LoraProjection`` owns the frozen base weight of one (optionally fused: q|k|v, gate|up)
+projection, the adapter registry slice for it (every tenant's A/B), and the trainable adapter's
+optimizer state.  Its ``forward`` / ``backward`` are the hot path:
+
+  forward (all rows)   : K1 shrink  H = s_a . X . A_a^T  -> per-tile LoRA slot blocks
+                         K2 tcgen05 GEMM  Y = X . W^T + sum_slots H_slot . B_a^T   (one write of Y)
+  backward (train rows): K1 shrink  dH = s . dY . B_t           (one rank group per sub-projection)
+                         K3 tcgen05 GEMM  dX = dY . W + dH . A_t  (W^T kept resident)
+                         K5 reductions dB = dY^T . H, dA^T = X^T . dH with fused AdamW
+
+Adapter layout follows the reference (`AdapterParams`, /root/reference/pkg/src/coserve/
+launcher.py:28-47): b_mat (d, r) = (out, rank), a_mat (r, l) = (rank, in); dW = b_mat @ a_mat;
+scale s_a = lora_alpha / r per adapter.  Ranks are zero-padded to r_pad (a multiple of 16) so the
+rank dimension is a whole number of tensor-core K-steps; padding contributes exact zeros.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib, ops
+from .domain import ConfigurationError
+from .segments import TILE_M, DevicePlan, HostPlan
+
+
+def pad_rank(r: int) -> int:
+    if r < 1:
+        raise ConfigurationError(f"LoRA rank must be >= 1, got {r}")
+    return 16 * math.ceil(r / 16)
+
+
+@dataclass(frozen=True)
+class ProjectionSpec:
+    """Shape of one (fused) projection: ``subs`` are the output widths of the fused members."""
+
+    name: str
+    in_features: int
+    subs: tuple[int, ...]
+    rank: int
+    alpha: float
+
+    @property
+    def out_features(self) -> int:
+        return sum(self.subs)
+
+    @property
+    def r_pad(self) -> int:
+        return pad_rank(self.rank)
+
+    @property
+    def R(self) -> int:
+        return len(self.subs) * self.r_pad
+
+    @property
+    def sub_bounds(self) -> list[int]:
+        b = [0]
+        for n in self.subs:
+            b.append(b[-1] + n)
+        return b
+
+
+@dataclass
+class AdamWConfig:
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+
+    def args(self, step: int) -> list[float]:
+        return [self.lr, self.beta1, self.beta2, self.eps, self.weight_decay,
+                1.0 - self.beta1 ** step, 1.0 - self.beta2 ** step]
+
+
+@dataclass
+class TrainState:
+    """fp32 master copies + AdamW moments of the trainable adapter, in the layouts the gradient
+    reductions produce (B: [N, r_pad]; A^T: [K, R]), plus the extra bf16 layouts the backward
+    kernels read (A^T for dX, B^T for dH)."""
+
+    adapter: int
+    master_B: torch.Tensor
+    master_AT: torch.Tensor
+    m_B: torch.Tensor
+    v_B: torch.Tensor
+    m_AT: torch.Tensor
+    v_AT: torch.Tensor
+    grad_B: torch.Tensor
+    grad_AT: torch.Tensor
+    AT16: torch.Tensor
+    BT16: torch.Tensor
+    step: int = 0
+
+
+@dataclass
+class ForwardCache:
+    """What backward needs from forward: the training rows' input and rank-space activations."""
+
+    X: torch.Tensor
+    H16: torch.Tensor
+    n_train: int
+
+
+class LoraProjection:
+    def __init__(self, spec: ProjectionSpec, n_adapters: int, device: torch.device | str = "cuda",
+                 weight: torch.Tensor | None = None, keep_transpose: bool = True):
+        self.spec = spec
+        self.n_adapters = n_adapters
+        self.device = torch.device(device)
+        K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
+        for v, what in ((K, "in_features"), (N, "out_features")):
+            if v % 8:
+                raise ConfigurationError(f"{spec.name}: {what}={v} must be a multiple of 8")
+        self.W = (weight if weight is not None else
+                  torch.empty(N, K, dtype=torch.bfloat16, device=self.device))
+        self.WT = torch.empty(K, N, dtype=torch.bfloat16, device=self.device) if keep_transpose else None
+        self.A = torch.zeros(n_adapters, R, K, dtype=torch.bfloat16, device=self.device)
+        self.B = torch.zeros(n_adapters, N, rp, dtype=torch.bfloat16, device=self.device)
+        self.scale = torch.zeros(n_adapters, dtype=torch.float32, device=self.device)
+        self.train_state: TrainState | None = None
+        self._H16: torch.Tensor | None = None
+        self._Hslots: torch.Tensor | None = None
+
+    # ------------------------------------------------------------------ weights / registry
+    def refresh_transpose(self) -> None:
+        if self.WT is not None:
+            self.WT.copy_(self.W.t())
+
+    def set_adapter(self, slot: int, b_mats, a_mats, alpha: float | None = None) -> None:
+        """Load adapter ``slot`` from per-sub (b_mat (d_s, r), a_mat (r, K)) pairs — the
+        reference's AdapterParams layout (launcher.py:28-33)."""
+        spec = self.spec
+        if len(b_mats) != len(spec.subs) or len(a_mats) != len(spec.subs):
+            raise ConfigurationError(f"{spec.name}: expected {len(spec.subs)} (b, a) pairs")
+        r, rp = spec.rank, spec.r_pad
+        bnd = spec.sub_bounds
+        self.A[slot].zero_()
+        self.B[slot].zero_()
+        for s, (b, a) in enumerate(zip(b_mats, a_mats)):
+            b = torch.as_tensor(b)
+            a = torch.as_tensor(a)
+            if tuple(b.shape) != (spec.subs[s], r) or tuple(a.shape) != (r, spec.in_features):
+                raise ConfigurationError(
+                    f"{spec.name}[{s}]: adapter dimensions {tuple(b.shape)}/{tuple(a.shape)} do "
+                    f"not match ({spec.subs[s]}, {r})/({r}, {spec.in_features})")
+            self.A[slot, s * rp:s * rp + r] = a.to(self.device, torch.bfloat16)
+            self.B[slot, bnd[s]:bnd[s + 1], :r] = b.to(self.device, torch.bfloat16)
+        self.scale[slot] = (alpha if alpha is not None else spec.alpha) / r
+
+    def get_adapter(self, slot: int):
+        """Inverse of set_adapter: per-sub (b_mat (d_s, r), a_mat (r, K)) float32 CPU tensors."""
+        spec = self.spec
+        r, rp = spec.rank, spec.r_pad
+        bnd = spec.sub_bounds
+        return [(self.B[slot, bnd[s]:bnd[s + 1], :r].float().cpu(),
+                 self.A[slot, s * rp:s * rp + r].float().cpu()) for s in range(len(spec.subs))]
+
+    def make_trainable(self, slot: int) -> TrainState:
+        """Start fine-tuning adapter ``slot``: fp32 masters from its current bf16 weights."""
+        K, N, R, rp = self.spec.in_features, self.spec.out_features, self.spec.R, self.spec.r_pad
+        if self.WT is None:
+            raise ConfigurationError(f"{self.spec.name}: training needs the resident W^T copy")
+        dev = self.device
+        mB = self.B[slot].float().contiguous()
+        mAT = self.A[slot].float().t().contiguous()
+        z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)  # noqa: E731
+        st = TrainState(adapter=slot, master_B=mB, master_AT=mAT, m_B=z(N, rp), v_B=z(N, rp),
+                        m_AT=z(K, R), v_AT=z(K, R), grad_B=z(N, rp), grad_AT=z(K, R),
+                        AT16=self.A[slot].t().contiguous(),
+                        BT16=torch.zeros(R, N, dtype=torch.bfloat16, device=dev))
+        bnd = self.spec.sub_bounds
+        for s in range(len(self.spec.subs)):
+            st.BT16[s * rp:(s + 1) * rp, bnd[s]:bnd[s + 1]] = self.B[slot, bnd[s]:bnd[s + 1]].t()
+        self.train_state = st
+        return st
+
+    # ------------------------------------------------------------------ buffers
+    def _buffers(self, T: int, n_slots: int):
+        R = self.spec.R
+        if self._H16 is None or self._H16.shape[0] < T:
+            self._H16 = torch.zeros(T, R, dtype=torch.bfloat16, device=self.device)
+        rows = max(1, n_slots) * TILE_M
+        if self._Hslots is None or self._Hslots.shape[0] < rows:
+            self._Hslots = torch.zeros(rows, R, dtype=torch.bfloat16, device=self.device)
+        return self._H16, self._Hslots
+
+    # ------------------------------------------------------------------ hot path
+    def forward(self, X: torch.Tensor, plan: DevicePlan, Y: torch.Tensor | None = None,
+                n_train: int = 0) -> tuple[torch.Tensor, ForwardCache]:
+        spec = self.spec
+        T = plan.n_rows
+        if X.shape[0] < T or X.shape[1] != spec.in_features:
+            raise ConfigurationError(f"{spec.name}: X {tuple(X.shape)} vs T={T}, K={spec.in_features}")
+        if Y is None:
+            Y = torch.empty(T, spec.out_features, dtype=torch.bfloat16, device=self.device)
+        H16, Hslots = self._buffers(T, plan.n_slots)
+        R, rp, K = spec.R, spec.r_pad, spec.in_features
+        if plan.n_slots:
+            Hs = Hslots[: plan.n_slots * TILE_M]
+            Hs.zero_()
+            groups = [(g, min(64, R - g), 0, K) for g in range(0, R, 64)]
+            ops.lora_shrink(X, self.A, plan.shrink_tiles, plan.n_shrink_tiles, self.scale, groups,
+                            R, H16=H16, Hslots=Hs, slot_of_row=plan.slot_of_row)
+            bnd = spec.sub_bounds
+            ops.gemm_lora(X, self.W, Y, M=T, Hslots=Hs, h_rows=Hs.shape[0],
+                          LB=self.B.view(self.n_adapters * spec.out_features, rp),
+                          lb_rows=self.n_adapters * spec.out_features,
+                          tile_slot_ptr=plan.tile_slot_ptr, slot_adapter=plan.slot_adapter,
+                          lora_rank=rp, lb_rows_per_adapter=spec.out_features, sub_n_start=bnd,
+                          sub_h_col=[s * rp for s in range(len(spec.subs))])
+        else:
+            ops.gemm_lora(X, self.W, Y, M=T)
+        return Y, ForwardCache(X=X, H16=H16, n_train=n_train)
+
+    def backward(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan,
+                 dX: torch.Tensor | None = None, *, optimizer: AdamWConfig | None = None,
+                 accumulate: bool = False, grad_scale: float = 1.0,
+                 need_dx: bool = True) -> torch.Tensor | None:
+        """Backward of the training rows [0, n_train).  ``optimizer`` given -> fused AdamW step
+        (after adding the gradient already accumulated when ``accumulate``); otherwise the
+        gradient is stored (or added, ``accumulate``) into the grad buffers, e.g. for a
+        cross-replica allreduce followed by :meth:`apply_optimizer`."""
+        st = self.train_state
+        if st is None:
+            raise ConfigurationError(f"{self.spec.name}: no trainable adapter (make_trainable)")
+        spec = self.spec
+        Ttr = cache.n_train
+        if Ttr <= 0:
+            return None
+        K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
+        bnd = spec.sub_bounds
+        dH16 = torch.empty(Ttr, R, dtype=torch.bfloat16, device=self.device)
+        # K1: dH = s * dY . B_t, one rank group per sub-projection (its own N range)
+        groups = [(s * rp + g, min(64, rp - g), bnd[s], bnd[s + 1])
+                  for s in range(len(spec.subs)) for g in range(0, rp, 64)]
+        ops.lora_shrink(dY, st.BT16, train_plan.shrink_tiles, train_plan.n_shrink_tiles,
+                        self.scale, groups, R, a_stride=0, H16=dH16)
+        # K3: dX = dY . W + dH . A_t
+        if need_dx:
+            if dX is None:
+                dX = torch.empty(Ttr, K, dtype=torch.bfloat16, device=self.device)
+            ops.gemm_lora(dY, self.WT, dX, M=Ttr, Hslots=dH16, h_rows=Ttr, LB=st.AT16, lb_rows=K,
+                          tile_slot_ptr=train_plan.tile_slot_ptr,
+                          slot_adapter=train_plan.slot_adapter, lora_rank=R,
+                          lb_rows_per_adapter=0)
+        # K5: dB = dY^T . H16 (per sub), dA^T = X^T . dH16 — fused AdamW or grad store
+        X_tr = cache.X[:Ttr]
+        H_tr = cache.H16[:Ttr]
+        gB = [(bnd[s], spec.subs[s], s * rp, rp, bnd[s], 0, s * rp, bnd[s])
+              for s in range(len(spec.subs))]
+        gA = [(0, K, q, min(64, R - q), 0, q, q, 0) for q in range(0, R, 64)]
+        if optimizer is not None:
+            st.step += 1
+            args = optimizer.args(st.step)
+            ops.lora_reduce(dY, H_tr, Ttr, gB, _lib.MODE_ADAMW, accum_in=accumulate,
+                            grad_scale=grad_scale, grad=st.grad_B, ldc=rp, master=st.master_B,
+                            m=st.m_B, v=st.v_B, out_same=self.B[st.adapter], out_trans=st.BT16,
+                            ld_trans=N, adamw=args)
+            ops.lora_reduce(X_tr, dH16, Ttr, gA, _lib.MODE_ADAMW, accum_in=accumulate,
+                            grad_scale=grad_scale, grad=st.grad_AT, ldc=R, master=st.master_AT,
+                            m=st.m_AT, v=st.v_AT, out_same=st.AT16, out_trans=self.A[st.adapter],
+                            ld_trans=K, adamw=args)
+        else:
+            ops.lora_reduce(dY, H_tr, Ttr, gB, _lib.MODE_STORE_GRAD, accum_in=accumulate,
+                            grad_scale=grad_scale, grad=st.grad_B, ldc=rp)
+            ops.lora_reduce(X_tr, dH16, Ttr, gA, _lib.MODE_STORE_GRAD, accum_in=accumulate,
+                            grad_scale=grad_scale, grad=st.grad_AT, ldc=R)
+        return dX
+
+    def apply_optimizer(self, optimizer: AdamWConfig) -> None:
+        """AdamW from the grad buffers (after a cross-replica allreduce of the gradients)."""
+        st = self.train_state
+        spec = self.spec
+        K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
+        bnd = spec.sub_bounds
+        st.step += 1
+        args = optimizer.args(st.step)
+        gB = [(bnd[s], spec.subs[s], s * rp, rp, bnd[s], 0, s * rp, bnd[s])
+              for s in range(len(spec.subs))]
+        gA = [(0, K, q, min(64, R - q), 0, q, q, 0) for q in range(0, R, 64)]
+        ops.lora_apply(gB, _lib.MODE_ADAMW, ldc=rp, master=st.master_B, grad=st.grad_B, m=st.m_B,
+                       v=st.v_B, out_same=self.B[st.adapter], out_trans=st.BT16, ld_trans=N,
+                       adamw=args)
+        ops.lora_apply(gA, _lib.MODE_ADAMW, ldc=R, master=st.master_AT, grad=st.grad_AT,
+                       m=st.m_AT, v=st.v_AT, out_same=st.AT16, out_trans=self.A[st.adapter],
+                       ld_trans=K, adamw=args)
+
+    def refresh_from_master(self) -> None:
+        """Rewrite every bf16 copy of the trainable adapter from the fp32 masters (after a
+        parameter average across replicas — the reference's fedavg, launcher.py:68-80)."""
+        st = self.train_state
+        spec = self.spec
+        K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
+        bnd = spec.sub_bounds
+        gB = [(bnd[s], spec.subs[s], s * rp, rp, bnd[s], 0, s * rp, bnd[s])
+              for s in range(len(spec.subs))]
+        gA = [(0, K, q, min(64, R - q), 0, q, q, 0) for q in range(0, R, 64)]
+        ops.lora_apply(gB, _lib.MODE_COPY_ONLY, ldc=rp, master=st.master_B,
+                       out_same=self.B[st.adapter], out_trans=st.BT16, ld_trans=N)
+        ops.lora_apply(gA, _lib.MODE_COPY_ONLY, ldc=R, master=st.master_AT, out_same=st.AT16,
+                       out_trans=self.A[st.adapter], ld_trans=K)

@@ -1,0 +1,161 @@
+"""Typed torch-tensor wrappers over the collm C ABI (one function per ABI entry point).
+
+Torch is plumbing here (device memory, streams); every computation is a collm kernel.  Each
+wrapper validates dtypes/devices, picks the split factors, and launches on the current stream.
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+
+import torch
+
+from . import _lib
+
+NUM_SMS_DEFAULT = 148
+_sms_cache: dict[int, int] = {}
+
+
+def num_sms(device: torch.device | None = None) -> int:
+    d = (device or torch.device("cuda")).index or 0
+    if d not in _sms_cache:
+        _sms_cache[d] = torch.cuda.get_device_properties(d).multi_processor_count
+    return _sms_cache[d]
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _p(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
+    if t.dtype != dtype or not t.is_cuda:
+        raise TypeError(f"{name}: expected a CUDA {dtype} tensor, got {t.dtype} on {t.device}")
+    if t.stride(-1) != 1:
+        raise TypeError(f"{name}: innermost dimension must be contiguous")
+
+
+class Workspace:
+    """Grow-only, zero-initialised scratch for the split-K / split-T ordered reductions.
+
+    The kernels restore their arrival counters to zero, so the buffer stays valid across launches
+    and CUDA-graph replays.  Size it (call once outside capture) before capturing a graph."""
+
+    def __init__(self) -> None:
+        self._bufs: dict[int, torch.Tensor] = {}
+        self._lock = threading.Lock()
+
+    def get(self, nbytes: int, device: torch.device) -> torch.Tensor | None:
+        if nbytes <= 0:
+            return None
+        d = device.index or 0
+        with self._lock:
+            buf = self._bufs.get(d)
+            if buf is None or buf.numel() < nbytes:
+                if torch.cuda.is_current_stream_capturing():
+                    raise RuntimeError("collm workspace must be sized before CUDA graph capture")
+                nb = max(nbytes, 1 << 20)
+                buf = torch.zeros(nb, dtype=torch.uint8, device=device)
+                self._bufs[d] = buf
+            return buf
+
+
+_shrink_ws = Workspace()
+_reduce_ws = Workspace()
+
+
+def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: int,
+                scale: torch.Tensor, groups: list[tuple[int, int, int, int]], ldh: int, *,
+                a_stride: int | None = None, H32: torch.Tensor | None = None,
+                H16: torch.Tensor | None = None, Hslots: torch.Tensor | None = None,
+                slot_of_row: torch.Tensor | None = None, ksplit: int | None = None) -> None:
+    """K1: H[t, ranks of g] = scale[a] * X[t, K-range of g] . A_a[ranks of g]^T (see collm.h)."""
+    _need(X, torch.bfloat16, "X")
+    _need(A, torch.bfloat16, "A")
+    if n_tiles == 0:
+        return
+    lda = A.stride(-2)
+    if a_stride is None:
+        a_stride = A.stride(0) if A.dim() == 3 else 0
+    if ksplit is None:
+        steps = max(math.ceil((g[3] - g[2]) / 32) for g in groups)
+        want = math.ceil(2 * num_sms(X.device) / (n_tiles * len(groups)))
+        ksplit = max(1, min(want, steps // 8, 32))
+    ws_bytes = _lib.load().collm_shrink_workspace_bytes(n_tiles, len(groups), ksplit)
+    ws = _shrink_ws.get(ws_bytes, X.device)
+    flat = [v for g in groups for v in g]
+    _lib.call("collm_lora_shrink", X.data_ptr(), X.stride(0), A.data_ptr(), int(a_stride), lda,
+              tiles.data_ptr(), n_tiles, scale.data_ptr(), _lib.int_array(flat), len(groups),
+              ksplit, _p(H32), _p(H16), ldh, _p(Hslots), _p(slot_of_row), _p(ws),
+              0 if ws is None else ws.numel(), _stream())
+
+
+def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | None = None,
+              Hslots: torch.Tensor | None = None, h_rows: int = 0, LB: torch.Tensor | None = None,
+              lb_rows: int = 0, tile_slot_ptr: torch.Tensor | None = None,
+              slot_adapter: torch.Tensor | None = None, lora_rank: int = 0,
+              lb_rows_per_adapter: int = 0, sub_n_start: list[int] | None = None,
+              sub_h_col: list[int] | None = None, bn: int = 0) -> None:
+    """K2/K3: Y[M,N] = A[M,K] . B[N,K]^T (+ fused multi-adapter LoRA expand), bf16 -> bf16."""
+    for t, n in ((A, "A"), (B, "B"), (Y, "Y")):
+        _need(t, torch.bfloat16, n)
+    M = A.shape[0] if M is None else M
+    K = A.shape[1]
+    N = B.shape[0]
+    if B.shape[1] != K or Y.shape[1] < N or Y.shape[0] < M:
+        raise ValueError(f"gemm_lora shapes: A {tuple(A.shape)} B {tuple(B.shape)} Y {tuple(Y.shape)}")
+    lora = tile_slot_ptr is not None
+    n_sub = len(sub_n_start) - 1 if (lora and sub_n_start) else 1
+    _lib.call(
+        "collm_gemm_lora", A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), Y.data_ptr(),
+        Y.stride(0), M, N, K,
+        _p(Hslots) if lora else None, Hslots.stride(0) if lora else 0, h_rows,
+        _p(LB) if lora else None, LB.stride(-2) if lora else 0, lb_rows,
+        _p(tile_slot_ptr), _p(slot_adapter), lora_rank, lb_rows_per_adapter, n_sub,
+        _lib.int_array(sub_n_start) if (lora and sub_n_start) else None,
+        _lib.int_array(sub_h_col) if (lora and sub_h_col) else None, bn, _stream())
+
+
+def reduce_tsplit(T: int, n_tiles: int, device: torch.device) -> int:
+    chunks = math.ceil(T / 32)
+    want = math.ceil(2 * num_sms(device) / max(1, n_tiles))
+    return max(1, min(want, chunks // 2, 64))
+
+
+def lora_reduce(U: torch.Tensor, V: torch.Tensor, T: int, groups: list[tuple], mode: int, *,
+                accum_in: bool = False, grad_scale: float = 1.0,
+                grad: torch.Tensor | None = None, ldc: int = 0,
+                master: torch.Tensor | None = None, m: torch.Tensor | None = None,
+                v: torch.Tensor | None = None, out_same: torch.Tensor | None = None,
+                out_trans: torch.Tensor | None = None, ld_trans: int = 0,
+                adamw: list[float] | None = None, tsplit: int | None = None) -> None:
+    """K5: C = U^T V per group -> grad store or fused AdamW (see collm.h)."""
+    _need(U, torch.bfloat16, "U")
+    _need(V, torch.bfloat16, "V")
+    flat = [v_ for g in groups for v_ in g]
+    garr = _lib.int_array(flat)
+    if tsplit is None:
+        n_tiles = sum(math.ceil(g[1] / 64) for g in groups)
+        tsplit = reduce_tsplit(T, n_tiles, U.device)
+    ws_bytes = _lib.load().collm_reduce_workspace_bytes(garr, len(groups), tsplit)
+    ws = _reduce_ws.get(ws_bytes, U.device)
+    _lib.call("collm_lora_reduce", U.data_ptr(), U.stride(0), V.data_ptr(), V.stride(0), T, garr,
+              len(groups), mode, int(accum_in), float(grad_scale), _p(grad), ldc, _p(master),
+              _p(m), _p(v), _p(out_same), _p(out_trans), ld_trans,
+              _lib.float_array(adamw) if adamw else None, tsplit, _p(ws),
+              0 if ws is None else ws.numel(), _stream())
+
+
+def lora_apply(groups: list[tuple], mode: int, *, ldc: int, master: torch.Tensor,
+               grad: torch.Tensor | None = None, m: torch.Tensor | None = None,
+               v: torch.Tensor | None = None, out_same: torch.Tensor | None = None,
+               out_trans: torch.Tensor | None = None, ld_trans: int = 0,
+               adamw: list[float] | None = None) -> None:
+    flat = [v_ for g in groups for v_ in g]
+    _lib.call("collm_lora_apply", _lib.int_array(flat), len(groups), mode, _p(grad), ldc,
+              master.data_ptr(), _p(m), _p(v), _p(out_same), _p(out_trans), ld_trans,
+              _lib.float_array(adamw) if adamw else None, _stream())

@@ -1,0 +1,159 @@
+"""Kernel-level numerics on the B200: each collm kernel against a plain PyTorch fp32 computation
+of the same op on the same bf16 inputs (the layer-level parity against the oracle is in
+test_gpu_parity.py).  Tolerances: bf16 outputs |err| <= 1e-2*max|ref| + 1e-3 (one bf16 rounding
+of the output plus fp32 summation-order differences); fp32 outputs rel. Frobenius <= 1e-4."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf(*shape, scale=1.0, gen=None):
+    return (torch.randn(*shape, generator=gen) * scale).to(torch.bfloat16).cuda()
+
+
+def _close_bf16(out, ref):
+    err = (out.float() - ref).abs().max().item()
+    tol = 1e-2 * ref.abs().max().item() + 1e-3
+    assert err <= tol, f"max err {err} > tol {tol}"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def lib():
+    from paper_2604_16400_b200 import _lib, build
+    build.build()
+    return _lib.load()
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (200, 384, 320, 0), (77, 136, 200, 128),
+                                      (1024, 4096, 4096, 0), (512, 1024, 12288, 128),
+                                      (300, 688, 256, 128)])
+def test_gemm_plain(M, N, K, bn):
+    from paper_2604_16400_b200 import ops
+    g = torch.Generator().manual_seed(M * 7 + N)
+    A = _bf(M, K, gen=g)
+    B = _bf(N, K, scale=0.05, gen=g)
+    Y = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    ops.gemm_lora(A, B, Y, bn=bn)
+    torch.cuda.synchronize()
+    _close_bf16(Y, A.float() @ B.float().t())
+
+
+@pytest.mark.parametrize("r_pad,n_sub,bn", [(16, 1, 256), (16, 3, 128), (32, 1, 128), (64, 2, 256),
+                                            (48, 1, 128)])
+def test_gemm_lora_slots(r_pad, n_sub, bn):
+    """Forward-style LoRA K-extension: multiple slots per tile, per-sub H column offsets."""
+    from paper_2604_16400_b200 import ops
+    g = torch.Generator().manual_seed(r_pad * 31 + n_sub)
+    M, K = 300, 256
+    n_each = 256 if bn == 256 else 128
+    N = n_each * n_sub
+    n_ad = 5
+    R = r_pad * n_sub
+    A = _bf(M, K, gen=g)
+    W = _bf(N, K, scale=0.05, gen=g)
+    # tile slots: tile0 adapters [0, 3], tile1 [3, 1, 4], tile2 [2]
+    row_ad = torch.tensor([0] * 100 + [3] * 60 + [1] * 50 + [4] * 46 + [2] * 44, dtype=torch.int32)
+    tiles_adapters = []
+    for m in range(math.ceil(M / 128)):
+        seen = []
+        for a in row_ad[m * 128:(m + 1) * 128].tolist():
+            if a not in seen:
+                seen.append(a)
+        tiles_adapters.append(seen)
+    tsp = [0]
+    slots = []
+    for s in tiles_adapters:
+        slots += s
+        tsp.append(len(slots))
+    H = torch.randn(M, R, generator=g).to(torch.bfloat16)
+    Hslots = torch.zeros(len(slots) * 128, R, dtype=torch.bfloat16)
+    for t in range(M):
+        m = t // 128
+        s = tsp[m] + tiles_adapters[m].index(int(row_ad[t]))
+        Hslots[s * 128 + t % 128] = H[t]
+    LB = (torch.randn(n_ad, N, r_pad, generator=g) * 0.1).to(torch.bfloat16)
+    Y = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    sub_n = [i * n_each for i in range(n_sub + 1)]
+    sub_h = [i * r_pad for i in range(n_sub)]
+    ops.gemm_lora(A, W, Y, Hslots=Hslots.cuda(), h_rows=Hslots.shape[0],
+                  LB=LB.cuda().view(n_ad * N, r_pad), lb_rows=n_ad * N,
+                  tile_slot_ptr=torch.tensor(tsp, dtype=torch.int32).cuda(),
+                  slot_adapter=torch.tensor(slots, dtype=torch.int32).cuda(), lora_rank=r_pad,
+                  lb_rows_per_adapter=N, sub_n_start=sub_n, sub_h_col=sub_h, bn=bn)
+    torch.cuda.synchronize()
+    ref = A.float().cpu() @ W.float().cpu().t()
+    for t in range(M):
+        a = int(row_ad[t])
+        for s in range(n_sub):
+            cols = slice(sub_n[s], sub_n[s + 1])
+            ref[t, cols] += H[t, sub_h[s]:sub_h[s] + r_pad].float() @ LB[a, cols].float().t()
+    _close_bf16(Y.cpu(), ref)
+
+
+@pytest.mark.parametrize("R,ksplit", [(16, 1), (48, 3), (64, 4), (32, None)])
+def test_shrink(R, ksplit):
+    from paper_2604_16400_b200 import ops
+    g = torch.Generator().manual_seed(R)
+    T, K, n_ad = 150, 512, 4
+    X = _bf(T, K, gen=g)
+    A = _bf(n_ad, R, K, scale=0.05, gen=g)
+    scale = torch.tensor([1.0, 2.0, 0.5, 3.0]).cuda()
+    seg = [0, 40, 41, 90, 150]
+    seg_ad = [2, 0, 3, 1]
+    tiles = []
+    for s in range(len(seg_ad)):
+        for r in range(seg[s], seg[s + 1], 16):
+            tiles.append((r, min(16, seg[s + 1] - r), seg_ad[s]))
+    tt = torch.tensor(tiles, dtype=torch.int32).cuda()
+    groups = [(i, min(64, R - i), 0, K) for i in range(0, R, 64)]
+    H32 = torch.zeros(T, R, device="cuda")
+    H16 = torch.zeros(T, R, dtype=torch.bfloat16, device="cuda")
+    ops.lora_shrink(X, A, tt, len(tiles), scale, groups, R, H32=H32, H16=H16, ksplit=ksplit)
+    torch.cuda.synchronize()
+    ref = torch.zeros(T, R)
+    for s in range(len(seg_ad)):
+        a = seg_ad[s]
+        rows = slice(seg[s], seg[s + 1])
+        ref[rows] = scale[a].item() * (X[rows].float().cpu() @ A[a].float().cpu().t())
+    rel = (H32.cpu() - ref).norm() / ref.norm()
+    assert rel < 1e-4, rel
+    _close_bf16(H16.cpu(), ref)
+
+
+def test_reduce_adamw():
+    from paper_2604_16400_b200 import _lib, ops
+    g = torch.Generator().manual_seed(5)
+    T, P, Q = 300, 200, 48
+    U = _bf(T, P + 8, gen=g)
+    V = _bf(T, Q + 16, gen=g)
+    groups = [(8, P, 16, Q, 0, 0, 0, 0)]
+    grad = torch.zeros(P, Q, device="cuda")
+    ops.lora_reduce(U, V, T, groups, _lib.MODE_STORE_GRAD, grad=grad, ldc=Q)
+    torch.cuda.synchronize()
+    ref = U[:, 8:8 + P].float().t() @ V[:, 16:16 + Q].float()
+    rel = ((grad - ref).norm() / ref.norm()).item()
+    assert rel < 1e-5, rel
+    # fused AdamW from the same reduction, deterministic across runs
+    master = torch.randn(P, Q, generator=g).cuda()
+    m = torch.zeros_like(master)
+    v = torch.zeros_like(master)
+    same = torch.empty(P, Q, dtype=torch.bfloat16, device="cuda")
+    trans = torch.empty(Q, P, dtype=torch.bfloat16, device="cuda")
+    lr, b1, b2, eps, wd = 1e-3, 0.9, 0.999, 1e-8, 0.01
+    p_ref = master.clone()
+    ops.lora_reduce(U, V, T, groups, _lib.MODE_ADAMW, ldc=Q, master=master, m=m, v=v,
+                    out_same=same, out_trans=trans, ld_trans=P,
+                    adamw=[lr, b1, b2, eps, wd, 1 - b1, 1 - b2])
+    torch.cuda.synchronize()
+    gr = ref.cuda()
+    p_ref.mul_(1 - lr * wd)
+    m_ref = (1 - b1) * gr
+    v_ref = (1 - b2) * gr * gr
+    p_ref -= (lr / (1 - b1)) * m_ref / (v_ref.sqrt() / math.sqrt(1 - b2) + eps)
+    assert torch.allclose(master, p_ref, rtol=1e-5, atol=1e-6)
+    assert torch.equal(same, master.to(torch.bfloat16))
+    assert torch.equal(trans, master.to(torch.bfloat16).t())
