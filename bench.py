@@ -1,0 +1,464 @@
+#!/usr/bin/env python
+"""bench.py — co-batched LoRA fwd+bwd throughput of the B200 unified PEFT layer stack.
+
+One "step" = one mixed pass of BASELINE config 2 (Llama-2-7B shape: 32 adapters r=16 serving 512
+inference rows + a 1x512 fine-tuning micro-batch) through all 32 layers x 7 LoRA-augmented
+projections (q|k|v and gate|up fused): forward of every row, backward (dX, dH, dA, dB) of the
+training rows and the fused AdamW step.  `value` is whole-job rows/s with inputs resident in HBM
+(CUDA-graph replay timed with CUDA events, max over ranks); `e2e` adds, every step, the host->
+device copy of the pass inputs (layer-0 hidden state, top output grad, segment tables, optimizer
+args) and the device->host read of the final hidden state.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config llama2-7b] [--impl reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank is an independent replica of the same
+config ("weak" scaling); the only collective is the NCCL allreduce (average) of the shared
+training adapter's LoRA gradients each step, followed by the AdamW apply kernels.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "co-batched LoRA fwd+bwd tokens/s/GPU at Llama-2-7B; % of tensor-pipe peak"
+UNIT = "tokens/s"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="llama2-7b")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph (debug)")
+    return ap.parse_args(argv)
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+# --------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.sw_power_cap",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown"]
+    REASONS = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self._t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(self.REASONS, parts[3:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------------- CPU side
+def cpu_layer_sample(cfg, seed: int = 0) -> dict:
+    """Time the CPU oracle (numpy) on ONE layer of the config — every projection's forward over
+    all mixed rows, backward of the training rows and the AdamW step — and extrapolate to all
+    layers.  This is the 'reference CPU path' (the reference has no LoRA arithmetic)."""
+    import numpy as np
+
+    import oracle
+    from paper_2604_16400_b200.segments import build_mixed_batch
+
+    train, items = cfg.batch(seed)
+    mb = build_mixed_batch(train, items)
+    T, Ttr = mb.n_rows, mb.n_train_rows
+    row_ad = oracle.expand_segments(list(mb.seg_start), list(mb.seg_adapter))
+    g = np.random.Generator(np.random.PCG64(seed))
+    n_ad = cfg.n_adapters
+    data = []
+    for sp in cfg.projections:
+        K, N, rp, R = sp.in_features, sp.out_features, sp.r_pad, sp.R
+        used = sorted({a for a in mb.seg_adapter if a >= 0})
+        A = np.zeros((n_ad, R, K), np.float32)
+        B = np.zeros((n_ad, N, rp), np.float32)
+        for a in used:
+            A[a] = 0.01 * g.standard_normal((R, K), dtype=np.float32)
+            B[a] = 0.02 * g.standard_normal((N, rp), dtype=np.float32)
+        data.append(dict(
+            sp=sp, X=g.standard_normal((T, K), dtype=np.float32),
+            W=0.02 * g.standard_normal((N, K), dtype=np.float32), A=A, B=B,
+            scale=np.full(n_ad, sp.alpha / sp.rank, np.float32),
+            dY=g.standard_normal((Ttr, N), dtype=np.float32)))
+
+    def one_layer():
+        for d in data:
+            sp = d["sp"]
+            Y, H16 = oracle.lora_forward(d["X"], d["W"], d["A"], d["B"], d["scale"], row_ad,
+                                         sp.subs, sp.r_pad)
+            if Ttr:
+                t = mb.train_adapter
+                dX, dB, dAT, _ = oracle.lora_backward(
+                    d["dY"], d["X"][:Ttr], H16[:Ttr], d["W"], d["A"][t], d["B"][t],
+                    float(d["scale"][t]), sp.subs, sp.r_pad)
+                for p, gr in ((d["B"][t], dB), (d["A"][t].T, dAT)):
+                    st = oracle.AdamWState(np.zeros_like(p), np.zeros_like(p))
+                    oracle.adamw_step(p, gr.astype(np.float32), st)
+
+    return {"fn": one_layer, "rows": T, "layers": cfg.model.layers}
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def time_cpu_sample(cfg, repeats: int = 1) -> dict:
+    s = cpu_layer_sample(cfg)
+    s["fn"]()  # warm
+    ts = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        s["fn"]()
+        ts.append(time.perf_counter() - t0)
+    t_layer = statistics.median(ts)
+    step_s = t_layer * s["layers"]
+    return {"value": s["rows"] / step_s, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+            "sample": (f"numpy float64 oracle (oracle/lora_oracle.py), 1 of {s['layers']} layers "
+                       f"(all projections fwd over {s['rows']} rows + training bwd + AdamW), "
+                       f"{t_layer:.2f} s/layer, extrapolated x{s['layers']}"),
+            "seconds_per_layer": t_layer}
+
+
+def run_reference(args, cfg, workload):
+    """--impl reference: the CPU oracle port timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np  # noqa: F401
+    s = cpu_layer_sample(cfg, args.seed)
+    for _ in range(args.warmup):
+        s["fn"]()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        s["fn"]()
+        ts.append(time.perf_counter() - t0)
+    t_layer = sum(ts) / len(ts)
+    step_s = t_layer * s["layers"]
+    value = s["rows"] / step_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                         "sample": (f"each step = 1 of {s['layers']} layers of the workload "
+                                    f"through the numpy oracle (all projections, fwd + training "
+                                    f"bwd + AdamW), time x{s['layers']}")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------------- GPU side
+def timed(fn, reps: int, stream) -> float:
+    """ms per call of fn() over `reps` calls, CUDA events on `stream`."""
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def run_ours(args, cfg, workload):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_16400_b200 import _lib, ops
+    from paper_2604_16400_b200.replica import ReplicaStack
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py (ours) needs a CUDA device")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    st_dev = torch.cuda.current_stream()
+
+    stack = ReplicaStack(cfg, dev, seed=args.seed)
+    train, items = cfg.batch(args.seed)
+    plan = stack.plan(train, items)
+    stack.allocate(plan)
+    T, Ttr = plan.n_rows, plan.n_train
+    fused_opt = world == 1
+
+    flat_grad = None
+    if not fused_opt:
+        flat_grad = stack.flatten_grads()
+
+    def sync_and_apply():
+        dist.all_reduce(flat_grad, op=dist.ReduceOp.AVG)
+        apply_graph.replay()
+
+    # eager step sizes the workspaces; then capture
+    stack.run_step(plan, optimizer_step=fused_opt)
+    torch.cuda.synchronize()
+    use_graph = not args.eager
+    if use_graph:
+        stack.capture(plan, optimizer_step=fused_opt)
+    if not fused_opt:
+        stack.opt.advance()
+        for p in stack.projections():
+            p.apply_optimizer(stack.opt)
+        apply_graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(st_dev)
+        with torch.cuda.stream(s), torch.cuda.graph(apply_graph, stream=s):
+            for p in stack.projections():
+                p.apply_optimizer(stack.opt)
+        st_dev.wait_stream(s)
+
+    n0 = ops.launch_count()
+    if use_graph:
+        step = lambda: stack.replay(optimizer_step=fused_opt)  # noqa: E731
+    else:
+        step = lambda: stack.run_step(plan, optimizer_step=fused_opt)  # noqa: E731
+    # launches per step (counted on one eager step)
+    c0 = ops.launch_count()
+    stack.run_step(plan, optimizer_step=fused_opt)
+    launches_per_step = ops.launch_count() - c0 + (2 * sum(1 for _ in stack.projections())
+                                                     if not fused_opt else 0)
+    del n0
+
+    def full_step():
+        if not fused_opt:
+            stack.opt.advance()
+        step()
+        if not fused_opt:
+            sync_and_apply()
+
+    for _ in range(args.warmup):
+        full_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = timed(full_step, args.steps, st_dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = T * world / (ms_max / 1e3)
+
+    peaks, peaks_src = load_peaks()
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights of the named shape; seeded synthetic rows)",
+        "config": dict(workload, sync=("none (1 replica): fused AdamW" if fused_opt else
+                                       "NCCL allreduce(avg) of LoRA grads each step + AdamW "
+                                       "apply")),
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+    }
+    step_flops = stack.step_flops(plan)
+    out["tensor_tflops_step"] = step_flops / (ms_max / 1e3) / 1e12
+
+    # ---------------- roofline: GEMM-only and LoRA-only graphs of the same step
+    if not args.no_roofline and use_graph:
+        gg = torch.cuda.CUDAGraph()
+        gl = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(st_dev)
+        with torch.cuda.stream(s):
+            with ops.only("gemm"), torch.cuda.graph(gg, stream=s):
+                stack.run_step(plan, optimizer_step=fused_opt, advance=False)
+            with ops.only("lora", "plan"), torch.cuda.graph(gl, stream=s):
+                stack.run_step(plan, optimizer_step=fused_opt, advance=False)
+        st_dev.wait_stream(s)
+        reps = max(3, min(20, args.steps))
+        gg.replay()
+        gemm_ms = timed(gg.replay, reps, st_dev)
+        gl.replay()
+        lora_ms = timed(gl.replay, reps, st_dev)
+        n_gemm = sum(2 if Ttr else 1 for _ in stack.projections())
+        achieved = step_flops / (gemm_ms / 1e3) / 1e12
+        peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+        traffic = None
+        tf = ROOT / "profiles" / "gemm_traffic.json"
+        if tf.exists():
+            try:
+                traffic = json.loads(tf.read_text()).get(cfg.key)
+            except (ValueError, OSError):
+                traffic = None
+        out["roofline"] = {
+            "bound": "tensor", "kernel": "gemm_lora_kernel (tcgen05, K2 fwd + K3 dX)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": f"{peaks_src} bf16_tflops_sustained",
+            "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": n_gemm,
+            "share_of_step": gemm_ms / ms_max}
+        lb = stack.lora_bytes(plan)
+        hbm = peaks.get("hbm_gbs")
+        lora_gbs = lb["total"] / (lora_ms / 1e3) / 1e9
+        out["roofline_lora"] = {
+            "bound": "hbm", "kernels": "lora_shrink + lora_reduce(+AdamW) + segment expand",
+            "achieved": lora_gbs, "peak": hbm, "unit": "GB/s", "frac": lora_gbs / hbm,
+            "algorithmic_bytes_per_step": lb["total"], "lora_ms_per_step": lora_ms,
+            "share_of_step": lora_ms / ms_max, "peak_source": f"{peaks_src} hbm_gbs"}
+        del gg, gl
+
+    # ---------------- e2e: host buffers, copies inside the timed region
+    if not args.no_e2e and use_graph:
+        acts = stack._acts
+        L = cfg.model.layers
+        h = cfg.model.hidden
+        x_host = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
+        x_host.copy_(acts["X"][0].cpu())
+        dy_host = torch.empty(max(Ttr, 1), h, dtype=torch.bfloat16).pin_memory()
+        if Ttr:
+            dy_host.copy_(acts["dY_top"].cpu())
+        out_host = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
+        h2d = x_host.numel() * 2 + (Ttr * h * 2 if Ttr else 0) + 28
+
+        def e2e_step():
+            nonlocal h2d_step
+            acts["X"][0].copy_(x_host, non_blocking=True)
+            if Ttr:
+                acts["dY_top"].copy_(dy_host[:Ttr], non_blocking=True)
+            b = plan.device.upload()
+            if plan.train_device is not None:
+                b += plan.train_device.upload()
+            h2d_step = h2d + b
+            full_step()
+            out_host.copy_(acts["X"][L], non_blocking=True)
+
+        h2d_step = 0
+        e2e_step()
+        e_ms = timed(e2e_step, args.steps, st_dev)
+        te = torch.tensor([e_ms], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        out["e2e"] = {"value": T * world / (float(te.item()) / 1e3), "unit": UNIT,
+                      "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": out_host.numel() * 2,
+                      "ms_per_step": float(te.item()),
+                      "api": "ReplicaStack.replay (CUDA graph of the C-ABI calls) + pinned copies"}
+
+    # ---------------- CPU baseline (rank 0, N=1)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = time_cpu_sample(cfg)
+        except MemoryError as e:  # pragma: no cover
+            out["cpu_baseline"] = {"value": None, "error": f"{type(e).__name__}: {e}"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def workload_for(cfg, args) -> dict:
+    from paper_2604_16400_b200.segments import build_mixed_batch
+    train, items = cfg.batch(args.seed)
+    mb = build_mixed_batch(train, items)
+    return {
+        "workload": f"{cfg.key}: {cfg.description}",
+        "rows_per_step": mb.n_rows, "train_rows": mb.n_train_rows, "infer_rows": mb.n_infer_rows,
+        "segments": mb.n_segments, "adapters": cfg.n_adapters, "rank": cfg.rank,
+        "layers": cfg.model.layers, "hidden": cfg.model.hidden,
+        "intermediate": cfg.model.intermediate,
+        "projections": ",".join(s.name for s in cfg.projections) + " (all 7, q|k|v and gate|up fused)",
+        "parallelism": f"replicas x{args.gpus}",
+        "l2": "inputs larger than L2 (all frozen weights, ~2x the model in bf16 with W^T, stream "
+              "through HBM every step)",
+    }
+
+
+def main(argv=None) -> int:
+    args = parse_args(argv)
+    from paper_2604_16400_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    workload = workload_for(cfg, args)
+    if args.impl == "reference":
+        return run_reference(args, cfg, workload)
+    return run_ours(args, cfg, workload)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -104,8 +104,9 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
  * Element (p,q) of group g lives at fp32 index (c_row_off+p)*ldc + c_col_off+q of grad / master /
  * m / v and of out_same (bf16), and at (t_row_off+q)*ld_trans + t_col_off+p of out_trans (bf16).
  * mode STORE_GRAD: grad = C*grad_scale (+grad if accum_in).  mode ADAMW: the same gradient drives
- * an AdamW step (adamw = {lr, beta1, beta2, eps, weight_decay, 1-beta1^step, 1-beta2^step},
- * PyTorch semantics) on master/m/v and the bf16 copies are rewritten.  Deterministic. */
+ * an AdamW step on master/m/v (PyTorch semantics) and the bf16 copies are rewritten.  `adamw` is
+ * a DEVICE pointer to 7 floats {lr, beta1, beta2, eps, weight_decay, 1-beta1^step, 1-beta2^step}
+ * so a captured CUDA graph can be replayed with a changing step.  Deterministic. */
 size_t collm_reduce_workspace_bytes(const int32_t* groups, int n_groups, int tsplit);
 int collm_lora_reduce(const void* U, int ldu, const void* V, int ldv, int T,
                       const int32_t* groups, int n_groups, int mode, int accum_in,

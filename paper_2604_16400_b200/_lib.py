@@ -41,8 +41,8 @@ SIGNATURES: dict[str, tuple] = {
                              _I, _I, _I, _IP, _IP, _I, _P]),
     "collm_reduce_workspace_bytes": (_SZ, [_IP, _I, _I]),
     "collm_lora_reduce": (_I, [_P, _I, _P, _I, _I, _IP, _I, _I, _I, _F, _P, _I, _P, _P, _P, _P,
-                               _P, _I, _FP, _I, _P, _SZ, _P]),
-    "collm_lora_apply": (_I, [_IP, _I, _I, _P, _I, _P, _P, _P, _P, _P, _I, _FP, _P]),
+                               _P, _I, _P, _I, _P, _SZ, _P]),
+    "collm_lora_apply": (_I, [_IP, _I, _I, _P, _I, _P, _P, _P, _P, _P, _I, _P, _P]),
 }
 
 _lib = None

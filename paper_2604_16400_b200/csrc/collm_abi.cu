@@ -397,18 +397,6 @@ size_t collm_reduce_workspace_bytes(const int32_t* groups, int n_groups, int tsp
   return kCounterBytes + (size_t)tsplit * tiles * 64 * 64 * sizeof(float);
 }
 
-static void fill_opt(ReduceParams& p, const float* adamw) {
-  if (adamw) {
-    p.opt.lr = adamw[0];
-    p.opt.beta1 = adamw[1];
-    p.opt.beta2 = adamw[2];
-    p.opt.eps = adamw[3];
-    p.opt.weight_decay = adamw[4];
-    p.opt.bc1 = adamw[5];
-    p.opt.bc2 = adamw[6];
-  }
-}
-
 int collm_lora_reduce(const void* U, int ldu, const void* V, int ldv, int T,
                       const int32_t* groups, int n_groups, int mode, int accum_in,
                       float grad_scale, float* grad, int ldc, float* master, float* m, float* v,
@@ -444,7 +432,7 @@ int collm_lora_reduce(const void* U, int ldu, const void* V, int ldv, int T,
   p.out_same = (bf16*)out_same;
   p.out_trans = (bf16*)out_trans;
   p.ld_trans = ld_trans;
-  fill_opt(p, adamw);
+  p.opt = adamw;
   if (tsplit > 1) {
     const size_t need = collm_reduce_workspace_bytes(groups, n_groups, tsplit);
     CHECK_ARG(workspace && ws_bytes >= need, "reduce workspace too small: %zu < %zu", ws_bytes,
@@ -483,7 +471,7 @@ int collm_lora_apply(const int32_t* groups, int n_groups, int mode, float* grad,
   p.out_same = (bf16*)out_same;
   p.out_trans = (bf16*)out_trans;
   p.ld_trans = ld_trans;
-  fill_opt(p, adamw);
+  p.opt = adamw;
   long long total = 0;
   for (int g = 0; g < n_groups; ++g) total += (long long)p.groups[g].P * p.groups[g].Q;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 4LL * num_sms_cached());

@@ -37,10 +37,9 @@ struct ReduceGroup {
   int tile_begin;            // first CTA tile of this group (64-row P tiles)
 };
 
-struct AdamWArgs {
-  float lr, beta1, beta2, eps, weight_decay;
-  float bc1, bc2;  // 1 - beta^step
-};
+// AdamW hyper-parameters live in DEVICE memory ({lr, beta1, beta2, eps, weight_decay,
+// 1-beta1^step, 1-beta2^step}) so a captured CUDA graph can be replayed step after step with the
+// host updating only this 28-byte block.
 
 struct ReduceParams {
   const bf16* U;
@@ -63,7 +62,7 @@ struct ReduceParams {
   bf16* out_same;
   bf16* out_trans;
   int ld_trans;
-  AdamWArgs opt;
+  const float* opt;  // device [7]
   float* partials;  // [tsplit][n_tiles][64*64]
   int32_t* counters;
 };
@@ -111,14 +110,16 @@ __device__ __forceinline__ void finalize_elem(const ReduceParams& p, const Reduc
   }
   float w = p.master[idx];
   if (p.mode == kModeAdamW) {
-    const AdamWArgs& o = p.opt;
-    w -= o.lr * o.weight_decay * w;
-    const float m = o.beta1 * p.m[idx] + (1.f - o.beta1) * g;
-    const float v = o.beta2 * p.v[idx] + (1.f - o.beta2) * g * g;
+    const float lr = __ldg(p.opt + 0), beta1 = __ldg(p.opt + 1), beta2 = __ldg(p.opt + 2);
+    const float eps = __ldg(p.opt + 3), wd = __ldg(p.opt + 4);
+    const float bc1 = __ldg(p.opt + 5), bc2 = __ldg(p.opt + 6);
+    w -= lr * wd * w;
+    const float m = beta1 * p.m[idx] + (1.f - beta1) * g;
+    const float v = beta2 * p.v[idx] + (1.f - beta2) * g * g;
     p.m[idx] = m;
     p.v[idx] = v;
-    const float denom = sqrtf(v) / sqrtf(o.bc2) + o.eps;
-    w -= (o.lr / o.bc1) * (m / denom);
+    const float denom = sqrtf(v) / sqrtf(bc2) + eps;
+    w -= (lr / bc1) * (m / denom);
     p.master[idx] = w;
   }
   const bf16 wb = __float2bfloat16_rn(w);

@@ -66,6 +66,8 @@ class ProjectionSpec:
 
 @dataclass
 class AdamWConfig:
+    """AdamW hyper-parameters (torch.optim.AdamW semantics; HF Trainer's default optimizer)."""
+
     lr: float = 1e-4
     beta1: float = 0.9
     beta2: float = 0.999
@@ -75,6 +77,24 @@ class AdamWConfig:
     def args(self, step: int) -> list[float]:
         return [self.lr, self.beta1, self.beta2, self.eps, self.weight_decay,
                 1.0 - self.beta1 ** step, 1.0 - self.beta2 ** step]
+
+
+class OptimizerState:
+    """Step counter + the device-resident 7-float argument block the fused AdamW kernels read.
+
+    ``advance()`` bumps the step and enqueues a 28-byte H2D copy on the current stream, so the
+    same captured CUDA graph replays correctly step after step."""
+
+    def __init__(self, cfg: AdamWConfig | None = None, device: torch.device | str = "cuda"):
+        self.cfg = cfg or AdamWConfig()
+        self.step = 0
+        self.args = torch.zeros(7, dtype=torch.float32, device=device)
+        self._host = torch.zeros(7, dtype=torch.float32).pin_memory()
+
+    def advance(self) -> None:
+        self.step += 1
+        self._host.copy_(torch.tensor(self.cfg.args(self.step), dtype=torch.float32))
+        self.args.copy_(self._host, non_blocking=True)
 
 
 @dataclass
@@ -94,7 +114,6 @@ class TrainState:
     grad_AT: torch.Tensor
     AT16: torch.Tensor
     BT16: torch.Tensor
-    step: int = 0
 
 
 @dataclass
@@ -202,7 +221,8 @@ class LoraProjection:
         R, rp, K = spec.R, spec.r_pad, spec.in_features
         if plan.n_slots:
             Hs = Hslots[: plan.n_slots * TILE_M]
-            Hs.zero_()
+            if ops.enabled("lora"):
+                Hs.zero_()
             groups = [(g, min(64, R - g), 0, K) for g in range(0, R, 64)]
             ops.lora_shrink(X, self.A, plan.shrink_tiles, plan.n_shrink_tiles, self.scale, groups,
                             R, H16=H16, Hslots=Hs, slot_of_row=plan.slot_of_row)
@@ -218,11 +238,12 @@ class LoraProjection:
         return Y, ForwardCache(X=X, H16=H16, n_train=n_train)
 
     def backward(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan,
-                 dX: torch.Tensor | None = None, *, optimizer: AdamWConfig | None = None,
+                 dX: torch.Tensor | None = None, *, optimizer: OptimizerState | None = None,
                  accumulate: bool = False, grad_scale: float = 1.0,
                  need_dx: bool = True) -> torch.Tensor | None:
         """Backward of the training rows [0, n_train).  ``optimizer`` given -> fused AdamW step
-        (after adding the gradient already accumulated when ``accumulate``); otherwise the
+        (after adding the gradient already accumulated when ``accumulate``) using the step the
+        caller already advanced (``OptimizerState.advance``); otherwise the
         gradient is stored (or added, ``accumulate``) into the grad buffers, e.g. for a
         cross-replica allreduce followed by :meth:`apply_optimizer`."""
         st = self.train_state
@@ -255,8 +276,7 @@ class LoraProjection:
               for s in range(len(spec.subs))]
         gA = [(0, K, q, min(64, R - q), 0, q, q, 0) for q in range(0, R, 64)]
         if optimizer is not None:
-            st.step += 1
-            args = optimizer.args(st.step)
+            args = optimizer.args
             ops.lora_reduce(dY, H_tr, Ttr, gB, _lib.MODE_ADAMW, accum_in=accumulate,
                             grad_scale=grad_scale, grad=st.grad_B, ldc=rp, master=st.master_B,
                             m=st.m_B, v=st.v_B, out_same=self.B[st.adapter], out_trans=st.BT16,
@@ -272,14 +292,13 @@ class LoraProjection:
                             grad_scale=grad_scale, grad=st.grad_AT, ldc=R)
         return dX
 
-    def apply_optimizer(self, optimizer: AdamWConfig) -> None:
+    def apply_optimizer(self, optimizer: OptimizerState) -> None:
         """AdamW from the grad buffers (after a cross-replica allreduce of the gradients)."""
         st = self.train_state
         spec = self.spec
         K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
         bnd = spec.sub_bounds
-        st.step += 1
-        args = optimizer.args(st.step)
+        args = optimizer.args
         gB = [(bnd[s], spec.subs[s], s * rp, rp, bnd[s], 0, s * rp, bnd[s])
               for s in range(len(spec.subs))]
         gA = [(0, K, q, min(64, R - q), 0, q, q, 0) for q in range(0, R, 64)]

@@ -8,10 +8,49 @@ from __future__ import annotations
 
 import math
 import threading
+from contextlib import contextmanager
 
 import torch
 
 from . import _lib
+
+
+class _LaunchFilter(threading.local):
+    """Per-thread launch accounting: which op kinds are issued ('plan', 'lora', 'gemm') and how
+    many collm kernels were launched.  Used by bench.py to build GEMM-only / LoRA-only graphs
+    of the same step (per-kernel roofline timing) and to count launches."""
+
+    def __init__(self) -> None:
+        self.kinds: set[str] | None = None
+        self.count = 0
+
+
+_filter = _LaunchFilter()
+
+
+@contextmanager
+def only(*kinds: str):
+    prev = _filter.kinds
+    _filter.kinds = set(kinds)
+    try:
+        yield
+    finally:
+        _filter.kinds = prev
+
+
+def enabled(kind: str) -> bool:
+    return _filter.kinds is None or kind in _filter.kinds
+
+
+def launch_count() -> int:
+    return _filter.count
+
+
+def _launch(kind: str) -> bool:
+    if not enabled(kind):
+        return False
+    _filter.count += 1
+    return True
 
 NUM_SMS_DEFAULT = 148
 _sms_cache: dict[int, int] = {}
@@ -76,7 +115,7 @@ def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: 
     """K1: H[t, ranks of g] = scale[a] * X[t, K-range of g] . A_a[ranks of g]^T (see collm.h)."""
     _need(X, torch.bfloat16, "X")
     _need(A, torch.bfloat16, "A")
-    if n_tiles == 0:
+    if n_tiles == 0 or not _launch("lora"):
         return
     lda = A.stride(-2)
     if a_stride is None:
@@ -108,6 +147,8 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
     N = B.shape[0]
     if B.shape[1] != K or Y.shape[1] < N or Y.shape[0] < M:
         raise ValueError(f"gemm_lora shapes: A {tuple(A.shape)} B {tuple(B.shape)} Y {tuple(Y.shape)}")
+    if not _launch("gemm"):
+        return
     lora = tile_slot_ptr is not None
     n_sub = len(sub_n_start) - 1 if (lora and sub_n_start) else 1
     _lib.call(
@@ -132,10 +173,12 @@ def lora_reduce(U: torch.Tensor, V: torch.Tensor, T: int, groups: list[tuple], m
                 master: torch.Tensor | None = None, m: torch.Tensor | None = None,
                 v: torch.Tensor | None = None, out_same: torch.Tensor | None = None,
                 out_trans: torch.Tensor | None = None, ld_trans: int = 0,
-                adamw: list[float] | None = None, tsplit: int | None = None) -> None:
+                adamw: torch.Tensor | None = None, tsplit: int | None = None) -> None:
     """K5: C = U^T V per group -> grad store or fused AdamW (see collm.h)."""
     _need(U, torch.bfloat16, "U")
     _need(V, torch.bfloat16, "V")
+    if not _launch("lora"):
+        return
     flat = [v_ for g in groups for v_ in g]
     garr = _lib.int_array(flat)
     if tsplit is None:
@@ -146,7 +189,7 @@ def lora_reduce(U: torch.Tensor, V: torch.Tensor, T: int, groups: list[tuple], m
     _lib.call("collm_lora_reduce", U.data_ptr(), U.stride(0), V.data_ptr(), V.stride(0), T, garr,
               len(groups), mode, int(accum_in), float(grad_scale), _p(grad), ldc, _p(master),
               _p(m), _p(v), _p(out_same), _p(out_trans), ld_trans,
-              _lib.float_array(adamw) if adamw else None, tsplit, _p(ws),
+              _p(adamw), tsplit, _p(ws),
               0 if ws is None else ws.numel(), _stream())
 
 
@@ -154,8 +197,10 @@ def lora_apply(groups: list[tuple], mode: int, *, ldc: int, master: torch.Tensor
                grad: torch.Tensor | None = None, m: torch.Tensor | None = None,
                v: torch.Tensor | None = None, out_same: torch.Tensor | None = None,
                out_trans: torch.Tensor | None = None, ld_trans: int = 0,
-               adamw: list[float] | None = None) -> None:
+               adamw: torch.Tensor | None = None) -> None:
+    if not _launch("lora"):
+        return
     flat = [v_ for g in groups for v_ in g]
     _lib.call("collm_lora_apply", _lib.int_array(flat), len(groups), mode, _p(grad), ldc,
               master.data_ptr(), _p(m), _p(v), _p(out_same), _p(out_trans), ld_trans,
-              _lib.float_array(adamw) if adamw else None, _stream())
+              _p(adamw), _stream())

@@ -1,0 +1,289 @@
+"""One replica's co-batched step through the whole LoRA-augmented projection stack.
+
+This is the B200 body of the reference's replica step: ``Engine._start_batch`` (inference,
+/root/reference/pkg/src/coserve/engine.py:312-333) and ``_handle_train_start`` /
+``_handle_train_done`` (training, engine.py:372-408), which today call the latency surfaces
+``true_infer_latency`` / ``true_train_latency`` and the convergence stand-in ``train_step``
+(perf.py:62-126).  Here one pass runs the forward of every row (inference + training) through
+every projection of every layer and the backward + fused AdamW of the training rows, over frozen
+bf16 base weights resident in HBM.
+
+Data flow per layer l (attention / MLP nonlinearities are outside this hot path):
+  X_l --qkv--> ;  Xo_l --o--> ;  X_l --gate_up--> ;  Xd_l --down--> X_{l+1}
+where Xo_l / Xd_l (attention output / MLP activation) are synthetic device-resident stand-ins.
+Backward runs from the top: dY(down_l) = dX(qkv_{l+1}) (dY_top for the last layer); the other
+projections' output grads are synthetic stand-ins.  Every projection computes dX, dA, dB and its
+fused AdamW step, as the metric's FLOP count assumes.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from .configs import LayerConfig
+from .domain import ConfigurationError, InferenceItem, MixedBatch, TrainItem
+from .layer import AdamWConfig, LoraProjection, OptimizerState
+from .segments import DevicePlan, HostPlan, build_mixed_batch, plan_segments, uniform_plan
+
+ENTRY = ("qkv", "q", "k", "v", "gate_up", "gate", "up")
+
+
+@dataclass
+class StepPlan:
+    batch: MixedBatch
+    host: HostPlan
+    device: DevicePlan
+    train_host: HostPlan | None
+    train_device: DevicePlan | None
+
+    @property
+    def n_rows(self) -> int:
+        return self.batch.n_rows
+
+    @property
+    def n_train(self) -> int:
+        return self.batch.n_train_rows
+
+
+class ReplicaStack:
+    def __init__(self, cfg: LayerConfig, device: torch.device | str = "cuda", seed: int = 0,
+                 optimizer: AdamWConfig | None = None, init: bool = True):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.specs = cfg.projections
+        L = cfg.model.layers
+        self.layers: list[list[LoraProjection]] = [
+            [LoraProjection(spec, cfg.n_adapters, self.device) for spec in self.specs]
+            for _ in range(L)]
+        self.opt = OptimizerState(optimizer, self.device)
+        self.seed = seed
+        if init:
+            self.init_synthetic(seed)
+        self._acts: dict | None = None
+        self._graph: torch.cuda.CUDAGraph | None = None
+
+    # ------------------------------------------------------------------ weights
+    @torch.no_grad()
+    def init_synthetic(self, seed: int) -> None:
+        """Random-init weights of the named architecture (no checkpoints offline):
+        W ~ N(0, 0.02^2); A ~ U(+-1/sqrt(K)); B ~ N(0, 0.02^2) (non-zero, so the expand path is
+        exercised); scale = alpha / r."""
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        r = self.cfg.rank
+        for layer in self.layers:
+            for proj in layer:
+                sp = proj.spec
+                K, rp = sp.in_features, sp.r_pad
+                proj.W.normal_(0.0, 0.02, generator=g)
+                proj.refresh_transpose()
+                lim = 1.0 / (K ** 0.5)
+                proj.A.zero_()
+                proj.B.zero_()
+                bnd = sp.sub_bounds
+                for s in range(len(sp.subs)):
+                    a = torch.empty(self.cfg.n_adapters, r, K, device=self.device)
+                    a.uniform_(-lim, lim, generator=g)
+                    proj.A[:, s * rp:s * rp + r] = a.to(torch.bfloat16)
+                    b = torch.empty(self.cfg.n_adapters, sp.subs[s], r, device=self.device)
+                    b.normal_(0.0, 0.02, generator=g)
+                    proj.B[:, bnd[s]:bnd[s + 1], :r] = b.to(torch.bfloat16)
+                proj.scale.fill_(sp.alpha / r)
+                proj.make_trainable(self.cfg.train_adapter)
+
+    def projections(self):
+        for layer in self.layers:
+            yield from layer
+
+    def trainable_tensors(self, which: str = "master") -> list[torch.Tensor]:
+        """The trainable adapter's fp32 tensors across the stack (for cross-replica sync):
+        'master' = parameters (fedavg mode), 'grad' = gradients (grad-sync mode)."""
+        out = []
+        for p in self.projections():
+            st = p.train_state
+            if which == "master":
+                out += [st.master_B, st.master_AT]
+            else:
+                out += [st.grad_B, st.grad_AT]
+        return out
+
+    def flatten_grads(self) -> torch.Tensor:
+        """Re-home every projection's gradient buffers as views of ONE flat fp32 tensor, so the
+        cross-replica sync is a single NCCL allreduce (call before capturing a graph)."""
+        states = [p.train_state for p in self.projections()]
+        total = sum(st.grad_B.numel() + st.grad_AT.numel() for st in states)
+        flat = torch.zeros(total, dtype=torch.float32, device=self.device)
+        off = 0
+        for st in states:
+            for name in ("grad_B", "grad_AT"):
+                t = getattr(st, name)
+                setattr(st, name, flat[off:off + t.numel()].view(t.shape))
+                off += t.numel()
+        self.flat_grad = flat
+        return flat
+
+    def flatten_masters(self) -> torch.Tensor:
+        """Same for the fp32 master parameters (fedavg parameter-averaging mode)."""
+        states = [p.train_state for p in self.projections()]
+        total = sum(st.master_B.numel() + st.master_AT.numel() for st in states)
+        flat = torch.empty(total, dtype=torch.float32, device=self.device)
+        off = 0
+        for st in states:
+            for name in ("master_B", "master_AT"):
+                t = getattr(st, name)
+                flat[off:off + t.numel()].copy_(t.reshape(-1))
+                setattr(st, name, flat[off:off + t.numel()].view(t.shape))
+                off += t.numel()
+        self.flat_master = flat
+        return flat
+
+    # ------------------------------------------------------------------ plans
+    def plan(self, train: TrainItem | None, items: list[InferenceItem]) -> StepPlan:
+        mb = build_mixed_batch(train, items)
+        hp = plan_segments(mb.seg_start, mb.seg_adapter)
+        dp = DevicePlan(hp, self.device, expand=False)
+        th = td = None
+        if mb.n_train_rows:
+            if mb.train_adapter != self.cfg.train_adapter:
+                raise ConfigurationError(
+                    f"training rows use adapter {mb.train_adapter}, the replica trains "
+                    f"{self.cfg.train_adapter}")
+            th = uniform_plan(mb.n_train_rows, mb.train_adapter)
+            td = DevicePlan(th, self.device)
+        return StepPlan(mb, hp, dp, th, td)
+
+    # ------------------------------------------------------------------ activations
+    def allocate(self, plan: StepPlan, distinct_synthetic: bool | None = None, seed: int = 1) -> dict:
+        """Device buffers of one pass.  Synthetic stand-ins (Xo, Xd, the non-chained output grads)
+        are per layer when they fit comfortably in HBM, else shared across layers (same traffic,
+        inputs are far larger than L2 either way)."""
+        T, Ttr = plan.n_rows, plan.n_train
+        h = self.cfg.model.hidden
+        i = self.cfg.model.intermediate
+        L = self.cfg.model.layers
+        dev = self.device
+        bf = torch.bfloat16
+        per_layer_bytes = 2 * (T * h + T * i + Ttr * sum(s.out_features for s in self.specs))
+        if distinct_synthetic is None:
+            free, _ = torch.cuda.mem_get_info(dev)
+            distinct_synthetic = per_layer_bytes * L < 0.5 * free
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+
+        def rnd(*shape):
+            return torch.randn(*shape, device=dev, generator=g, dtype=torch.float32).to(bf)
+
+        n_syn = L if distinct_synthetic else 1
+        acts = {
+            "distinct_synthetic": distinct_synthetic,
+            "X": [torch.empty(T, h, dtype=bf, device=dev) for _ in range(L + 1)],
+            "Xo": [rnd(T, h) for _ in range(n_syn)],
+            "Xd": [rnd(T, i) for _ in range(n_syn)],
+            "dY": [{s.name: rnd(Ttr, s.out_features) for s in self.specs
+                    if s.name != "down"} for _ in range(n_syn)] if Ttr else [],
+            "dY_top": rnd(Ttr, h) if Ttr else None,
+            "Y": {s.name: torch.empty(T, s.out_features, dtype=bf, device=dev)
+                  for s in self.specs if s.name != "down"},
+            "dX_first": [torch.empty(Ttr, h, dtype=bf, device=dev) for _ in range(L)] if Ttr else [],
+            "dX": {s.name: torch.empty(Ttr, s.in_features, dtype=bf, device=dev)
+                   for s in self.specs} if Ttr else {},
+        }
+        acts["X"][0].copy_(rnd(T, h))
+        self._acts = acts
+        self._plan = plan
+        return acts
+
+    # ------------------------------------------------------------------ the step
+    def run_step(self, plan: StepPlan | None = None, optimizer_step: bool = True,
+                 advance: bool = True) -> torch.Tensor:
+        """Enqueue one full co-batched step on the current stream; returns the final hidden state
+        buffer (device).  With ``advance`` the optimizer step counter is bumped first (keep it
+        False inside CUDA-graph capture; call ``opt.advance()`` before each replay instead)."""
+        plan = plan or self._plan
+        a = self._acts
+        if a is None:
+            raise ConfigurationError("allocate() the step buffers first")
+        L = self.cfg.model.layers
+        Ttr = plan.n_train
+        if advance and Ttr and optimizer_step:
+            self.opt.advance()
+        plan.device.expand()
+        first = self.specs[0].name
+        caches: list[dict] = []
+        for l, layer in enumerate(self.layers):
+            syn = l if a["distinct_synthetic"] else 0
+            c = {}
+            for proj in layer:
+                name = proj.spec.name
+                if name in ENTRY:
+                    X = a["X"][l]
+                elif name == "o":
+                    X = a["Xo"][syn]
+                else:  # down
+                    X = a["Xd"][syn]
+                Y = a["X"][l + 1] if name == "down" else a["Y"][name]
+                _, c[name] = proj.forward(X, plan.device, Y, n_train=Ttr)
+            caches.append(c)
+        if Ttr:
+            opt = self.opt if optimizer_step else None
+            for l in range(L - 1, -1, -1):
+                syn = l if a["distinct_synthetic"] else 0
+                for proj in reversed(self.layers[l]):
+                    name = proj.spec.name
+                    if name == "down":
+                        dY = a["dY_top"] if l == L - 1 else a["dX_first"][l + 1]
+                    else:
+                        dY = a["dY"][syn][name]
+                    dX = a["dX_first"][l] if name == first else a["dX"][name]
+                    proj.backward(dY, caches[l][name], plan.train_device, dX, optimizer=opt)
+        return a["X"][L]
+
+    # ------------------------------------------------------------------ graphs
+    def capture(self, plan: StepPlan | None = None, optimizer_step: bool = True) -> torch.cuda.CUDAGraph:
+        """Capture one step into a CUDA graph (buffers and workspaces must already be sized: run
+        one eager step first)."""
+        plan = plan or self._plan
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self.run_step(plan, optimizer_step=optimizer_step, advance=False)
+        torch.cuda.current_stream().wait_stream(s)
+        self._graph = g
+        return g
+
+    def replay(self, optimizer_step: bool = True) -> torch.Tensor:
+        if self._graph is None:
+            raise ConfigurationError("capture() first")
+        if optimizer_step and self._plan.n_train:
+            self.opt.advance()
+        self._graph.replay()
+        return self._acts["X"][self.cfg.model.layers]
+
+    # ------------------------------------------------------------------ accounting
+    def step_flops(self, plan: StepPlan | None = None) -> int:
+        """Algorithmic tensor-pipe FLOPs of one step: 2*K*N*(T + T_tr) summed over projections."""
+        plan = plan or self._plan
+        T, Ttr = plan.n_rows, plan.n_train
+        return sum(2 * s.in_features * s.out_features * (T + Ttr)
+                   for s in self.specs) * self.cfg.model.layers
+
+    def lora_bytes(self, plan: StepPlan | None = None) -> dict:
+        """Algorithmic HBM bytes of the LoRA segments per step: distinct adapters'
+        A and B once (bf16), X read by the shrink, H write+read; backward adds dY and X_tr reads
+        and the fp32 optimizer read-modify-write."""
+        plan = plan or self._plan
+        T, Ttr = plan.n_rows, plan.n_train
+        n_distinct = len({a for a in plan.batch.seg_adapter if a >= 0})
+        fwd = bwd = 0
+        for s in self.specs:
+            K, N, r = s.in_features, s.out_features, s.rank
+            nsub = len(s.subs)
+            fwd += n_distinct * 2 * r * (K * nsub + N) + 2 * T * K + 4 * T * s.R
+            if Ttr:
+                bwd += 2 * Ttr * N + 2 * Ttr * K + 16 * r * (K * nsub + N)
+        L = self.cfg.model.layers
+        return {"fwd": fwd * L, "bwd": bwd * L, "total": (fwd + bwd) * L}

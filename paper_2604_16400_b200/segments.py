@@ -137,6 +137,7 @@ class DevicePlan:
         buf = torch.empty(packed.numel(), dtype=torch.int32, device=dev)
         buf.copy_(packed, non_blocking=True)
         offs = np.cumsum([0] + sizes)
+        self._pinned = packed
         self._buf = buf
         self.seg_start = buf[offs[0]:offs[1]]
         self.seg_adapter = buf[offs[1]:offs[2]]
@@ -150,7 +151,16 @@ class DevicePlan:
         if expand:
             self.expand(stream)
 
+    def upload(self) -> int:
+        """Re-send the (pinned) host tables to the same device buffers on the current stream —
+        what a serving loop does once per pass; returns the bytes copied."""
+        self._buf.copy_(self._pinned, non_blocking=True)
+        return self.h2d_bytes
+
     def expand(self, stream: torch.cuda.Stream | None = None) -> None:
+        from . import ops
+        if not ops._launch("plan"):
+            return
         st = (stream or torch.cuda.current_stream()).cuda_stream
         _lib.call("collm_expand_segments", self.seg_start.data_ptr(), self.seg_adapter.data_ptr(),
                   len(self.host.seg_adapter), self.n_rows, self.tile_slot_ptr.data_ptr(),

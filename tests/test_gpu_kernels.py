@@ -147,7 +147,7 @@ def test_reduce_adamw():
     p_ref = master.clone()
     ops.lora_reduce(U, V, T, groups, _lib.MODE_ADAMW, ldc=Q, master=master, m=m, v=v,
                     out_same=same, out_trans=trans, ld_trans=P,
-                    adamw=[lr, b1, b2, eps, wd, 1 - b1, 1 - b2])
+                    adamw=torch.tensor([lr, b1, b2, eps, wd, 1 - b1, 1 - b2]).cuda())
     torch.cuda.synchronize()
     gr = ref.cuda()
     p_ref.mul_(1 - lr * wd)

@@ -61,7 +61,8 @@ CASES = [
 def test_projection_fwd_bwd(case):
     from paper_2604_16400_b200 import segments
     from paper_2604_16400_b200.domain import InferenceItem, RowRole, TrainItem
-    from paper_2604_16400_b200.layer import AdamWConfig, LoraProjection, ProjectionSpec
+    from paper_2604_16400_b200.layer import (AdamWConfig, LoraProjection, OptimizerState,
+                                             ProjectionSpec)
 
     name, K, subs, rank, n_ad, T_tr, n_dec, n_pre, n_base, seed = case
     g = rng(seed)
@@ -127,7 +128,9 @@ def test_projection_fwd_bwd(case):
     mB0 = st.master_B.cpu().numpy().copy()
     mAT0 = st.master_AT.cpu().numpy().copy()
     opt = AdamWConfig(lr=1e-3, weight_decay=0.01)
-    proj.backward(dY, cache, tp, optimizer=opt, need_dx=False)
+    ostate = OptimizerState(opt)
+    ostate.advance()
+    proj.backward(dY, cache, tp, optimizer=ostate, need_dx=False)
     torch.cuda.synchronize()
     for master0, grad, dev, r in ((mB0, gB, st.master_B, "B"), (mAT0, gAT, st.master_AT, "AT")):
         ost = oracle.AdamWState(np.zeros_like(master0), np.zeros_like(master0))
