@@ -56,8 +56,9 @@ int collm_device_info(int device, int* sm_major, int* sm_minor, int* num_sms);
  *
  * collm_plan_segments (HOST, pure CPU): per 128-row tile the distinct adapters in order of first
  * appearance (tile_slot_ptr[n_tiles+1], slot_adapter[n_slots]) — the LoRA "slots" the GEMM folds
- * into its accumulator — and the shrink work list: segments cut into <=16-row tiles
- * (shrink_tiles[3*i] = row_start, n_rows, adapter).  Capacities are checked (COLLM_EINVAL). */
+ * into its accumulator — and the shrink work list: maximal same-adapter runs cut into <=16-row
+ * tiles (shrink_tiles[3*i] = row_start, n_rows, adapter; base-only runs included with adapter
+ * -1).  Capacities are checked (COLLM_EINVAL). */
 int collm_plan_segments(const int32_t* seg_start, const int32_t* seg_adapter, int n_seg,
                         int n_rows, int32_t* tile_slot_ptr, int32_t* slot_adapter, int slot_cap,
                         int32_t* n_slots, int32_t* shrink_tiles, int shrink_tile_cap,
@@ -70,16 +71,17 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
 
 /* ---- K1: LoRA shrink (SGMV) ------------------------------------------------------------------
  * H[t, g.rank_off + j] = scale[a] * sum_{k in [g.k_lo, g.k_hi)} X[t,k] * A[a][g.rank_off + j, k]
- * for each shrink tile (rows of one adapter a) and each rank group g (groups: n_groups x 4 ints
- * rank_off, n_ranks (multiple of 8, <= 64), k_lo, k_hi).  Outputs (each optional): H32 fp32
- * [T, ldh]; H16 bf16 [T, ldh]; Hslots bf16 [n_slots*128, ldh], row slot_of_row[t]*128 + t%128
- * (the caller zero-fills Hslots first: rows of other adapters stay zero).  `ksplit` >= 1 splits K
- * across CTAs with a deterministic ordered reduction through `workspace`. */
-size_t collm_shrink_workspace_bytes(int n_tiles, int n_groups, int ksplit);
+ * for each shrink tile (rows of one adapter a; a = -1 -> no LoRA, zeros) and each rank group g
+ * (groups: n_groups x 4 ints rank_off, n_ranks (multiple of 8, <= 64), k_lo, k_hi).  Outputs
+ * (each optional): H32 fp32 [T, ldh]; H16 bf16 [T, ldh]; Hslots bf16 [n_slots*128, ldh] — the
+ * GEMM's LoRA slot blocks, written completely: row t's value at row slot_of_row[t]*128 + t%128 and
+ * zeros in the other slots of its 128-row tile (tile_slot_ptr).  One CTA per (tile, group) covers
+ * the whole K range; the reduction is in-CTA and fixed-order (deterministic, no workspace).
+ * Replaces: the inference half of perf.true_infer_latency (perf.py:62-74). */
 int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
                       const int32_t* tiles, int n_tiles, const float* scale, const int32_t* groups,
-                      int n_groups, int ksplit, float* H32, void* H16, int ldh, void* Hslots,
-                      const int32_t* slot_of_row, void* workspace, size_t ws_bytes, void* stream);
+                      int n_groups, float* H32, void* H16, int ldh, void* Hslots,
+                      const int32_t* slot_of_row, const int32_t* tile_slot_ptr, void* stream);
 
 /* ---- K2 / K3: base projection on tcgen05 with the LoRA expand fused into the accumulator ------
  * Y[M,N] = A[M,K] . B[N,K]^T + sum over the LoRA slots s of each 128-row tile of
@@ -91,33 +93,50 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
  * pointers; sub-projection boundaries multiples of the N tile.
  * Forward: A = X, B = W [N,K], Hslots from collm_lora_shrink, LB = adapters' B [n_ad*N, r].
  * Backward dX: A = dY, B = W^T [K_in, N], Hslots = s*dY.B_t [T_tr, R] with one slot per tile,
- *              LB = A_t^T [K_in, R]. */
+ *              LB = A_t^T [K_in, R].
+ * Replaces: perf.true_infer_latency / true_train_latency (perf.py:62-89). */
 int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int ldy, int M, int N,
                     int K, const void* Hslots, int ldh, int h_rows, const void* LB, int ld_lb,
                     int lb_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
                     int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
                     const int32_t* sub_h_col, int bn, void* stream);
 
-/* ---- K5: LoRA weight-gradient reduction with fused AdamW --------------------------------------
- * C[p,q] = sum_t U[t, g.u_off+p] * V[t, g.v_off+q] for each group g (groups: n_groups x 8 ints
- * u_off, P, v_off, Q, c_row_off, c_col_off, t_row_off, t_col_off; Q <= 64; P, Q multiples of 8).
- * Element (p,q) of group g lives at fp32 index (c_row_off+p)*ldc + c_col_off+q of grad / master /
- * m / v and of out_same (bf16), and at (t_row_off+q)*ld_trans + t_col_off+p of out_trans (bf16).
- * mode STORE_GRAD: grad = C*grad_scale (+grad if accum_in).  mode ADAMW: the same gradient drives
+/* ---- K5: LoRA weight-gradient reductions with fused AdamW ------------------------------------
+ * One group = one reduction C[p,q] = sum_t U[t, u_off+p] * V[t, v_off+q] (p < P, q < Q <= 64;
+ * P, Q multiples of 8) and the tensors it updates.  Element (p,q) lives at fp32 index
+ * (c_row_off+p)*ldc + c_col_off+q of grad / master / m / v and of out_same (bf16), and at
+ * (t_row_off+q)*ld_trans + t_col_off+p of out_trans (bf16).  One launch serves all groups of a
+ * projection (dB per sub-projection: U = dY, V = H16; dA^T: U = X_tr, V = dH16).
+ * Replaces: AdapterParams.perturbed (launcher.py:43-47) and perf.train_step (perf.py:111-126). */
+typedef struct {
+  const void* U;     /* bf16 [T, ldu] */
+  const void* V;     /* bf16 [T, ldv] */
+  float* grad;       /* fp32, may be NULL unless STORE_GRAD / accum_in / apply(ADAMW) */
+  float* master;     /* fp32 master weights (ADAMW / COPY_ONLY) */
+  float* m;          /* AdamW first moment */
+  float* v;          /* AdamW second moment */
+  void* out_same;    /* bf16 copy in the master layout, may be NULL */
+  void* out_trans;   /* bf16 transposed copy, may be NULL */
+  int ldu, ldv;
+  int u_off, P, v_off, Q;
+  int ldc, ld_trans;
+  int c_row_off, c_col_off, t_row_off, t_col_off;
+} collm_reduce_group;
+
+/* mode STORE_GRAD: grad = C*grad_scale (+grad if accum_in).  mode ADAMW: the same gradient drives
  * an AdamW step on master/m/v (PyTorch semantics) and the bf16 copies are rewritten.  `adamw` is
  * a DEVICE pointer to 7 floats {lr, beta1, beta2, eps, weight_decay, 1-beta1^step, 1-beta2^step}
- * so a captured CUDA graph can be replayed with a changing step.  Deterministic. */
-size_t collm_reduce_workspace_bytes(const int32_t* groups, int n_groups, int tsplit);
-int collm_lora_reduce(const void* U, int ldu, const void* V, int ldv, int T,
-                      const int32_t* groups, int n_groups, int mode, int accum_in,
-                      float grad_scale, float* grad, int ldc, float* master, float* m, float* v,
-                      void* out_same, void* out_trans, int ld_trans, const float* adamw,
-                      int tsplit, void* workspace, size_t ws_bytes, void* stream);
-/* Elementwise update over the same group table from `grad` (mode ADAMW, e.g. after a cross-
- * replica gradient allreduce) or master -> bf16 copies only (mode COPY_ONLY, after fedavg). */
-int collm_lora_apply(const int32_t* groups, int n_groups, int mode, float* grad, int ldc,
-                     float* master, float* m, float* v, void* out_same, void* out_trans,
-                     int ld_trans, const float* adamw, void* stream);
+ * so a captured CUDA graph can be replayed with a changing step.  Deterministic (split-T partials
+ * reduced in a fixed order by the last-arriving CTA). */
+size_t collm_reduce_workspace_bytes(const collm_reduce_group* groups, int n_groups, int tsplit);
+int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int mode,
+                      int accum_in, float grad_scale, const float* adamw, int tsplit,
+                      void* workspace, size_t ws_bytes, void* stream);
+/* Elementwise update over the same groups from `grad` (mode ADAMW, e.g. after a cross-replica
+ * gradient allreduce) or master -> bf16 copies only (mode COPY_ONLY, after fedavg; replaces
+ * fedavg's result hand-back, launcher.py:68-80 / :226). */
+int collm_lora_apply(const collm_reduce_group* groups, int n_groups, int mode,
+                     const float* adamw, void* stream);
 
 #ifdef __cplusplus
 }

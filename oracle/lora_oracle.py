@@ -108,12 +108,16 @@ def slot_of_row(row_adapter, tile_slot_ptr, slot_adapter, tile_m: int = 128) -> 
 
 
 def shrink_tiles(seg_start, seg_adapter, tile: int = 16) -> np.ndarray:
+    """Maximal runs of equal adapter (base-only runs too, adapter -1), cut into <= tile-row items."""
     out = []
-    for s, a in enumerate(seg_adapter):
-        if a < 0:
-            continue
-        for r in range(seg_start[s], seg_start[s + 1], tile):
-            out.append((r, min(tile, seg_start[s + 1] - r), a))
+    s = 0
+    while s < len(seg_adapter):
+        e = s + 1
+        while e < len(seg_adapter) and seg_adapter[e] == seg_adapter[s]:
+            e += 1
+        for r in range(seg_start[s], seg_start[e], tile):
+            out.append((r, min(tile, seg_start[e] - r), seg_adapter[s]))
+        s = e
     return np.array(out, np.int32).reshape(-1, 3)
 
 

@@ -27,6 +27,17 @@ _SZ = C.c_size_t
 _IP = C.POINTER(C.c_int32)
 _FP = C.POINTER(C.c_float)
 
+class ReduceGroup(C.Structure):
+    """Mirror of ``collm_reduce_group`` (include/collm.h)."""
+
+    _fields_ = [("U", _P), ("V", _P), ("grad", _P), ("master", _P), ("m", _P), ("v", _P),
+                ("out_same", _P), ("out_trans", _P), ("ldu", _I), ("ldv", _I), ("u_off", _I),
+                ("P", _I), ("v_off", _I), ("Q", _I), ("ldc", _I), ("ld_trans", _I),
+                ("c_row_off", _I), ("c_col_off", _I), ("t_row_off", _I), ("t_col_off", _I)]
+
+
+_RGP = C.POINTER(ReduceGroup)
+
 # name -> (restype, argtypes); mirrors include/collm.h one to one (tests check the exports).
 SIGNATURES: dict[str, tuple] = {
     "collm_version": (_I, []),
@@ -34,15 +45,13 @@ SIGNATURES: dict[str, tuple] = {
     "collm_device_info": (_I, [_I, _IP, _IP, _IP]),
     "collm_plan_segments": (_I, [_IP, _IP, _I, _I, _IP, _IP, _I, _IP, _IP, _I, _IP]),
     "collm_expand_segments": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P]),
-    "collm_shrink_workspace_bytes": (_SZ, [_I, _I, _I]),
-    "collm_lora_shrink": (_I, [_P, _I, _P, _LL, _I, _P, _I, _P, _IP, _I, _I, _P, _P, _I, _P, _P,
-                               _P, _SZ, _P]),
+    "collm_lora_shrink": (_I, [_P, _I, _P, _LL, _I, _P, _I, _P, _IP, _I, _P, _P, _I, _P, _P,
+                               _P, _P]),
     "collm_gemm_lora": (_I, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _P,
                              _I, _I, _I, _IP, _IP, _I, _P]),
-    "collm_reduce_workspace_bytes": (_SZ, [_IP, _I, _I]),
-    "collm_lora_reduce": (_I, [_P, _I, _P, _I, _I, _IP, _I, _I, _I, _F, _P, _I, _P, _P, _P, _P,
-                               _P, _I, _P, _I, _P, _SZ, _P]),
-    "collm_lora_apply": (_I, [_IP, _I, _I, _P, _I, _P, _P, _P, _P, _P, _I, _P, _P]),
+    "collm_reduce_workspace_bytes": (_SZ, [_RGP, _I, _I]),
+    "collm_lora_reduce": (_I, [_I, _RGP, _I, _I, _I, _F, _P, _I, _P, _SZ, _P]),
+    "collm_lora_apply": (_I, [_RGP, _I, _I, _P, _P]),
 }
 
 _lib = None

@@ -167,18 +167,23 @@ int collm_plan_segments(const int32_t* seg_start, const int32_t* seg_adapter, in
   }
   if (tile_slot_ptr) tile_slot_ptr[n_tiles] = ns;
   if (n_slots) *n_slots = ns;
+  // shrink work list: maximal runs of equal adapter (roles may differ: rows of one tenant's
+  // prefill and decode requests share the adapter's A) cut into <= 16-row tiles; base-only runs
+  // (adapter -1) are listed too so the shrink zero-fills their slot rows.
   int nt = 0;
-  for (int s = 0; s < n_seg; ++s) {
-    if (seg_adapter[s] < 0) continue;
-    for (int r = seg_start[s]; r < seg_start[s + 1]; r += 16) {
+  for (int s = 0; s < n_seg;) {
+    int e = s + 1;
+    while (e < n_seg && seg_adapter[e] == seg_adapter[s]) ++e;
+    for (int r = seg_start[s]; r < seg_start[e]; r += 16) {
       CHECK_ARG(nt < shrink_tile_cap, "shrink tile capacity %d exceeded", shrink_tile_cap);
       if (shrink_tiles) {
         shrink_tiles[3 * nt + 0] = r;
-        shrink_tiles[3 * nt + 1] = std::min(16, seg_start[s + 1] - r);
+        shrink_tiles[3 * nt + 1] = std::min(16, seg_start[e] - r);
         shrink_tiles[3 * nt + 2] = seg_adapter[s];
       }
       ++nt;
     }
+    s = e;
   }
   if (n_shrink_tiles) *n_shrink_tiles = nt;
   return COLLM_OK;
@@ -203,25 +208,18 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
 constexpr size_t kCounterCap = 1 << 16;
 constexpr size_t kCounterBytes = kCounterCap * sizeof(int32_t);
 
-size_t collm_shrink_workspace_bytes(int n_tiles, int n_groups, int ksplit) {
-  if (ksplit <= 1) return 0;
-  return kCounterBytes + (size_t)ksplit * n_groups * n_tiles * 16 * 64 * sizeof(float);
-}
-
 int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
                       const int32_t* tiles, int n_tiles, const float* scale, const int32_t* groups,
-                      int n_groups, int ksplit, float* H32, void* H16, int ldh, void* Hslots,
-                      const int32_t* slot_of_row, void* workspace, size_t ws_bytes,
-                      void* stream) {
+                      int n_groups, float* H32, void* H16, int ldh, void* Hslots,
+                      const int32_t* slot_of_row, const int32_t* tile_slot_ptr, void* stream) {
   CHECK_ARG(X && A && tiles && scale && groups, "null input");
   CHECK_ARG(n_tiles >= 0, "n_tiles < 0");
   if (n_tiles == 0) return COLLM_OK;
   CHECK_ARG(n_groups >= 1 && n_groups <= kShrinkMaxGroups, "n_groups=%d out of [1,%d]", n_groups,
             kShrinkMaxGroups);
-  CHECK_ARG(ksplit >= 1 && ksplit <= 64, "ksplit=%d out of [1,64]", ksplit);
   CHECK_ARG(ldx % 8 == 0 && lda % 8 == 0 && a_stride % 8 == 0, "ldx/lda/a_stride must be x8");
   CHECK_ARG(aligned16(X) && aligned16(A), "X/A must be 16-byte aligned");
-  CHECK_ARG(!Hslots || slot_of_row, "Hslots needs slot_of_row");
+  CHECK_ARG(!Hslots || (slot_of_row && tile_slot_ptr), "Hslots needs slot_of_row, tile_slot_ptr");
   ShrinkParams p{};
   p.X = (const bf16*)X;
   p.ldx = ldx;
@@ -245,28 +243,23 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
     p.groups[g] = sg;
     max_ranks = std::max(max_ranks, sg.n_ranks);
   }
-  p.ksplit = ksplit;
   p.H32 = H32;
   p.H16 = (bf16*)H16;
   p.ldh = ldh;
   p.Hslots = (bf16*)Hslots;
   p.slot_of_row = slot_of_row;
-  if (ksplit > 1) {
-    const size_t need = collm_shrink_workspace_bytes(n_tiles, n_groups, ksplit);
-    CHECK_ARG(workspace && ws_bytes >= need, "shrink workspace too small: %zu < %zu", ws_bytes,
-              need);
-    CHECK_ARG((size_t)n_groups * n_tiles <= kCounterCap, "too many shrink tiles (%d)", n_tiles);
-    p.counters = (int32_t*)workspace;
-    p.partials = (float*)((char*)workspace + kCounterBytes);
-  }
-  dim3 grid(n_tiles, n_groups, ksplit);
+  p.tile_slot_ptr = tile_slot_ptr;
+  dim3 grid(n_tiles, n_groups);
+  const int threads = kShrinkWarps * 32;
   cudaStream_t st = (cudaStream_t)stream;
   if (max_ranks <= 16)
-    lora_shrink_kernel<2><<<grid, kShrinkWarps * 32, 0, st>>>(p);
+    lora_shrink_kernel<2, 4><<<grid, threads, 0, st>>>(p);
   else if (max_ranks <= 32)
-    lora_shrink_kernel<4><<<grid, kShrinkWarps * 32, 0, st>>>(p);
+    lora_shrink_kernel<4, 3><<<grid, threads, 0, st>>>(p);
+  else if (max_ranks <= 48)
+    lora_shrink_kernel<6, 2><<<grid, threads, 0, st>>>(p);
   else
-    lora_shrink_kernel<8><<<grid, kShrinkWarps * 32, 0, st>>>(p);
+    lora_shrink_kernel<8, 2><<<grid, threads, 0, st>>>(p);
   CUDA_TRY(cudaGetLastError());
   return COLLM_OK;
 }
@@ -370,68 +363,110 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
 }
 
 // ------------------------------------------------------------------------------------ K5
-static int build_reduce_params(ReduceParams& p, const int32_t* groups, int n_groups, int& qmax) {
+static int build_reduce_params(ReduceParams& p, const collm_reduce_group* groups, int n_groups,
+                               int& qmax, bool need_uv) {
   CHECK_ARG(groups && n_groups >= 1 && n_groups <= kReduceMaxGroups, "n_groups=%d out of [1,%d]",
             n_groups, kReduceMaxGroups);
   p.n_groups = n_groups;
   int tiles = 0;
   qmax = 0;
   for (int g = 0; g < n_groups; ++g) {
-    const int32_t* r = groups + 8 * g;
-    ReduceGroup gr{r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], tiles};
+    const collm_reduce_group& s = groups[g];
+    ReduceGroup gr;
+    gr.U = (const bf16*)s.U;
+    gr.V = (const bf16*)s.V;
+    gr.grad = s.grad;
+    gr.master = s.master;
+    gr.m = s.m;
+    gr.v = s.v;
+    gr.out_same = (bf16*)s.out_same;
+    gr.out_trans = (bf16*)s.out_trans;
+    gr.ldu = s.ldu;
+    gr.ldv = s.ldv;
+    gr.u_off = s.u_off;
+    gr.P = s.P;
+    gr.v_off = s.v_off;
+    gr.Q = s.Q;
+    gr.ldc = s.ldc;
+    gr.ld_trans = s.ld_trans;
+    gr.c_row_off = s.c_row_off;
+    gr.c_col_off = s.c_col_off;
+    gr.t_row_off = s.t_row_off;
+    gr.t_col_off = s.t_col_off;
+    gr.tile_begin = tiles;
     CHECK_ARG(gr.P > 0 && gr.P % 8 == 0 && gr.Q > 0 && gr.Q % 8 == 0 && gr.Q <= 64,
               "group %d: P=%d, Q=%d (need multiples of 8, Q <= 64)", g, gr.P, gr.Q);
-    CHECK_ARG(gr.u_off % 8 == 0 && gr.v_off % 8 == 0, "group %d: offsets must be x8", g);
+    if (need_uv) {
+      CHECK_ARG(gr.U && gr.V, "group %d: null U/V", g);
+      CHECK_ARG(gr.u_off % 8 == 0 && gr.v_off % 8 == 0 && gr.ldu % 8 == 0 && gr.ldv % 8 == 0 &&
+                    aligned16(gr.U) && aligned16(gr.V),
+                "group %d: U/V must be 16-byte aligned with x8 offsets/leading dimensions", g);
+    }
+    CHECK_ARG(gr.ldc >= gr.c_col_off + gr.Q, "group %d: ldc=%d too small", g, gr.ldc);
+    CHECK_ARG(gr.ldc % 4 == 0 && gr.c_col_off % 4 == 0,
+              "group %d: ldc and c_col_off must be multiples of 4 (vectorized finalize)", g);
     p.groups[g] = gr;
-    tiles += (gr.P + 63) / 64;
+    tiles += (gr.P + kReducePT - 1) / kReducePT;
     qmax = std::max(qmax, gr.Q);
   }
   p.n_tiles = tiles;
   return COLLM_OK;
 }
 
-size_t collm_reduce_workspace_bytes(const int32_t* groups, int n_groups, int tsplit) {
-  if (tsplit <= 1 || !groups) return 0;
-  int tiles = 0;
-  for (int g = 0; g < n_groups; ++g) tiles += (groups[8 * g + 1] + 63) / 64;
-  return kCounterBytes + (size_t)tsplit * tiles * 64 * 64 * sizeof(float);
+static int check_mode_targets(const ReduceParams& p, int mode, int accum_in) {
+  for (int g = 0; g < p.n_groups; ++g) {
+    const ReduceGroup& gr = p.groups[g];
+    if (mode == COLLM_MODE_STORE_GRAD || accum_in)
+      CHECK_ARG(gr.grad, "group %d: this mode needs grad", g);
+    if (mode == COLLM_MODE_ADAMW) CHECK_ARG(gr.master && gr.m && gr.v, "group %d: ADAMW needs master/m/v", g);
+    if (mode == COLLM_MODE_COPY_ONLY) CHECK_ARG(gr.master, "group %d: COPY_ONLY needs master", g);
+  }
+  return COLLM_OK;
 }
 
-int collm_lora_reduce(const void* U, int ldu, const void* V, int ldv, int T,
-                      const int32_t* groups, int n_groups, int mode, int accum_in,
-                      float grad_scale, float* grad, int ldc, float* master, float* m, float* v,
-                      void* out_same, void* out_trans, int ld_trans, const float* adamw,
-                      int tsplit, void* workspace, size_t ws_bytes, void* stream) {
-  CHECK_ARG(U && V, "null operand");
+size_t collm_reduce_workspace_bytes(const collm_reduce_group* groups, int n_groups, int tsplit) {
+  if (tsplit <= 1 || !groups) return 0;
+  int tiles = 0;
+  for (int g = 0; g < n_groups; ++g) tiles += (groups[g].P + kReducePT - 1) / kReducePT;
+  return kCounterBytes + (size_t)tsplit * tiles * kReducePT * 64 * sizeof(float);
+}
+
+}  // extern "C"
+
+template <int QT>
+static int launch_reduce(const ReduceParams& p, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ReduceSmem<QT>::kTotal));
+    configured = true;
+  }
+  dim3 grid(p.n_tiles, p.tsplit);
+  lora_reduce_kernel<QT><<<grid, kReduceThreads, ReduceSmem<QT>::kTotal, st>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  return COLLM_OK;
+}
+
+extern "C" {
+
+int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int mode,
+                      int accum_in, float grad_scale, const float* adamw, int tsplit,
+                      void* workspace, size_t ws_bytes, void* stream) {
   CHECK_ARG(T >= 1, "T=%d", T);
-  CHECK_ARG(ldu % 8 == 0 && ldv % 8 == 0 && aligned16(U) && aligned16(V),
-            "U/V must be 16-byte aligned with x8 leading dimensions");
   CHECK_ARG(mode == COLLM_MODE_STORE_GRAD || mode == COLLM_MODE_ADAMW, "bad mode %d", mode);
-  CHECK_ARG(mode != COLLM_MODE_STORE_GRAD || grad, "STORE_GRAD needs grad");
-  CHECK_ARG(!accum_in || grad, "accum_in needs grad");
-  CHECK_ARG(mode != COLLM_MODE_ADAMW || (master && m && v && adamw), "ADAMW needs master/m/v");
-  CHECK_ARG(tsplit >= 1 && tsplit <= 128, "tsplit=%d", tsplit);
+  CHECK_ARG(mode != COLLM_MODE_ADAMW || adamw, "ADAMW needs the device argument block");
+  CHECK_ARG(tsplit >= 1 && tsplit <= 256, "tsplit=%d", tsplit);
   ReduceParams p{};
   int qmax = 0;
-  int rc = build_reduce_params(p, groups, n_groups, qmax);
+  int rc = build_reduce_params(p, groups, n_groups, qmax, true);
   if (rc) return rc;
-  p.U = (const bf16*)U;
-  p.ldu = ldu;
-  p.V = (const bf16*)V;
-  p.ldv = ldv;
+  rc = check_mode_targets(p, mode, accum_in);
+  if (rc) return rc;
   p.T = T;
   p.tsplit = tsplit;
   p.mode = mode;
   p.accum_in = accum_in;
   p.grad_scale = grad_scale;
-  p.grad = grad;
-  p.ldc = ldc;
-  p.master = master;
-  p.m = m;
-  p.v = v;
-  p.out_same = (bf16*)out_same;
-  p.out_trans = (bf16*)out_trans;
-  p.ld_trans = ld_trans;
   p.opt = adamw;
   if (tsplit > 1) {
     const size_t need = collm_reduce_workspace_bytes(groups, n_groups, tsplit);
@@ -441,36 +476,25 @@ int collm_lora_reduce(const void* U, int ldu, const void* V, int ldv, int T,
     p.counters = (int32_t*)workspace;
     p.partials = (float*)((char*)workspace + kCounterBytes);
   }
-  dim3 grid(p.n_tiles, tsplit);
   cudaStream_t st = (cudaStream_t)stream;
-  if (qmax <= 16) lora_reduce_kernel<16><<<grid, 128, 0, st>>>(p);
-  else if (qmax <= 32) lora_reduce_kernel<32><<<grid, 128, 0, st>>>(p);
-  else lora_reduce_kernel<64><<<grid, 128, 0, st>>>(p);
-  CUDA_TRY(cudaGetLastError());
-  return COLLM_OK;
+  if (qmax <= 16) return launch_reduce<16>(p, st);
+  if (qmax <= 32) return launch_reduce<32>(p, st);
+  return launch_reduce<64>(p, st);
 }
 
-int collm_lora_apply(const int32_t* groups, int n_groups, int mode, float* grad, int ldc,
-                     float* master, float* m, float* v, void* out_same, void* out_trans,
-                     int ld_trans, const float* adamw, void* stream) {
+int collm_lora_apply(const collm_reduce_group* groups, int n_groups, int mode,
+                     const float* adamw, void* stream) {
   CHECK_ARG(mode == COLLM_MODE_ADAMW || mode == COLLM_MODE_COPY_ONLY, "bad mode %d", mode);
-  CHECK_ARG(master, "null master");
-  CHECK_ARG(mode != COLLM_MODE_ADAMW || (grad && m && v && adamw), "ADAMW needs grad/m/v");
+  CHECK_ARG(mode != COLLM_MODE_ADAMW || adamw, "ADAMW needs the device argument block");
   ReduceParams p{};
   int qmax = 0;
-  int rc = build_reduce_params(p, groups, n_groups, qmax);
+  int rc = build_reduce_params(p, groups, n_groups, qmax, false);
+  if (rc) return rc;
+  rc = check_mode_targets(p, mode, mode == COLLM_MODE_ADAMW);
   if (rc) return rc;
   p.mode = mode;
   p.accum_in = 1;
   p.grad_scale = 1.f;
-  p.grad = grad;
-  p.ldc = ldc;
-  p.master = master;
-  p.m = m;
-  p.v = v;
-  p.out_same = (bf16*)out_same;
-  p.out_trans = (bf16*)out_trans;
-  p.ld_trans = ld_trans;
   p.opt = adamw;
   long long total = 0;
   for (int g = 0; g < n_groups; ++g) total += (long long)p.groups[g].P * p.groups[g].Q;

@@ -144,6 +144,7 @@ class LoraProjection:
         self.train_state: TrainState | None = None
         self._H16: torch.Tensor | None = None
         self._Hslots: torch.Tensor | None = None
+        self._dH16: torch.Tensor | None = None
 
     # ------------------------------------------------------------------ weights / registry
     def refresh_transpose(self) -> None:
@@ -208,9 +209,15 @@ class LoraProjection:
             self._Hslots = torch.zeros(rows, R, dtype=torch.bfloat16, device=self.device)
         return self._H16, self._Hslots
 
+    def _dh_buffer(self, T: int) -> torch.Tensor:
+        if self._dH16 is None or self._dH16.shape[0] < T:
+            self._dH16 = torch.zeros(T, self.spec.R, dtype=torch.bfloat16, device=self.device)
+        return self._dH16[:T]
+
     # ------------------------------------------------------------------ hot path
     def forward(self, X: torch.Tensor, plan: DevicePlan, Y: torch.Tensor | None = None,
                 n_train: int = 0) -> tuple[torch.Tensor, ForwardCache]:
+        """K1 + K2 over all rows of the pass: Y = X.W^T + per-row s_a.(X.A_a^T).B_a^T."""
         spec = self.spec
         T = plan.n_rows
         if X.shape[0] < T or X.shape[1] != spec.in_features:
@@ -221,11 +228,10 @@ class LoraProjection:
         R, rp, K = spec.R, spec.r_pad, spec.in_features
         if plan.n_slots:
             Hs = Hslots[: plan.n_slots * TILE_M]
-            if ops.enabled("lora"):
-                Hs.zero_()
             groups = [(g, min(64, R - g), 0, K) for g in range(0, R, 64)]
             ops.lora_shrink(X, self.A, plan.shrink_tiles, plan.n_shrink_tiles, self.scale, groups,
-                            R, H16=H16, Hslots=Hs, slot_of_row=plan.slot_of_row)
+                            R, H16=H16, Hslots=Hs, slot_of_row=plan.slot_of_row,
+                            tile_slot_ptr=plan.tile_slot_ptr)
             bnd = spec.sub_bounds
             ops.gemm_lora(X, self.W, Y, M=T, Hslots=Hs, h_rows=Hs.shape[0],
                           LB=self.B.view(self.n_adapters * spec.out_features, rp),
@@ -237,15 +243,41 @@ class LoraProjection:
             ops.gemm_lora(X, self.W, Y, M=T)
         return Y, ForwardCache(X=X, H16=H16, n_train=n_train)
 
+    def _grad_groups(self, dY=None, X_tr=None, H_tr=None, dH16=None, *, targets: str):
+        """The K5 group table of this projection: dB per sub-projection (U = dY, V = H16) and
+        dA^T in <=64-wide rank chunks (U = X_tr, V = dH16), with their optimizer targets."""
+        st = self.train_state
+        spec = self.spec
+        K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
+        bnd = spec.sub_bounds
+        full = targets != "grad"
+        groups = []
+        for s in range(len(spec.subs)):
+            groups.append(ops.reduce_group(
+                dY, H_tr, u_off=bnd[s], P=spec.subs[s], v_off=s * rp, Q=rp, ldc=rp,
+                c_row_off=bnd[s], grad=st.grad_B,
+                master=st.master_B if full else None, m=st.m_B if full else None,
+                v=st.v_B if full else None, out_same=self.B[st.adapter] if full else None,
+                out_trans=st.BT16 if full else None, ld_trans=N, t_row_off=s * rp,
+                t_col_off=bnd[s]))
+        for q in range(0, R, 64):
+            groups.append(ops.reduce_group(
+                X_tr, dH16, u_off=0, P=K, v_off=q, Q=min(64, R - q), ldc=R, c_col_off=q,
+                grad=st.grad_AT, master=st.master_AT if full else None,
+                m=st.m_AT if full else None, v=st.v_AT if full else None,
+                out_same=st.AT16 if full else None, out_trans=self.A[st.adapter] if full else None,
+                ld_trans=K, t_row_off=q))
+        return groups
+
     def backward(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan,
                  dX: torch.Tensor | None = None, *, optimizer: OptimizerState | None = None,
                  accumulate: bool = False, grad_scale: float = 1.0,
                  need_dx: bool = True) -> torch.Tensor | None:
         """Backward of the training rows [0, n_train).  ``optimizer`` given -> fused AdamW step
         (after adding the gradient already accumulated when ``accumulate``) using the step the
-        caller already advanced (``OptimizerState.advance``); otherwise the
-        gradient is stored (or added, ``accumulate``) into the grad buffers, e.g. for a
-        cross-replica allreduce followed by :meth:`apply_optimizer`."""
+        caller already advanced (``OptimizerState.advance``); otherwise the gradient is stored (or
+        added, ``accumulate``) into the grad buffers, e.g. for a cross-replica allreduce followed
+        by :meth:`apply_optimizer`."""
         st = self.train_state
         if st is None:
             raise ConfigurationError(f"{self.spec.name}: no trainable adapter (make_trainable)")
@@ -255,7 +287,7 @@ class LoraProjection:
             return None
         K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
         bnd = spec.sub_bounds
-        dH16 = torch.empty(Ttr, R, dtype=torch.bfloat16, device=self.device)
+        dH16 = self._dh_buffer(Ttr)
         # K1: dH = s * dY . B_t, one rank group per sub-projection (its own N range)
         groups = [(s * rp + g, min(64, rp - g), bnd[s], bnd[s + 1])
                   for s in range(len(spec.subs)) for g in range(0, rp, 64)]
@@ -269,57 +301,20 @@ class LoraProjection:
                           tile_slot_ptr=train_plan.tile_slot_ptr,
                           slot_adapter=train_plan.slot_adapter, lora_rank=R,
                           lb_rows_per_adapter=0)
-        # K5: dB = dY^T . H16 (per sub), dA^T = X^T . dH16 — fused AdamW or grad store
-        X_tr = cache.X[:Ttr]
-        H_tr = cache.H16[:Ttr]
-        gB = [(bnd[s], spec.subs[s], s * rp, rp, bnd[s], 0, s * rp, bnd[s])
-              for s in range(len(spec.subs))]
-        gA = [(0, K, q, min(64, R - q), 0, q, q, 0) for q in range(0, R, 64)]
-        if optimizer is not None:
-            args = optimizer.args
-            ops.lora_reduce(dY, H_tr, Ttr, gB, _lib.MODE_ADAMW, accum_in=accumulate,
-                            grad_scale=grad_scale, grad=st.grad_B, ldc=rp, master=st.master_B,
-                            m=st.m_B, v=st.v_B, out_same=self.B[st.adapter], out_trans=st.BT16,
-                            ld_trans=N, adamw=args)
-            ops.lora_reduce(X_tr, dH16, Ttr, gA, _lib.MODE_ADAMW, accum_in=accumulate,
-                            grad_scale=grad_scale, grad=st.grad_AT, ldc=R, master=st.master_AT,
-                            m=st.m_AT, v=st.v_AT, out_same=st.AT16, out_trans=self.A[st.adapter],
-                            ld_trans=K, adamw=args)
-        else:
-            ops.lora_reduce(dY, H_tr, Ttr, gB, _lib.MODE_STORE_GRAD, accum_in=accumulate,
-                            grad_scale=grad_scale, grad=st.grad_B, ldc=rp)
-            ops.lora_reduce(X_tr, dH16, Ttr, gA, _lib.MODE_STORE_GRAD, accum_in=accumulate,
-                            grad_scale=grad_scale, grad=st.grad_AT, ldc=R)
+        # K5: dB = dY^T . H16 (per sub), dA^T = X^T . dH16 — one launch, fused AdamW or grad store
+        rg = self._grad_groups(dY, cache.X[:Ttr], cache.H16[:Ttr], dH16,
+                               targets="full" if optimizer is not None else "grad")
+        mode = _lib.MODE_ADAMW if optimizer is not None else _lib.MODE_STORE_GRAD
+        ops.lora_reduce(Ttr, rg, mode, accum_in=accumulate, grad_scale=grad_scale,
+                        adamw=optimizer.args if optimizer is not None else None,
+                        device=self.device)
         return dX
 
     def apply_optimizer(self, optimizer: OptimizerState) -> None:
         """AdamW from the grad buffers (after a cross-replica allreduce of the gradients)."""
-        st = self.train_state
-        spec = self.spec
-        K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
-        bnd = spec.sub_bounds
-        args = optimizer.args
-        gB = [(bnd[s], spec.subs[s], s * rp, rp, bnd[s], 0, s * rp, bnd[s])
-              for s in range(len(spec.subs))]
-        gA = [(0, K, q, min(64, R - q), 0, q, q, 0) for q in range(0, R, 64)]
-        ops.lora_apply(gB, _lib.MODE_ADAMW, ldc=rp, master=st.master_B, grad=st.grad_B, m=st.m_B,
-                       v=st.v_B, out_same=self.B[st.adapter], out_trans=st.BT16, ld_trans=N,
-                       adamw=args)
-        ops.lora_apply(gA, _lib.MODE_ADAMW, ldc=R, master=st.master_AT, grad=st.grad_AT,
-                       m=st.m_AT, v=st.v_AT, out_same=st.AT16, out_trans=self.A[st.adapter],
-                       ld_trans=K, adamw=args)
+        ops.lora_apply(self._grad_groups(targets="full"), _lib.MODE_ADAMW, adamw=optimizer.args)
 
     def refresh_from_master(self) -> None:
         """Rewrite every bf16 copy of the trainable adapter from the fp32 masters (after a
         parameter average across replicas — the reference's fedavg, launcher.py:68-80)."""
-        st = self.train_state
-        spec = self.spec
-        K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
-        bnd = spec.sub_bounds
-        gB = [(bnd[s], spec.subs[s], s * rp, rp, bnd[s], 0, s * rp, bnd[s])
-              for s in range(len(spec.subs))]
-        gA = [(0, K, q, min(64, R - q), 0, q, q, 0) for q in range(0, R, 64)]
-        ops.lora_apply(gB, _lib.MODE_COPY_ONLY, ldc=rp, master=st.master_B,
-                       out_same=self.B[st.adapter], out_trans=st.BT16, ld_trans=N)
-        ops.lora_apply(gA, _lib.MODE_COPY_ONLY, ldc=R, master=st.master_AT, out_same=st.AT16,
-                       out_trans=self.A[st.adapter], ld_trans=K)
+        ops.lora_apply(self._grad_groups(targets="full"), _lib.MODE_COPY_ONLY)

@@ -103,7 +103,6 @@ class Workspace:
             return buf
 
 
-_shrink_ws = Workspace()
 _reduce_ws = Workspace()
 
 
@@ -111,7 +110,8 @@ def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: 
                 scale: torch.Tensor, groups: list[tuple[int, int, int, int]], ldh: int, *,
                 a_stride: int | None = None, H32: torch.Tensor | None = None,
                 H16: torch.Tensor | None = None, Hslots: torch.Tensor | None = None,
-                slot_of_row: torch.Tensor | None = None, ksplit: int | None = None) -> None:
+                slot_of_row: torch.Tensor | None = None,
+                tile_slot_ptr: torch.Tensor | None = None) -> None:
     """K1: H[t, ranks of g] = scale[a] * X[t, K-range of g] . A_a[ranks of g]^T (see collm.h)."""
     _need(X, torch.bfloat16, "X")
     _need(A, torch.bfloat16, "A")
@@ -120,17 +120,10 @@ def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: 
     lda = A.stride(-2)
     if a_stride is None:
         a_stride = A.stride(0) if A.dim() == 3 else 0
-    if ksplit is None:
-        steps = max(math.ceil((g[3] - g[2]) / 32) for g in groups)
-        want = math.ceil(2 * num_sms(X.device) / (n_tiles * len(groups)))
-        ksplit = max(1, min(want, steps // 8, 32))
-    ws_bytes = _lib.load().collm_shrink_workspace_bytes(n_tiles, len(groups), ksplit)
-    ws = _shrink_ws.get(ws_bytes, X.device)
     flat = [v for g in groups for v in g]
     _lib.call("collm_lora_shrink", X.data_ptr(), X.stride(0), A.data_ptr(), int(a_stride), lda,
               tiles.data_ptr(), n_tiles, scale.data_ptr(), _lib.int_array(flat), len(groups),
-              ksplit, _p(H32), _p(H16), ldh, _p(Hslots), _p(slot_of_row), _p(ws),
-              0 if ws is None else ws.numel(), _stream())
+              _p(H32), _p(H16), ldh, _p(Hslots), _p(slot_of_row), _p(tile_slot_ptr), _stream())
 
 
 def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | None = None,
@@ -162,45 +155,40 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
 
 
 def reduce_tsplit(T: int, n_tiles: int, device: torch.device) -> int:
-    chunks = math.ceil(T / 32)
+    chunks = math.ceil(T / 64)
     want = math.ceil(2 * num_sms(device) / max(1, n_tiles))
-    return max(1, min(want, chunks // 2, 64))
+    return max(1, min(want, chunks // 2, 128))
 
 
-def lora_reduce(U: torch.Tensor, V: torch.Tensor, T: int, groups: list[tuple], mode: int, *,
-                accum_in: bool = False, grad_scale: float = 1.0,
-                grad: torch.Tensor | None = None, ldc: int = 0,
-                master: torch.Tensor | None = None, m: torch.Tensor | None = None,
-                v: torch.Tensor | None = None, out_same: torch.Tensor | None = None,
-                out_trans: torch.Tensor | None = None, ld_trans: int = 0,
-                adamw: torch.Tensor | None = None, tsplit: int | None = None) -> None:
-    """K5: C = U^T V per group -> grad store or fused AdamW (see collm.h)."""
-    _need(U, torch.bfloat16, "U")
-    _need(V, torch.bfloat16, "V")
+def reduce_group(U=None, V=None, *, u_off=0, P, v_off=0, Q, ldc, c_row_off=0, c_col_off=0,
+                 grad=None, master=None, m=None, v=None, out_same=None, out_trans=None,
+                 ld_trans=0, t_row_off=0, t_col_off=0) -> _lib.ReduceGroup:
+    """One ``collm_reduce_group``: C[p,q] = sum_t U[t,u_off+p] V[t,v_off+q] and its targets."""
+    return _lib.ReduceGroup(
+        _p(U), _p(V), _p(grad), _p(master), _p(m), _p(v), _p(out_same), _p(out_trans),
+        U.stride(0) if U is not None else 0, V.stride(0) if V is not None else 0,
+        u_off, P, v_off, Q, ldc, ld_trans, c_row_off, c_col_off, t_row_off, t_col_off)
+
+
+def lora_reduce(T: int, groups: list, mode: int, *, accum_in: bool = False,
+                grad_scale: float = 1.0, adamw: torch.Tensor | None = None,
+                tsplit: int | None = None, device: torch.device | None = None) -> None:
+    """K5: C = U^T V per group -> grad store or fused AdamW, one launch (see collm.h)."""
     if not _launch("lora"):
         return
-    flat = [v_ for g in groups for v_ in g]
-    garr = _lib.int_array(flat)
+    arr = (_lib.ReduceGroup * len(groups))(*groups)
+    device = device or torch.device("cuda", torch.cuda.current_device())
     if tsplit is None:
-        n_tiles = sum(math.ceil(g[1] / 64) for g in groups)
-        tsplit = reduce_tsplit(T, n_tiles, U.device)
-    ws_bytes = _lib.load().collm_reduce_workspace_bytes(garr, len(groups), tsplit)
-    ws = _reduce_ws.get(ws_bytes, U.device)
-    _lib.call("collm_lora_reduce", U.data_ptr(), U.stride(0), V.data_ptr(), V.stride(0), T, garr,
-              len(groups), mode, int(accum_in), float(grad_scale), _p(grad), ldc, _p(master),
-              _p(m), _p(v), _p(out_same), _p(out_trans), ld_trans,
-              _p(adamw), tsplit, _p(ws),
-              0 if ws is None else ws.numel(), _stream())
+        n_tiles = sum(math.ceil(g.P / 128) for g in groups)
+        tsplit = reduce_tsplit(T, n_tiles, device)
+    ws_bytes = _lib.load().collm_reduce_workspace_bytes(arr, len(groups), tsplit)
+    ws = _reduce_ws.get(ws_bytes, device)
+    _lib.call("collm_lora_reduce", T, arr, len(groups), mode, int(accum_in), float(grad_scale),
+              _p(adamw), tsplit, _p(ws), 0 if ws is None else ws.numel(), _stream())
 
 
-def lora_apply(groups: list[tuple], mode: int, *, ldc: int, master: torch.Tensor,
-               grad: torch.Tensor | None = None, m: torch.Tensor | None = None,
-               v: torch.Tensor | None = None, out_same: torch.Tensor | None = None,
-               out_trans: torch.Tensor | None = None, ld_trans: int = 0,
-               adamw: torch.Tensor | None = None) -> None:
+def lora_apply(groups: list, mode: int, *, adamw: torch.Tensor | None = None) -> None:
     if not _launch("lora"):
         return
-    flat = [v_ for g in groups for v_ in g]
-    _lib.call("collm_lora_apply", _lib.int_array(flat), len(groups), mode, _p(grad), ldc,
-              master.data_ptr(), _p(m), _p(v), _p(out_same), _p(out_trans), ld_trans,
-              _p(adamw), _stream())
+    arr = (_lib.ReduceGroup * len(groups))(*groups)
+    _lib.call("collm_lora_apply", arr, len(groups), mode, _p(adamw), _stream())

@@ -94,8 +94,8 @@ def test_gemm_lora_slots(r_pad, n_sub, bn):
     _close_bf16(Y.cpu(), ref)
 
 
-@pytest.mark.parametrize("R,ksplit", [(16, 1), (48, 3), (64, 4), (32, None)])
-def test_shrink(R, ksplit):
+@pytest.mark.parametrize("R", [16, 32, 48, 64, 112])
+def test_shrink(R):
     from paper_2604_16400_b200 import ops
     g = torch.Generator().manual_seed(R)
     T, K, n_ad = 150, 512, 4
@@ -112,7 +112,7 @@ def test_shrink(R, ksplit):
     groups = [(i, min(64, R - i), 0, K) for i in range(0, R, 64)]
     H32 = torch.zeros(T, R, device="cuda")
     H16 = torch.zeros(T, R, dtype=torch.bfloat16, device="cuda")
-    ops.lora_shrink(X, A, tt, len(tiles), scale, groups, R, H32=H32, H16=H16, ksplit=ksplit)
+    ops.lora_shrink(X, A, tt, len(tiles), scale, groups, R, H32=H32, H16=H16)
     torch.cuda.synchronize()
     ref = torch.zeros(T, R)
     for s in range(len(seg_ad)):
@@ -130,30 +130,39 @@ def test_reduce_adamw():
     T, P, Q = 300, 200, 48
     U = _bf(T, P + 8, gen=g)
     V = _bf(T, Q + 16, gen=g)
-    groups = [(8, P, 16, Q, 0, 0, 0, 0)]
     grad = torch.zeros(P, Q, device="cuda")
-    ops.lora_reduce(U, V, T, groups, _lib.MODE_STORE_GRAD, grad=grad, ldc=Q)
+    grp = ops.reduce_group(U, V, u_off=8, P=P, v_off=16, Q=Q, ldc=Q, grad=grad)
+    ops.lora_reduce(T, [grp], _lib.MODE_STORE_GRAD)
     torch.cuda.synchronize()
     ref = U[:, 8:8 + P].float().t() @ V[:, 16:16 + Q].float()
     rel = ((grad - ref).norm() / ref.norm()).item()
     assert rel < 1e-5, rel
-    # fused AdamW from the same reduction, deterministic across runs
+    # fused AdamW from the same reduction, two groups in one launch (second: different T-split)
     master = torch.randn(P, Q, generator=g).cuda()
     m = torch.zeros_like(master)
     v = torch.zeros_like(master)
     same = torch.empty(P, Q, dtype=torch.bfloat16, device="cuda")
     trans = torch.empty(Q, P, dtype=torch.bfloat16, device="cuda")
+    master2 = torch.randn(64, 16, generator=g).cuda()
+    m2, v2 = torch.zeros_like(master2), torch.zeros_like(master2)
+    trans2 = torch.empty(16, 64, dtype=torch.bfloat16, device="cuda")
     lr, b1, b2, eps, wd = 1e-3, 0.9, 0.999, 1e-8, 0.01
     p_ref = master.clone()
-    ops.lora_reduce(U, V, T, groups, _lib.MODE_ADAMW, ldc=Q, master=master, m=m, v=v,
-                    out_same=same, out_trans=trans, ld_trans=P,
-                    adamw=torch.tensor([lr, b1, b2, eps, wd, 1 - b1, 1 - b2]).cuda())
+    p2_ref = master2.clone()
+    groups = [ops.reduce_group(U, V, u_off=8, P=P, v_off=16, Q=Q, ldc=Q, master=master, m=m, v=v,
+                               out_same=same, out_trans=trans, ld_trans=P),
+              ops.reduce_group(U, V, u_off=0, P=64, v_off=0, Q=16, ldc=16, master=master2, m=m2,
+                               v=v2, out_trans=trans2, ld_trans=64)]
+    ops.lora_reduce(T, groups, _lib.MODE_ADAMW,
+                    adamw=torch.tensor([lr, b1, b2, eps, wd, 1 - b1, 1 - b2]).cuda(), tsplit=3)
     torch.cuda.synchronize()
-    gr = ref.cuda()
-    p_ref.mul_(1 - lr * wd)
-    m_ref = (1 - b1) * gr
-    v_ref = (1 - b2) * gr * gr
-    p_ref -= (lr / (1 - b1)) * m_ref / (v_ref.sqrt() / math.sqrt(1 - b2) + eps)
-    assert torch.allclose(master, p_ref, rtol=1e-5, atol=1e-6)
+    for pr, gr, got in ((p_ref, ref.cuda(), master),
+                        (p2_ref, (U[:, :64].float().t() @ V[:, :16].float()).cuda(), master2)):
+        pr.mul_(1 - lr * wd)
+        m_ref = (1 - b1) * gr
+        v_ref = (1 - b2) * gr * gr
+        pr -= (lr / (1 - b1)) * m_ref / (v_ref.sqrt() / math.sqrt(1 - b2) + eps)
+        assert torch.allclose(got, pr, rtol=1e-5, atol=1e-6)
     assert torch.equal(same, master.to(torch.bfloat16))
     assert torch.equal(trans, master.to(torch.bfloat16).t())
+    assert torch.equal(trans2, master2.to(torch.bfloat16).t())
