@@ -94,12 +94,17 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
  * Forward: A = X, B = W [N,K], Hslots from collm_lora_shrink, LB = adapters' B [n_ad*N, r].
  * Backward dX: A = dY, B = W^T [K_in, N], Hslots = s*dY.B_t [T_tr, R] with one slot per tile,
  *              LB = A_t^T [K_in, R].
+ * Persistent stream-K schedule (one CTA per SM): boundary tiles are combined through fp32
+ * partials in `workspace` (zero-filled once; flags are reset by their consumers) in a fixed
+ * order, so results are bitwise deterministic.  collm_gemm_workspace_bytes(bn) sizes it (0 = max).
  * Replaces: perf.true_infer_latency / true_train_latency (perf.py:62-89). */
+size_t collm_gemm_workspace_bytes(int bn);
 int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int ldy, int M, int N,
                     int K, const void* Hslots, int ldh, int h_rows, const void* LB, int ld_lb,
                     int lb_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
                     int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
-                    const int32_t* sub_h_col, int bn, void* stream);
+                    const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
+                    void* stream);
 
 /* ---- K5: LoRA weight-gradient reductions with fused AdamW ------------------------------------
  * One group = one reduction C[p,q] = sum_t U[t, u_off+p] * V[t, v_off+q] (p < P, q < Q <= 64;

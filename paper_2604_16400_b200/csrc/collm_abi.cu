@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -43,6 +44,12 @@ int fail(int code, const char* fmt, ...) {
   do {                                              \
     if (!(cond)) return fail(COLLM_EINVAL, __VA_ARGS__); \
   } while (0)
+
+// Workspace layout shared by the split reductions: [kCounterCap int32 arrival counters][fp32
+// partials].  Counters sit at a fixed prefix so that any launch (whatever its split factor or
+// tile count) finds them zero — kernels restore them to zero, and partials never overlap them.
+constexpr size_t kCounterCap = 1 << 16;
+constexpr size_t kCounterBytes = kCounterCap * sizeof(int32_t);
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -100,7 +107,7 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, ui
 
 template <int BN, int STAGES>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& th,
-                const CUtensorMap& tlb, const GemmLoraParams& p, cudaStream_t stream) {
+                const CUtensorMap& tlb, const GemmLoraParams& p, int grid, cudaStream_t stream) {
   using L = GemmSmem<BN, STAGES>;
   static bool configured = false;
   if (!configured) {
@@ -108,8 +115,6 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
     configured = true;
   }
-  const int tiles = p.num_m_tiles * p.num_n_tiles;
-  const int grid = std::min(tiles, num_sms_cached());
   gemm_lora_kernel<BN, STAGES><<<grid, 256, L::kTotal, stream>>>(ta, tb, th, tlb, p);
   CUDA_TRY(cudaGetLastError());
   return COLLM_OK;
@@ -202,11 +207,7 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
 }
 
 // ------------------------------------------------------------------------------------ K1
-// Workspace layout shared by the split reductions: [kCounterCap int32 arrival counters][fp32
-// partials].  Counters sit at a fixed prefix so that any launch (whatever its split factor or
-// tile count) finds them zero — kernels restore them to zero, and partials never overlap them.
-constexpr size_t kCounterCap = 1 << 16;
-constexpr size_t kCounterBytes = kCounterCap * sizeof(int32_t);
+
 
 int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
                       const int32_t* tiles, int n_tiles, const float* scale, const int32_t* groups,
@@ -265,11 +266,25 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
 }
 
 // ------------------------------------------------------------------------------------ K2/K3
+// debug-only: device pointer of the last GEMM's timeline (COLLM_GEMM_DEBUG set)
+unsigned long long* collm_debug_timeline = nullptr;
+int collm_gemm_debug_copy(void* host_dst, size_t bytes) {
+  if (!collm_debug_timeline) return fail(COLLM_EINVAL, "no GEMM debug timeline (COLLM_GEMM_DEBUG)");
+  CUDA_TRY(cudaMemcpy(host_dst, collm_debug_timeline, bytes, cudaMemcpyDeviceToHost));
+  return COLLM_OK;
+}
+
+size_t collm_gemm_workspace_bytes(int bn) {
+  const int b = bn == 128 ? 128 : 256;
+  return kCounterBytes + (size_t)num_sms_cached() * kGemmBM * b * sizeof(float);
+}
+
 int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int ldy, int M, int N,
                     int K, const void* Hslots, int ldh, int h_rows, const void* LB, int ld_lb,
                     int lb_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
                     int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
-                    const int32_t* sub_h_col, int bn, void* stream) {
+                    const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
+                    void* stream) {
   CHECK_ARG(A && B && Y, "null operand");
   CHECK_ARG(M >= 1 && N >= 1 && K >= 1, "empty GEMM M=%d N=%d K=%d", M, N, K);
   CHECK_ARG(K % 8 == 0 && N % 8 == 0, "K=%d and N=%d must be multiples of 8", K, N);
@@ -280,7 +295,8 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   if (n_sub <= 0) n_sub = 1;
   CHECK_ARG(n_sub <= kMaxSub, "n_sub=%d > %d", n_sub, kMaxSub);
 
-  // N tile: sub-projection boundaries must be tile aligned; prefer the better-filled wave
+  // N tile: 256 unless the sub-projection boundaries (or a narrow N) call for 128; stream-K
+  // removes the wave-quantization reason to prefer narrower tiles.
   const int sms = num_sms_cached();
   auto aligned_to = [&](int t) {
     if (!lora || !sub_n_start) return true;
@@ -289,18 +305,35 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
     return true;
   };
   const int nm = (M + kGemmBM - 1) / kGemmBM;
+  CHECK_ARG(nm <= kMaxMTiles, "M=%d exceeds %d rows", M, kMaxMTiles * kGemmBM);
+  // Schedule choice by a cost model in units of one 128x256 k-block (calibrated on B200:
+  // a 128x128 k-block costs ~0.7 of that — smem-bandwidth bound — a stream-K fix-up ~35, an
+  // exposed epilogue ~4): data-parallel 256-wide, data-parallel 128-wide, or hybrid stream-K.
+  int sched = 0;
+  const char* sched_env = getenv("COLLM_GEMM_SCHED");
   if (bn == 0) {
-    auto eff = [&](int t) {
-      const int tiles = nm * ((N + t - 1) / t);
-      const int waves = (tiles + sms - 1) / sms;
-      // useful fraction: real columns / padded columns times SM occupancy of the waves
-      const double col_eff = (double)N / (((N + t - 1) / t) * t);
-      return col_eff * (double)tiles / (waves * sms) * (t == 256 ? 1.0 : 0.93);
-    };
-    const bool ok256 = aligned_to(256), ok128 = aligned_to(128);
-    if (ok256 && (!ok128 || eff(256) >= eff(128))) bn = 256;
-    else if (ok128) bn = 128;
-    else return fail(COLLM_EINVAL, "sub-projection boundaries are not multiples of 128");
+    const bool ok256 = aligned_to(256) && N > 128, ok128 = aligned_to(128);
+    if (!ok256 && !ok128)
+      return fail(COLLM_EINVAL, "sub-projection boundaries are not multiples of 128");
+    const double nk = (K + kGemmBK - 1) / kGemmBK;
+    const long long t256 = (long long)nm * ((N + 255) / 256);
+    const long long t128 = (long long)nm * ((N + 127) / 128);
+    const double dp256 = ok256 ? ((t256 + sms - 1) / sms) * nk + 4 : 1e30;
+    const double dp128 = ok128 ? ((t128 + sms - 1) / sms) * nk * 0.7 + 4 : 1e30;
+    const double sk256 = ok256 ? (double)t256 * nk / sms + 35 : 1e30;
+    if (sk256 < dp256 && sk256 < dp128) {
+      bn = 256;
+      sched = 1;
+    } else {
+      bn = dp256 <= dp128 ? 256 : 128;
+    }
+  } else {
+    sched = 1;
+  }
+  if (sched_env) {
+    if (strcmp(sched_env, "dp") == 0) sched = 0;
+    if (strcmp(sched_env, "hybrid") == 0) sched = 1;
+    if (strcmp(sched_env, "sknofix") == 0) sched = 2;  // debug only: wrong results
   }
   CHECK_ARG(bn == 128 || bn == 256, "bn must be 0, 128 or 256");
   CHECK_ARG(aligned_to(bn), "sub-projection boundaries are not multiples of bn=%d", bn);
@@ -357,9 +390,25 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
     th = ta;
     tlb = tb;
   }
+  // stream-K grid: one CTA per SM, never more CTAs than k-stages (every range non-empty)
+  const long long min_work = (long long)nm * p.num_n_tiles * ((K + kGemmBK - 1) / kGemmBK);
+  const int grid = (int)std::min<long long>(sms, min_work);
+  p.sched = sched;
+  const size_t need = collm_gemm_workspace_bytes(bn);
+  CHECK_ARG(workspace && ws_bytes >= need, "gemm workspace too small: %zu < %zu", ws_bytes, need);
+  p.flags = (int32_t*)workspace;
+  {
+    static unsigned long long* dbg_ptr = nullptr;
+    const char* dbg_env = getenv("COLLM_GEMM_DEBUG");
+    if (dbg_env && !dbg_ptr) cudaMalloc(&dbg_ptr, 256 * 16 * 8);
+    if (dbg_env) cudaMemsetAsync(dbg_ptr, 0, 256 * 16 * 8, (cudaStream_t)stream);
+    p.dbg = dbg_env ? dbg_ptr : nullptr;
+    collm_debug_timeline = p.dbg;
+  }
+  p.partials = (float*)((char*)workspace + kCounterBytes);
   cudaStream_t st = (cudaStream_t)stream;
-  if (bn == 256) return launch_gemm<256, 4>(ta, tb, th, tlb, p, st);
-  return launch_gemm<128, 6>(ta, tb, th, tlb, p, st);
+  if (bn == 256) return launch_gemm<256, 4>(ta, tb, th, tlb, p, grid, st);
+  return launch_gemm<128, 6>(ta, tb, th, tlb, p, grid, st);
 }
 
 // ------------------------------------------------------------------------------------ K5

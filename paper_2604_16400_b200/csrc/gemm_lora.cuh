@@ -1,5 +1,5 @@
-// gemm_lora.cuh — K2/K3: persistent tcgen05/TMEM GEMM fed by TMA, with the multi-adapter LoRA
-// expand folded into the same TMEM accumulator as extra K-steps ("tensor-core SGMV expand").
+// gemm_lora.cuh — K2/K3: persistent stream-K tcgen05/TMEM GEMM fed by TMA, with the multi-adapter
+// LoRA expand folded into the same TMEM accumulator as extra K-steps ("tensor-core SGMV expand").
 //
 //   Y[M,N] = A[M,K] . B[N,K]^T  +  sum_{slots s of the M-tile}  Hs[s][128, r] . LB_{a(s)}[N, r]^T
 //
@@ -12,13 +12,25 @@
 // Replaces the reference's latency stand-ins `perf.true_infer_latency` / `true_train_latency`
 // (/root/reference/pkg/src/coserve/perf.py:62-89) with the real projection arithmetic.
 //
-// Roles (256 threads, 1 CTA/SM, persistent over tiles, m-fastest raster so W tiles are shared
-// through L2 by the CTAs that run concurrently):
+// Roles (256 threads, 1 CTA/SM, persistent):
 //   warp 0 lane 0 : TMA producer (ring of STAGES smem stages, full/empty mbarriers)
 //   warp 1 lane 0 : tcgen05.mma issuer into a double-buffered TMEM accumulator (2 x BN columns)
 //   warp 2        : TMEM allocator
 //   warps 4..7    : epilogue — tcgen05.ld 32x32b -> bf16 -> st.global, overlapped with the next
-//                   tile's main loop through the second accumulator buffer.
+//                   segment's main loop through the second accumulator buffer.
+//
+// Hybrid data-parallel + stream-K schedule (computed on the device, identically by every role).
+// Tiles are rastered m-fastest, so the CTAs of one data-parallel wave share each W tile through
+// L2.  A tile's work is its k-stages (LoRA slot chunks first, then the K/64 main blocks).  All
+// full waves but the last are data-parallel (CTA c takes tiles c, c+G, ...); the remaining tiles
+// (between one and two waves' worth, or all of them when there is less than one wave) are cut into
+// gridDim.x equal contiguous k-stage ranges ("stream-K"), which removes the wave-quantization
+// tail.  A tile split across CTAs is finished by the CTA holding its last k-stage, which adds the
+// other parts' fp32 partials (written to `partials[cta]`, published with a release flag) in CTA
+// order — bitwise deterministic.  Each CTA walks its stream-K segments in REVERSE order, so the
+// partial it produces is its first stream-K segment and the partials it waits for were produced
+// first by the previous CTAs: no wait chain, no deadlock (all CTAs are co-resident: grid <= #SMs,
+// one CTA per SM).
 #pragma once
 #include "common.cuh"
 
@@ -27,6 +39,7 @@ namespace collm {
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;
 constexpr int kMaxSub = 4;
+constexpr int kMaxMTiles = 2048;
 
 struct GemmLoraParams {
   int M, N, K;
@@ -42,7 +55,19 @@ struct GemmLoraParams {
   int sub_n_start[kMaxSub + 1];  // N boundaries of the sub-projections (multiples of BN)
   int sub_h_col[kMaxSub];        // first H column used by each sub-projection
   int num_m_tiles, num_n_tiles;
+  int sched;  // 0 = data-parallel (round-robin tiles), 1 = hybrid data-parallel + stream-K,
+              // 2 = debug: stream-K split without fix-up (timing experiments only)
+  // ---- stream-K
+  float* partials;  // [gridDim.x][BM*BN] fp32 partial tiles
+  int32_t* flags;   // [gridDim.x] partial-ready flags (0 on entry; consumers reset them)
+  unsigned long long* dbg;  // optional timeline [gridDim.x][16] (globaltimer ns), debug only
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int BN, int STAGES>
 struct GemmSmem {
@@ -50,8 +75,9 @@ struct GemmSmem {
   static constexpr uint32_t kBBytes = BN * kGemmBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
-  static constexpr uint32_t kTotal = kBarOffset + 256 + 1024;  // barriers + alignment slack
-  static constexpr uint32_t kTmemCols = 2 * BN;               // double-buffered fp32 accumulator
+  static constexpr uint32_t kPrefixOffset = kBarOffset + 256;
+  static constexpr uint32_t kTotal = kPrefixOffset + (kMaxMTiles + 1) * 4 + 1024;
+  static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
 };
 
 __device__ __forceinline__ int sub_of_n0(const GemmLoraParams& p, int n0) {
@@ -61,6 +87,92 @@ __device__ __forceinline__ int sub_of_n0(const GemmLoraParams& p, int n0) {
     if (i < p.n_sub && n0 >= p.sub_n_start[i]) s = i;
   return s;
 }
+
+// One contiguous piece of a tile's k-stage list processed by one CTA.
+struct Segment {
+  int m_blk, n_blk;
+  int k0, k1;     // stage range [k0, k1) within the tile
+  int n_lora;     // LoRA stages at the head of this tile's stage list
+  int mode;       // 0 = whole tile, 1 = partial (write partials[cta]), 2 = finish (add parts)
+  int c_first;    // mode 2: the CTAs [c_first, this CTA) hold the earlier parts
+};
+
+struct StreamK {
+  const int32_t* prefix;  // smem: stage prefix over m-tiles (num_m_tiles + 1)
+  int num_m, sum_s;
+  int G;
+  int dp_tiles;           // tiles [0, dp_tiles) are data-parallel
+  long long W_lo, W;      // stream-K region [W_lo, W_lo + W) of the global stage line
+
+  __device__ void init(const int32_t* pre, int nm, int nn, int grid, int sched) {
+    prefix = pre;
+    num_m = nm;
+    sum_s = pre[nm];
+    G = grid;
+    const int tiles = nm * nn;
+    const int waves = tiles / grid;
+    dp_tiles = sched == 0 ? tiles : (waves >= 1 ? (waves - 1) * grid : 0);
+    W_lo = pos_of_tile(dp_tiles);
+    W = (long long)sum_s * nn - W_lo;
+  }
+  __device__ long long pos_of_tile(int t) const {
+    return (long long)(t / num_m) * sum_s + prefix[t % num_m];
+  }
+  __device__ int stages_of_m(int m) const { return prefix[m + 1] - prefix[m]; }
+  __device__ long long bound(int c) const { return W_lo + (long long)c * W / G; }
+  __device__ int cta_of(long long x) const {
+    int c = (int)(((x - W_lo) * G) / W);
+    while (c + 1 < G && bound(c + 1) <= x) ++c;
+    while (c > 0 && bound(c) > x) --c;
+    return c;
+  }
+  // The stream-K segment of CTA c that ends at global position x_end (exclusive).
+  __device__ Segment seg_ending_at(long long x_end, long long range_lo, int c) const {
+    const long long x = x_end - 1;
+    const int n = (int)(x / sum_s);
+    const int r = (int)(x % sum_s);
+    int lo = 0, hi = num_m - 1;  // largest m with prefix[m] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int m = lo;
+    const long long t0 = (long long)n * sum_s + prefix[m];
+    const long long t1 = t0 + stages_of_m(m);
+    const long long s0 = t0 > range_lo ? t0 : range_lo;
+    Segment sg;
+    sg.m_blk = m;
+    sg.n_blk = n;
+    sg.k0 = (int)(s0 - t0);
+    sg.k1 = (int)(x_end - t0);
+    const bool first = s0 == t0, last = x_end == t1;
+    sg.mode = (first && last) ? 0 : (last ? 2 : 1);
+    sg.c_first = (sg.mode == 2) ? cta_of(t0) : c;
+    sg.n_lora = 0;
+    return sg;
+  }
+  // Visit this CTA's work: its data-parallel tiles, then its stream-K segments in reverse.
+  template <class F>
+  __device__ void for_each(int c, F&& f) const {
+    for (int t = c; t < dp_tiles; t += G) {
+      Segment sg;
+      sg.m_blk = t % num_m;
+      sg.n_blk = t / num_m;
+      sg.k0 = 0;
+      sg.k1 = stages_of_m(sg.m_blk);
+      sg.mode = 0;
+      sg.c_first = c;
+      sg.n_lora = 0;
+      f(sg);
+    }
+    const long long lo = bound(c);
+    for (long long x_end = bound(c + 1); x_end > lo;) {
+      const Segment sg = seg_ending_at(x_end, lo, c);
+      x_end -= sg.k1 - sg.k0;
+      f(sg);
+    }
+  }
+};
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
@@ -76,13 +188,25 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* fixbar = tempty + 2;  // stream-K fix-up: bulk copy of one partial into the stages
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixbar + 1);
+  int32_t* s_prefix = reinterpret_cast<int32_t*>(smem + L::kPrefixOffset);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const bool has_lora = p.tile_slot_ptr != nullptr;
+  const int nk = (p.K + BK - 1) / BK;
 
+  // per-m-tile stage counts -> prefix (every role needs it for the schedule)
   if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int m = 0; m < p.num_m_tiles; ++m) {
+      s_prefix[m] = acc;
+      const int nl =
+          has_lora ? (p.tile_slot_ptr[m + 1] - p.tile_slot_ptr[m]) * p.lora_chunks : 0;
+      acc += nl + nk;
+    }
+    s_prefix[p.num_m_tiles] = acc;
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     if (has_lora) {
@@ -97,6 +221,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
     }
+    mbar_init(fixbar, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<L::kTmemCols>(tmem_slot);
@@ -105,41 +230,41 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
-  const int nk = (p.K + BK - 1) / BK;
+  StreamK sk;
+  sk.init(s_prefix, p.num_m_tiles, p.num_n_tiles, gridDim.x, p.sched);
+  const int cta = blockIdx.x;
+  auto lora_stages = [&](int m) {
+    return has_lora ? (p.tile_slot_ptr[m + 1] - p.tile_slot_ptr[m]) * p.lora_chunks : 0;
+  };
 
   if (warp == 0 && lane == 0) {
     // ===================== TMA producer =====================
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m_blk = tile % p.num_m_tiles, n_blk = tile / p.num_m_tiles;
-      const int m0 = m_blk * BM, n0 = n_blk * BN;
-      if (has_lora) {
-        const int s_beg = p.tile_slot_ptr[m_blk], s_end = p.tile_slot_ptr[m_blk + 1];
-        const int hcol = p.sub_h_col[sub_of_n0(p, n0)];
-        const uint32_t rc = p.lora_rc;
-        for (int s = s_beg; s < s_end; ++s) {
-          const int lb_row = p.slot_adapter[s] * p.lb_rows_per_adapter + n0;
-          for (int c = 0; c < p.lora_chunks; ++c) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sa = smem + stage * L::kStageBytes;
-            mbar_arrive_expect_tx(&full[stage], (BM + BN) * rc * 2);
-            tma_load_2d(sa, &tmH, &full[stage], hcol + c * rc, s * BM);
-            tma_load_2d(sa + L::kABytes, &tmLB, &full[stage], c * rc, lb_row);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          }
-        }
-      }
-      for (int kb = 0; kb < nk; ++kb) {
+    sk.for_each(cta, [&](const Segment& sg) {
+      const int m0 = sg.m_blk * BM, n0 = sg.n_blk * BN;
+      const int n_lora = lora_stages(sg.m_blk);
+      const int hcol = has_lora ? p.sub_h_col[sub_of_n0(p, n0)] : 0;
+      const uint32_t rc = p.lora_rc;
+      for (int i = sg.k0; i < sg.k1; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * L::kStageBytes;
-        mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-        tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
-        tma_load_2d(sa + L::kABytes, &tmB, &full[stage], kb * BK, n0);
+        if (i < n_lora) {
+          const int s = p.tile_slot_ptr[sg.m_blk] + i / p.lora_chunks;
+          const int c = i % p.lora_chunks;
+          const int lb_row = p.slot_adapter[s] * p.lb_rows_per_adapter + n0;
+          mbar_arrive_expect_tx(&full[stage], (BM + BN) * rc * 2);
+          tma_load_2d(sa, &tmH, &full[stage], hcol + c * rc, s * BM);
+          tma_load_2d(sa + L::kABytes, &tmLB, &full[stage], c * rc, lb_row);
+        } else {
+          const int kb = i - n_lora;
+          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+          tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
+          tma_load_2d(sa + L::kABytes, &tmB, &full[stage], kb * BK, n0);
+        }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-    }
+    });
   } else if (warp == 1 && lane == 0) {
     // ===================== tcgen05.mma issuer =====================
     constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
@@ -147,38 +272,30 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t phase = 0;
     uint32_t acc = 0, acc_phase = 0;
     const uint32_t smem_base = smem_u32(smem);
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m_blk = tile % p.num_m_tiles;
+    const uint32_t lrow = p.lora_rc * 2, lsteps = p.lora_rc / 16;
+    sk.for_each(cta, [&](const Segment& sg) {
+      const int n_lora = lora_stages(sg.m_blk);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       uint32_t accumulate = 0;
-      if (has_lora) {
-        const int n_lora = (p.tile_slot_ptr[m_blk + 1] - p.tile_slot_ptr[m_blk]) * p.lora_chunks;
-        const uint32_t row_bytes = p.lora_rc * 2;
-        const uint32_t ksteps = p.lora_rc / 16;
-        for (int i = 0; i < n_lora; ++i) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sa = smem_base + stage * L::kStageBytes;
-          for (uint32_t k = 0; k < ksteps; ++k) {
-            umma_bf16(d_tmem, umma_desc_kmajor(sa + k * 32, row_bytes),
-                      umma_desc_kmajor(sa + L::kABytes + k * 32, row_bytes), idesc, accumulate);
-            accumulate = 1;
-          }
-          umma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-      for (int kb = 0; kb < nk; ++kb) {
+      for (int i = sg.k0; i < sg.k1; ++i) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         const uint32_t sa = smem_base + stage * L::kStageBytes;
+        if (i < n_lora) {
+          for (uint32_t k = 0; k < lsteps; ++k) {
+            umma_bf16(d_tmem, umma_desc_kmajor(sa + k * 32, lrow),
+                      umma_desc_kmajor(sa + L::kABytes + k * 32, lrow), idesc, accumulate);
+            accumulate = 1;
+          }
+        } else {
 #pragma unroll
-        for (uint32_t k = 0; k < BK / 16; ++k) {
-          umma_bf16(d_tmem, umma_desc_kmajor(sa + k * 32, 128),
-                    umma_desc_kmajor(sa + L::kABytes + k * 32, 128), idesc, accumulate);
-          accumulate = 1;
+          for (uint32_t k = 0; k < BK / 16; ++k) {
+            umma_bf16(d_tmem, umma_desc_kmajor(sa + k * 32, 128),
+                      umma_desc_kmajor(sa + L::kABytes + k * 32, 128), idesc, accumulate);
+            accumulate = 1;
+          }
         }
         umma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -186,23 +303,101 @@ __global__ void __launch_bounds__(256, 1)
       umma_commit(&tfull[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    }
+    });
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew+32)
-    uint32_t acc = 0, acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m_blk = tile % p.num_m_tiles, n_blk = tile / p.num_m_tiles;
-      const int row = m_blk * BM + ew * 32 + lane;
-      const int n0 = n_blk * BN;
+    const int tid = threadIdx.x - 128;
+    uint32_t acc = 0, acc_phase = 0, fix_phase = 0;
+    int seg_i = 0;
+    unsigned long long* dbg = p.dbg ? p.dbg + (size_t)cta * 16 : nullptr;
+    if (dbg && tid == 0) dbg[0] = gtimer();
+    sk.for_each(cta, [&](const Segment& sg_in) {
+      Segment sg = sg_in;
+      if (p.sched == 2) sg.mode = 0;  // debug: stream-K split without the fix-up (timing only)
+      const int lrow_i = ew * 32 + lane;
+      const int row = sg.m_blk * BM + lrow_i;
+      const int n0 = sg.n_blk * BN;
+      if (dbg && tid == 0 && seg_i < 3) dbg[1 + 4 * seg_i] = gtimer() | ((unsigned long long)sg.mode << 60);
+      if (sg.mode == 2) {  // wait for the earlier parts of this tile (produced first by their CTAs)
+        if (tid == 0) {
+          for (int c = sg.c_first; c < cta; ++c) {
+            if (sk.bound(c) == sk.bound(c + 1)) continue;  // empty range: no part
+            const int32_t* f = p.flags + c;
+            uint32_t v;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            } while (v == 0);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (dbg && tid == 0 && seg_i < 3) dbg[2 + 4 * seg_i] = gtimer();
+      // Finishing segment = this CTA's last: the MMAs are done with the pipeline smem, so the
+      // first earlier part is pulled in with one bulk copy (the rest stream from L2).
+      int smem_part = -1;
+      if (sg.mode == 2) {
+        for (int pc = sg.c_first; pc < cta; ++pc)
+          if (sk.bound(pc) != sk.bound(pc + 1)) { smem_part = pc; break; }
+        if (smem_part >= 0) {
+          if (tid == 0) {
+            mbar_arrive_expect_tx(fixbar, BM * BN * 4);
+            bulk_copy_g2s(smem, p.partials + (size_t)smem_part * (BM * BN), BM * BN * 4, fixbar);
+          }
+          mbar_wait(fixbar, fix_phase);
+          fix_phase ^= 1;
+        }
+      }
       bf16* yrow = p.Y + (size_t)row * p.ldy;
+      // partial tiles are stored in the epilogue's own thread order — float4 index
+      // ((chunk * 8 + j) * 128 + tid) — so writes and reads are 512 B-coalesced per warp
+      float4* part_mine = reinterpret_cast<float4*>(p.partials + (size_t)cta * (BM * BN)) + tid;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c, r);
         tmem_wait_ld();
+        const int chunk = c >> 5;
+        if (sg.mode == 1) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            __stcg(part_mine + (chunk * 8 + j) * 128,
+                   make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+          continue;
+        }
+        if (sg.mode == 2) {
+          if (smem_part >= 0) {
+            const float4* src = reinterpret_cast<const float4*>(smem) + tid + chunk * 8 * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 v = src[j * 128];
+              r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + v.x);
+              r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + v.y);
+              r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + v.z);
+              r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
+            }
+          }
+          for (int pc = sg.c_first; pc < cta; ++pc) {
+            if (pc == smem_part || sk.bound(pc) == sk.bound(pc + 1)) continue;
+            const float4* src =
+                reinterpret_cast<const float4*>(p.partials + (size_t)pc * (BM * BN)) + tid +
+                chunk * 8 * 128;
+            float4 v8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v8[j] = __ldcg(src + j * 128);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 v = v8[j];
+              r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + v.x);
+              r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + v.y);
+              r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + v.z);
+              r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
+            }
+          }
+        }
         if (row < p.M) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -222,7 +417,21 @@ __global__ void __launch_bounds__(256, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    }
+      if (sg.mode == 1) {  // publish the partial
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (tid == 0)
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.flags + cta), "r"(1u)
+                       : "memory");
+      } else if (sg.mode == 2) {  // consumed: reset the producers' flags for the next launch
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (tid == 0)
+          for (int c = sg.c_first; c < cta; ++c) p.flags[c] = 0;
+      }
+      if (dbg && tid == 0 && seg_i < 3) dbg[3 + 4 * seg_i] = gtimer();
+      ++seg_i;
+    });
+    if (dbg && tid == 0) dbg[13] = gtimer();
   }
 
   tc_fence_before();

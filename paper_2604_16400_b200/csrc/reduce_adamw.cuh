@@ -24,7 +24,7 @@ namespace collm {
 
 constexpr int kReduceMaxGroups = 8;
 constexpr int kReducePT = 128;     // P rows per CTA tile (8 warps x 16)
-constexpr int kReduceTC = 64;      // T rows per pipeline stage
+constexpr int kReduceTC = 32;      // T rows per pipeline stage
 constexpr int kReduceStages = 4;   // cp.async ring depth
 constexpr int kReduceThreads = 256;
 

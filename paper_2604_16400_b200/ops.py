@@ -104,6 +104,7 @@ class Workspace:
 
 
 _reduce_ws = Workspace()
+_gemm_ws = Workspace()
 
 
 def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: int,
@@ -144,6 +145,7 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
         return
     lora = tile_slot_ptr is not None
     n_sub = len(sub_n_start) - 1 if (lora and sub_n_start) else 1
+    ws = _gemm_ws.get(_lib.load().collm_gemm_workspace_bytes(0), A.device)
     _lib.call(
         "collm_gemm_lora", A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), Y.data_ptr(),
         Y.stride(0), M, N, K,
@@ -151,13 +153,15 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
         _p(LB) if lora else None, LB.stride(-2) if lora else 0, lb_rows,
         _p(tile_slot_ptr), _p(slot_adapter), lora_rank, lb_rows_per_adapter, n_sub,
         _lib.int_array(sub_n_start) if (lora and sub_n_start) else None,
-        _lib.int_array(sub_h_col) if (lora and sub_h_col) else None, bn, _stream())
+        _lib.int_array(sub_h_col) if (lora and sub_h_col) else None, bn, _p(ws),
+        0 if ws is None else ws.numel(), _stream())
 
 
 def reduce_tsplit(T: int, n_tiles: int, device: torch.device) -> int:
-    chunks = math.ceil(T / 64)
-    want = math.ceil(2 * num_sms(device) / max(1, n_tiles))
-    return max(1, min(want, chunks // 2, 128))
+    # one wave: the kernel keeps 4 CTAs/SM resident; keep >= 3 32-row chunks per split
+    chunks = math.ceil(T / 32)
+    want = (4 * num_sms(device)) // max(1, n_tiles)
+    return max(1, min(want, chunks // 3, 128))
 
 
 def reduce_group(U=None, V=None, *, u_off=0, P, v_off=0, Q, ldc, c_row_off=0, c_col_off=0,
