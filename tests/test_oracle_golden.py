@@ -1,0 +1,107 @@
+"""CPU: the oracle against its golden fixtures (tests/golden, made by make_golden.py).
+
+* fedavg / adapter layout: bit-exact against outputs of the reference's own launcher.fedavg and
+  AdapterParams.zeros (/root/reference/pkg/src/coserve/launcher.py:28-80).
+* LoRA forward/backward: against an independent torch-float64-autograd formulation.  Y and dB
+  share the oracle's rounding points exactly (rel 1e-12); dX and dA differ by the bf16 rounding of
+  dH that the device algorithm applies and autograd does not (rel <= 1e-2).
+* the reference's own FedAvg property tests (tests/test_launcher.py:41-82) re-run on the oracle.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def test_bf16_rounding_matches_torch():
+    import torch
+    g = np.random.default_rng(0)
+    x = np.concatenate([g.standard_normal(10000).astype(np.float32) * 10 ** g.uniform(-8, 8, 10000)
+                        .astype(np.float32), np.array([0.0, -0.0, 1e38, -1e38, 65504.0], np.float32)])
+    ref = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(oracle.bf16_round(x), ref)
+
+
+def test_fedavg_matches_reference_bitwise():
+    d = np.load(os.path.join(GOLD, "fedavg_ref.npz"))
+    ci = 0
+    while f"case{ci}_k" in d:
+        k = int(d[f"case{ci}_k"])
+        clients = [(d[f"case{ci}_b{j}"], d[f"case{ci}_a{j}"]) for j in range(k)]
+        b, a = oracle.fedavg(clients)
+        assert np.array_equal(b, d[f"case{ci}_mean_b"]) and np.array_equal(a, d[f"case{ci}_mean_a"])
+        ci += 1
+    assert ci == 5
+    # adapter layout convention: b_mat (d, r), a_mat (r, l)
+    assert tuple(d["zeros_b_shape"]) == (64, 8) and tuple(d["zeros_a_shape"]) == (8, 48)
+
+
+def test_fedavg_reference_properties():
+    """The reference's FedAvg tests (tests/test_launcher.py:41-82) on the oracle."""
+    g = np.random.default_rng(3)
+
+    def ad(d=8, l=8, r=2):
+        return g.normal(size=(d, r)), g.normal(size=(r, l))
+
+    one = ad()
+    out = oracle.fedavg([one])
+    assert out[0] is one[0] and out[1] is one[1]  # single client: same objects back
+    z = (np.zeros((4, 2)), np.zeros((2, 4)))
+    t = (np.full((4, 2), 2.0), np.full((2, 4), 2.0))
+    b, a = oracle.fedavg([z, t])
+    assert np.all(b == 1.0) and np.all(a == 1.0)
+    with pytest.raises(oracle.AggregationError, match="client 1"):
+        oracle.fedavg([ad(d=8), ad(d=4)])
+    for _ in range(200):
+        k = int(g.integers(1, 6))
+        cl = [ad(4, 4, 2) for _ in range(k)]
+        b, a = oracle.fedavg(cl)
+        perm = [cl[i] for i in g.permutation(k)]
+        b2, a2 = oracle.fedavg(perm)
+        assert np.allclose(b, b2, atol=1e-12) and np.allclose(a, a2, atol=1e-12)
+        st = np.stack([c[0] for c in cl])
+        assert np.all(b <= st.max(0) + 1e-12) and np.all(b >= st.min(0) - 1e-12)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_lora_oracle_vs_autograd(seed):
+    d = np.load(os.path.join(GOLD, "lora_autograd.npz"))
+    p = f"s{seed}_"
+    meta = d[p + "meta"]
+    K, r, r_pad, n_ad, T_tr, ta = (int(v) for v in meta[:6])
+    subs = tuple(int(v) for v in meta[6:])
+    f = lambda k: oracle.bits_to_f32(d[p + k])  # noqa: E731
+    X, W, A, B, dY = f("X"), f("W"), f("A"), f("B"), f("dY")
+    scale, row_ad = d[p + "scale"], d[p + "row_ad"]
+    Y, H16 = oracle.lora_forward(X, W, A, B, scale, row_ad, subs, r_pad)
+    assert _rel(Y, d[p + "Y"]) < 1e-12
+    dX, dB, dAT, _ = oracle.lora_backward(dY, X[:T_tr], H16[:T_tr], W, A[ta], B[ta],
+                                          float(scale[ta]), subs, r_pad)
+    assert _rel(dB, d[p + "dB"]) < 1e-12
+    assert _rel(dAT.T, d[p + "dA"]) < 1e-2
+    assert _rel(dX, d[p + "dX"]) < 1e-2
+
+
+def test_adamw_matches_torch():
+    import torch
+    g = np.random.default_rng(1)
+    p0 = g.standard_normal((16, 8)).astype(np.float32)
+    st = oracle.AdamWState(np.zeros_like(p0), np.zeros_like(p0))
+    tp = torch.nn.Parameter(torch.from_numpy(p0.copy()))
+    opt = torch.optim.AdamW([tp], lr=1e-3, weight_decay=0.01, foreach=False)
+    p = p0
+    for _ in range(5):
+        gr = g.standard_normal((16, 8)).astype(np.float32)
+        p = oracle.adamw_step(p, gr, st, lr=1e-3, wd=0.01)
+        tp.grad = torch.from_numpy(gr)
+        opt.step()
+    assert np.allclose(p, tp.detach().numpy(), rtol=1e-6, atol=1e-7)

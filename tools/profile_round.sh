@@ -1,0 +1,16 @@
+#!/bin/bash
+# Round profile capture (run under gpurun, 1 GPU): launch list of one step, per-launch DRAM bytes +
+# tensor-pipe activity for the whole step, and --set full captures of the key kernels.
+# usage: bash tools/profile_round.sh r01 [config]
+TAG=${1:-r01}; CFG=${2:-llama2-7b}; OUT=gpurun_out/$TAG; mkdir -p $OUT
+N=641
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_lora|lora_|expand_" \
+    -s $N -c $N --csv --log-file $OUT/launches_$CFG.csv python tools/profile_step.py --config $CFG 2>&1 | tail -1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed \
+    --clock-control none -k regex:"gemm_lora|lora_|expand_" -s $N -c $N --csv --log-file $OUT/metrics_$CFG.csv \
+    python tools/profile_step.py --config $CFG 2>&1 | tail -1
+# full sets: qkv forward GEMM (launch 2 of the step), its shrink (1), first dX GEMM, first reduce
+ncu --set full --clock-control none --import-source on -k regex:"gemm_lora" -s 256 -c 1 -o $OUT/full_gemm_fwd_qkv python tools/profile_step.py --config $CFG 2>&1 | tail -1
+ncu --set full --clock-control none --import-source on -k regex:"gemm_lora" -s 384 -c 1 -o $OUT/full_gemm_dx_down python tools/profile_step.py --config $CFG 2>&1 | tail -1
+ncu --set full --clock-control none --import-source on -k regex:"lora_shrink" -s 256 -c 1 -o $OUT/full_shrink_fwd_qkv python tools/profile_step.py --config $CFG 2>&1 | tail -1
+ncu --set full --clock-control none --import-source on -k regex:"lora_reduce" -s 128 -c 1 -o $OUT/full_reduce_down python tools/profile_step.py --config $CFG 2>&1 | tail -1
