@@ -250,18 +250,35 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
   p.Hslots = (bf16*)Hslots;
   p.slot_of_row = slot_of_row;
   p.tile_slot_ptr = tile_slot_ptr;
-  dim3 grid(n_tiles, n_groups);
-  const int threads = kShrinkWarps * 32;
-  cudaStream_t st = (cudaStream_t)stream;
+  // cluster size: split K across up to 8 CTAs so the grid fills two resident CTAs per SM
+  int csize = 1;
+  const int sms = num_sms_cached();
+  while (csize < 8 && (long long)n_tiles * n_groups * csize * 2 <= 2LL * sms) csize *= 2;
+  {
+    const char* env = getenv("COLLM_SHRINK_CLUSTER");
+    if (env) csize = std::max(1, std::min(8, atoi(env)));
+  }
+  p.csize = csize;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(n_tiles * csize, n_groups);
+  cfg.blockDim = dim3(kShrinkWarps * 32);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (max_ranks <= 16)
-    lora_shrink_kernel<2, 4><<<grid, threads, 0, st>>>(p);
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_kernel<2, 4>, p));
   else if (max_ranks <= 32)
-    lora_shrink_kernel<4, 3><<<grid, threads, 0, st>>>(p);
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_kernel<4, 3>, p));
   else if (max_ranks <= 48)
-    lora_shrink_kernel<6, 2><<<grid, threads, 0, st>>>(p);
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_kernel<6, 2>, p));
   else
-    lora_shrink_kernel<8, 2><<<grid, threads, 0, st>>>(p);
-  CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_kernel<8, 2>, p));
   return COLLM_OK;
 }
 

@@ -130,7 +130,7 @@ __device__ __forceinline__ bf16 finalize_elem(const ReduceParams& p, const Reduc
 // issues all loads (partials, grad, m, v, master) of UNR groups before using any of them, so the
 // tail of the split reduction runs at memory parallelism instead of one latency per element.
 // `cs` is the CTA's own tile in shared memory (tsplit == 1) or null (sum the global partials).
-template <int QT, int UNR = 2>
+template <int QT, int UNR = 1>
 __device__ __forceinline__ void finalize_tile(const ReduceParams& p, const ReduceGroup& gr, int p0,
                                               int prow, const float (*cs)[QT + 1],
                                               const float* parts, size_t part_stride,
@@ -233,7 +233,7 @@ struct ReduceSmem {
 };
 
 template <int QT>
-__global__ void __launch_bounds__(kReduceThreads) lora_reduce_kernel(const ReduceParams p) {
+__global__ void __launch_bounds__(kReduceThreads, 3) lora_reduce_kernel(const ReduceParams p) {
   using S = ReduceSmem<QT>;
   constexpr int PT = kReducePT, TC = kReduceTC, ST = kReduceStages;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -333,16 +333,17 @@ __global__ void __launch_bounds__(kReduceThreads) lora_reduce_kernel(const Reduc
   if (p.tsplit > 1) {
     float* mine = p.partials + ((size_t)ts * p.n_tiles + tile) * (PT * 64);
     for (int e = threadIdx.x; e < n_el; e += kReduceThreads) mine[e] = Cs[e / Q][e % Q];
-    __threadfence();
-    __syncthreads();
+    __syncthreads();  // CTA-scope: all partial stores happen-before thread 0's cumulative fence
     if (threadIdx.x == 0) {
+      __threadfence();
       const int prev = atomicAdd(p.counters + tile, 1);
       s_last = (prev == p.tsplit - 1);
       if (s_last) p.counters[tile] = 0;
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
+    if (threadIdx.x == 0) __threadfence();  // acquire side of the arrival counter
+    __syncthreads();
     finalize_tile<QT>(p, gr, p0, prow, nullptr, p.partials + (size_t)tile * (PT * 64),
                       (size_t)p.n_tiles * (PT * 64), Ct, trans);
   } else {

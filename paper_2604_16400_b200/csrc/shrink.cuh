@@ -7,26 +7,29 @@
 //           sub-projection (its own N range) -> dH = s * dY . B_t.
 //
 // Work unit = one "row tile" (<= 16 consecutive rows of ONE adapter, planned on the host from the
-// segment table) x one rank group, over the FULL K range: one CTA of 16 warps per work unit, the
-// warps interleaving 32-wide K steps.  Each warp streams X and the adapter's rank rows with 128-bit
-// loads and feeds them straight into mma.sync m16n8k16: the reduction index k is permuted
-// identically for both operands so that each lane's 16-byte vector IS its fragment (no
-// shared-memory staging, no ldmatrix).  Loads for UNR consecutive K steps are issued before any
-// MMA, so every lane keeps (2 + NT) * UNR 16-byte requests in flight.  The 16 warp partials are
-// reduced through shared memory in a fixed order (deterministic; no atomics, no cross-CTA
-// workspace).  CUDA-core FMAs cannot keep up with HBM here: X at 6.5 TB/s is 3.3 G elements/s and
-// every element needs R >= 16 FMAs, i.e. > 50 TFMA/s.
+// segment table) x one rank group.  A thread-block cluster of C CTAs (C = 1..8, chosen so the
+// grid fills the SMs) covers the unit's K range, each CTA a contiguous 1/C of it with its 8 warps
+// interleaving 32-wide K steps.  Each warp streams X and the adapter's rank rows with 128-bit
+// loads straight into mma.sync m16n8k16: the reduction index k is permuted identically for both
+// operands so each lane's 16-byte vector IS its fragment (no shared-memory staging, no ldmatrix).
+// Loads for UNR K steps are issued before any MMA, so every lane keeps (2 + NT) * UNR 16-byte
+// requests in flight.  Warp partials reduce through shared memory, the C CTA partials through
+// distributed shared memory (rank 0 sums ranks 0..C-1 in order): deterministic, no atomics, no
+// global workspace.  CUDA-core FMAs cannot keep up with HBM here: X at 6.5 TB/s is 3.3 G
+// elements/s and every element needs R >= 16 FMAs, i.e. > 50 TFMA/s.
 //
 // The Hslots output (the GEMM's LoRA slot blocks) is written completely by this kernel: each row
 // writes its value into its own adapter's slot and zeros into the other slots of its 128-row tile
 // (rows of base-only segments, adapter -1, write zeros everywhere), so no memset is needed.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace collm {
 
 constexpr int kShrinkMaxGroups = 8;
-constexpr int kShrinkWarps = 16;
+constexpr int kShrinkWarps = 8;
 
 struct ShrinkGroup {
   int rank_off;  // first rank row (and H column) of the group
@@ -52,6 +55,7 @@ struct ShrinkParams {
   bf16* Hslots;  // [n_slots*128, ldh] — row (slot*128 + t%128)
   const int32_t* slot_of_row;
   const int32_t* tile_slot_ptr;  // slot range of each 128-row tile (for the zero fill)
+  int csize;                     // CTAs per cluster splitting the K range (1, 2, 4, 8)
 };
 
 // Per-row output bookkeeping staged in shared memory once per CTA (no dependent global loads in
@@ -92,13 +96,16 @@ __device__ __forceinline__ void shrink_store(const ShrinkParams& p, const RowSlo
 }
 
 template <int NT, int UNR>  // NT: n8 rank tiles per warp (n_ranks <= 8*NT); UNR: K steps in flight
-__global__ void __launch_bounds__(kShrinkWarps * 32, 1)
+__global__ void __launch_bounds__(kShrinkWarps * 32, 2)
     lora_shrink_kernel(const ShrinkParams p) {
+  namespace cg = cooperative_groups;
   constexpr int W2 = kShrinkWarps / 2;
-  __shared__ float red[W2][16][8 * NT + 1];
+  constexpr int LD = 8 * NT + 1;
+  __shared__ float red[W2][16][LD];
   __shared__ RowSlots rs;
 
-  const int tile = blockIdx.x, gi = blockIdx.y;
+  const int C = p.csize;
+  const int tile = blockIdx.x / C, rank = blockIdx.x % C, gi = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
   const int row_start = p.tiles[3 * tile + 0];
@@ -107,7 +114,7 @@ __global__ void __launch_bounds__(kShrinkWarps * 32, 1)
   const ShrinkGroup grp = p.groups[gi];
   const int n_out = 16 * grp.n_ranks;
   const bool has_adapter = adapter >= 0;
-  load_row_slots(p, rs, row_start, n_rows, has_adapter);
+  if (rank == 0) load_row_slots(p, rs, row_start, n_rows, has_adapter);
 
   float d[NT][4];
 #pragma unroll
@@ -116,6 +123,8 @@ __global__ void __launch_bounds__(kShrinkWarps * 32, 1)
   if (has_adapter) {
     const int klen = grp.k_hi - grp.k_lo;
     const int steps = (klen + 31) / 32;
+    const int st_lo = (int)((long long)steps * rank / C);
+    const int st_hi = (int)((long long)steps * (rank + 1) / C);
     const bool r0_ok = g < n_rows, r1_ok = (g + 8) < n_rows;
     const bf16* x0 = p.X + (size_t)(row_start + g) * p.ldx + grp.k_lo + 8 * c;
     const bf16* x1 = x0 + (size_t)8 * p.ldx;
@@ -123,13 +132,13 @@ __global__ void __launch_bounds__(kShrinkWarps * 32, 1)
                          (size_t)(grp.rank_off + g) * p.lda + grp.k_lo + 8 * c;
     const int nt_used = grp.n_ranks >> 3;
     const uint4 zero4 = make_uint4(0, 0, 0, 0);
-    for (int st0 = warp; st0 < steps; st0 += kShrinkWarps * UNR) {
+    for (int st0 = st_lo + warp; st0 < st_hi; st0 += kShrinkWarps * UNR) {
       uint4 xa[UNR], xb[UNR], av[UNR][NT];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         const int st = st0 + u * kShrinkWarps;
         const int koff = st * 32;
-        const bool k_ok = st < steps && (koff + 8 * c + 8) <= klen;  // K multiple of 8 (host)
+        const bool k_ok = st < st_hi && (koff + 8 * c + 8) <= klen;  // K multiple of 8 (host)
         xa[u] = (r0_ok && k_ok) ? ld_global_nc_v4(x0 + koff) : zero4;
         xb[u] = (r1_ok && k_ok) ? ld_global_nc_v4(x1 + koff) : zero4;
 #pragma unroll
@@ -149,7 +158,7 @@ __global__ void __launch_bounds__(kShrinkWarps * 32, 1)
     }
   }
 
-  // fixed-order two-level reduction of the 16 warp partials through shared memory
+  // fixed-order reduction: warps (two levels through smem), then CTAs of the cluster (DSMEM)
   if (warp >= W2) {
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
@@ -170,14 +179,35 @@ __global__ void __launch_bounds__(kShrinkWarps * 32, 1)
     }
   }
   __syncthreads();
-
+  // red[0] <- sum of the W2 partials (in order)
+  for (int e = threadIdx.x; e < n_out; e += blockDim.x) {
+    const int i = e / grp.n_ranks, j = e % grp.n_ranks;
+    float v = red[0][i][j];
+#pragma unroll
+    for (int w = 1; w < W2; ++w) v += red[w][i][j];
+    red[0][i][j] = v;
+  }
+  if (C > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // every CTA's red[0] complete and visible cluster-wide
+    if (rank == 0) {
+      const float sc = has_adapter ? p.scale[adapter] : 0.f;
+      for (int e = threadIdx.x; e < n_out; e += blockDim.x) {
+        const int i = e / grp.n_ranks, j = e % grp.n_ranks;
+        float v = red[0][i][j];
+        for (int r = 1; r < C; ++r) v += cl.map_shared_rank(&red[0][i][j], r)[0];
+        if (i < n_rows) shrink_store(p, rs, i, row_start + i, grp.rank_off + j, v * sc, has_adapter);
+      }
+    }
+    cl.sync();  // peers keep their shared memory alive until rank 0 has read it
+    return;
+  }
+  __syncthreads();
   const float sc = has_adapter ? p.scale[adapter] : 0.f;
   for (int e = threadIdx.x; e < n_out; e += blockDim.x) {
     const int i = e / grp.n_ranks, j = e % grp.n_ranks;
-    float v = 0.f;
-#pragma unroll
-    for (int w = 0; w < W2; ++w) v += red[w][i][j];
-    if (i < n_rows) shrink_store(p, rs, i, row_start + i, grp.rank_off + j, v * sc, has_adapter);
+    if (i < n_rows)
+      shrink_store(p, rs, i, row_start + i, grp.rank_off + j, red[0][i][j] * sc, has_adapter);
   }
 }
 

@@ -158,9 +158,9 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
 
 
 def reduce_tsplit(T: int, n_tiles: int, device: torch.device) -> int:
-    # one wave: the kernel keeps 4 CTAs/SM resident; keep >= 3 32-row chunks per split
+    # one wave: the kernel keeps 3 CTAs/SM resident; keep >= 3 32-row chunks per split
     chunks = math.ceil(T / 32)
-    want = (4 * num_sms(device)) // max(1, n_tiles)
+    want = (3 * num_sms(device)) // max(1, n_tiles)
     return max(1, min(want, chunks // 3, 128))
 
 
