@@ -54,7 +54,7 @@ int collm_device_info(int device, int* sm_major, int* sm_minor, int* num_sms);
  * seg_adapter[s] (-1 = base model only).  Replaces domain.Batch (domain.py:64-86), which may not
  * mix streams (domain.py:75-77).
  *
- * collm_plan_segments (HOST, pure CPU): per 128-row tile the distinct adapters in order of first
+ * collm_plan_segments (HOST, pure CPU): per 256-row slot tile the distinct adapters in order of first
  * appearance (tile_slot_ptr[n_tiles+1], slot_adapter[n_slots]) — the LoRA "slots" the GEMM folds
  * into its accumulator — and the shrink work list: maximal same-adapter runs cut into <=16-row
  * tiles (shrink_tiles[3*i] = row_start, n_rows, adapter; base-only runs included with adapter
@@ -73,9 +73,9 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
  * H[t, g.rank_off + j] = scale[a] * sum_{k in [g.k_lo, g.k_hi)} X[t,k] * A[a][g.rank_off + j, k]
  * for each shrink tile (rows of one adapter a; a = -1 -> no LoRA, zeros) and each rank group g
  * (groups: n_groups x 4 ints rank_off, n_ranks (multiple of 8, <= 64), k_lo, k_hi).  Outputs
- * (each optional): H32 fp32 [T, ldh]; H16 bf16 [T, ldh]; Hslots bf16 [n_slots*128, ldh] — the
- * GEMM's LoRA slot blocks, written completely: row t's value at row slot_of_row[t]*128 + t%128 and
- * zeros in the other slots of its 128-row tile (tile_slot_ptr).  One CTA per (tile, group) covers
+ * (each optional): H32 fp32 [T, ldh]; H16 bf16 [T, ldh]; Hslots bf16 [n_slots*256, ldh] — the
+ * GEMM's LoRA slot blocks, written completely: row t's value at row slot_of_row[t]*256 + t%256 and
+ * zeros in the other slots of its 256-row slot tile (tile_slot_ptr).  One CTA per (tile, group) covers
  * the whole K range; the reduction is in-CTA and fixed-order (deterministic, no workspace).
  * Replaces: the inference half of perf.true_infer_latency (perf.py:62-74). */
 int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
@@ -84,8 +84,8 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
                       const int32_t* slot_of_row, const int32_t* tile_slot_ptr, void* stream);
 
 /* ---- K2 / K3: base projection on tcgen05 with the LoRA expand fused into the accumulator ------
- * Y[M,N] = A[M,K] . B[N,K]^T + sum over the LoRA slots s of each 128-row tile of
- *          Hslots[s*128 : s*128+128, hcol(n) : hcol(n)+lora_rank] . LB[a(s)*lb_rows_per_adapter + n,
+ * Y[M,N] = A[M,K] . B[N,K]^T + sum over the LoRA slots s of each 256-row slot tile of
+ *          Hslots[s*256 + r%256 (r = the tile's rows), hcol(n) : hcol(n)+lora_rank] . LB[a(s)*lb_rows_per_adapter + n,
  *          0 : lora_rank]^T,
  * hcol(n) = sub_h_col[i] for the sub-projection i with sub_n_start[i] <= n < sub_n_start[i+1].
  * Pass tile_slot_ptr = NULL for a plain GEMM.  lora_rank a multiple of 16.  bn = 0 picks the

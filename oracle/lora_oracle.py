@@ -81,7 +81,7 @@ def expand_segments(seg_start, seg_adapter) -> np.ndarray:
     return out
 
 
-def tile_slots(row_adapter: np.ndarray, tile_m: int = 128):
+def tile_slots(row_adapter: np.ndarray, tile_m: int = 256):
     """Distinct adapters (>= 0) of each tile_m-row tile, in order of first appearance."""
     ptr, slots = [0], []
     for m0 in range(0, len(row_adapter), tile_m):
@@ -94,7 +94,7 @@ def tile_slots(row_adapter: np.ndarray, tile_m: int = 128):
     return np.array(ptr, np.int32), np.array(slots, np.int32)
 
 
-def slot_of_row(row_adapter, tile_slot_ptr, slot_adapter, tile_m: int = 128) -> np.ndarray:
+def slot_of_row(row_adapter, tile_slot_ptr, slot_adapter, tile_m: int = 256) -> np.ndarray:
     out = np.full(len(row_adapter), -1, np.int32)
     for t, a in enumerate(row_adapter.tolist()):
         if a < 0:

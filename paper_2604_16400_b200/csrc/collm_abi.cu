@@ -105,18 +105,29 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, ui
   return COLLM_OK;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& th,
                 const CUtensorMap& tlb, const GemmLoraParams& p, int grid, cudaStream_t stream) {
-  using L = GemmSmem<BN, STAGES>;
+  using L = GemmSmem<BN, STAGES, CG>;
   static bool configured = false;
   if (!configured) {
-    CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES>,
+    CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
     configured = true;
   }
-  gemm_lora_kernel<BN, STAGES><<<grid, 256, L::kTotal, stream>>>(ta, tb, th, tlb, p);
-  CUDA_TRY(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = L::kTotal;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_lora_kernel<BN, STAGES, CG>, ta, tb, th, tlb, p));
   return COLLM_OK;
 }
 
@@ -151,12 +162,12 @@ int collm_plan_segments(const int32_t* seg_start, const int32_t* seg_adapter, in
             seg_start[0], seg_start[n_seg]);
   for (int s = 0; s < n_seg; ++s)
     CHECK_ARG(seg_start[s + 1] > seg_start[s], "segment %d is empty or unsorted", s);
-  const int n_tiles = (n_rows + kGemmBM - 1) / kGemmBM;
+  const int n_tiles = (n_rows + kSlotTileM - 1) / kSlotTileM;
   int ns = 0;
   int seg = 0;
   for (int m = 0; m < n_tiles; ++m) {
     if (tile_slot_ptr) tile_slot_ptr[m] = ns;
-    const int r0 = m * kGemmBM, r1 = std::min(n_rows, r0 + kGemmBM);
+    const int r0 = m * kSlotTileM, r1 = std::min(n_rows, r0 + kSlotTileM);
     while (seg_start[seg + 1] <= r0) ++seg;
     const int first = ns;
     for (int s = seg; s < n_seg && seg_start[s] < r1; ++s) {
@@ -321,37 +332,50 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
       if (sub_n_start[i] % t) return false;
     return true;
   };
-  const int nm = (M + kGemmBM - 1) / kGemmBM;
-  CHECK_ARG(nm <= kMaxMTiles, "M=%d exceeds %d rows", M, kMaxMTiles * kGemmBM);
-  // Schedule choice by a cost model in units of one 128x256 k-block (calibrated on B200:
-  // a 128x128 k-block costs ~0.7 of that — smem-bandwidth bound — a stream-K fix-up ~35, an
-  // exposed epilogue ~4): data-parallel 256-wide, data-parallel 128-wide, or hybrid stream-K.
-  int sched = 0;
+  // Tile / schedule choice by a cost model calibrated on B200 (tools/gemm_bench.py, µs): time of
+  // one 64-deep k-block of a unit tile — 1-CTA 128x256: 0.48, 1-CTA 128x128: 0.34, CTA-pair
+  // 256x256: 0.43, CTA-pair 256x128: 0.34 — times the k-blocks on the critical path;
+  // data-parallel: waves x k-blocks; hybrid stream-K: (full waves - 1) data-parallel + the rest
+  // split evenly, plus a fix-up of ~12 + 8 x (parts per split tile) µs.
+  struct Cand { int cg, bn, sched; double cost; };
+  auto env_int = [](const char* k, int d) { const char* e = getenv(k); return e ? atoi(e) : d; };
+  const int force_cg = env_int("COLLM_GEMM_CG", 0), force_bn = env_int("COLLM_GEMM_BN", bn);
   const char* sched_env = getenv("COLLM_GEMM_SCHED");
-  if (bn == 0) {
-    const bool ok256 = aligned_to(256) && N > 128, ok128 = aligned_to(128);
-    if (!ok256 && !ok128)
-      return fail(COLLM_EINVAL, "sub-projection boundaries are not multiples of 128");
-    const double nk = (K + kGemmBK - 1) / kGemmBK;
-    const long long t256 = (long long)nm * ((N + 255) / 256);
-    const long long t128 = (long long)nm * ((N + 127) / 128);
-    const double dp256 = ok256 ? ((t256 + sms - 1) / sms) * nk + 4 : 1e30;
-    const double dp128 = ok128 ? ((t128 + sms - 1) / sms) * nk * 0.7 + 4 : 1e30;
-    const double sk256 = ok256 ? (double)t256 * nk / sms + 35 : 1e30;
-    if (sk256 < dp256 && sk256 < dp128) {
-      bn = 256;
-      sched = 1;
-    } else {
-      bn = dp256 <= dp128 ? 256 : 128;
+  const int force_sched = !sched_env ? -1 : strcmp(sched_env, "dp") == 0 ? 0
+                          : strcmp(sched_env, "hybrid") == 0 ? 1 : strcmp(sched_env, "sknofix") == 0 ? 2 : -1;
+  Cand best{0, 0, 0, 1e30};
+  const double nk = (K + kGemmBK - 1) / kGemmBK;
+  for (int cg : {2, 1}) {
+    if (force_cg && cg != force_cg) continue;
+    const long long units = sms / cg;
+    const long long nmu = (M + kGemmBM * cg - 1) / (kGemmBM * cg);
+    for (int b : {256, 128}) {
+      if (force_bn && b != force_bn) continue;
+      if (!aligned_to(b) || (b == 256 && N <= 128 && !force_bn)) continue;
+      const double kb = cg == 2 ? (b == 256 ? 0.43 : 0.34) : (b == 256 ? 0.48 : 0.34);
+      const long long tiles = nmu * ((N + b - 1) / b);
+      for (int sc : {0, 1}) {
+        if (force_sched >= 0 && (force_sched == 2 ? 1 : force_sched) != sc) continue;
+        double cost;
+        if (sc == 0) {
+          cost = (double)((tiles + units - 1) / units) * nk * kb;
+        } else {
+          const long long waves = tiles / units;
+          const long long dp_waves = waves >= 1 ? waves - 1 : 0;
+          const long long sk_tiles = tiles - dp_waves * units;
+          const double parts = std::min(3.0, std::max(1.0, (double)units / sk_tiles));
+          cost = dp_waves * nk * kb + (double)sk_tiles * nk * kb / units + 12.0 + 8.0 * parts;
+        }
+        if (cost < best.cost) best = {cg, b, sc, cost};
+      }
     }
-  } else {
-    sched = 1;
   }
-  if (sched_env) {
-    if (strcmp(sched_env, "dp") == 0) sched = 0;
-    if (strcmp(sched_env, "hybrid") == 0) sched = 1;
-    if (strcmp(sched_env, "sknofix") == 0) sched = 2;  // debug only: wrong results
-  }
+  if (best.cg == 0) return fail(COLLM_EINVAL, "no GEMM tile fits (sub-projection boundaries must be x128)");
+  const int cg = best.cg;
+  bn = best.bn;
+  const int sched = force_sched == 2 ? 2 : best.sched;
+  const int nm = (M + kGemmBM * cg - 1) / (kGemmBM * cg);
+  CHECK_ARG(nm <= kMaxMTiles, "M=%d exceeds %d rows", M, kMaxMTiles * kGemmBM);
   CHECK_ARG(bn == 128 || bn == 256, "bn must be 0, 128 or 256");
   CHECK_ARG(aligned_to(bn), "sub-projection boundaries are not multiples of bn=%d", bn);
 
@@ -371,7 +395,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   CUtensorMap ta, tb, th, tlb;
   int rc = make_tmap(&ta, A, K, M, lda, kGemmBK, kGemmBM);
   if (rc) return rc;
-  rc = make_tmap(&tb, B, K, N, ldb, kGemmBK, bn);
+  rc = make_tmap(&tb, B, K, N, ldb, kGemmBK, bn / cg);
   if (rc) return rc;
   if (lora) {
     CHECK_ARG(Hslots && LB && slot_adapter, "LoRA GEMM needs Hslots, LB and slot_adapter");
@@ -401,15 +425,16 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
     CHECK_ARG(lora_rank <= ld_lb, "lora_rank %d exceeds LB width %d", lora_rank, ld_lb);
     rc = make_tmap(&th, Hslots, ldh, h_rows, ldh, lrc, kGemmBM);
     if (rc) return rc;
-    rc = make_tmap(&tlb, LB, ld_lb, lb_rows, ld_lb, lrc, bn);
+    rc = make_tmap(&tlb, LB, ld_lb, lb_rows, ld_lb, lrc, bn / cg);
     if (rc) return rc;
   } else {
     th = ta;
     tlb = tb;
   }
-  // stream-K grid: one CTA per SM, never more CTAs than k-stages (every range non-empty)
+  // persistent grid: one CTA (pair) per SM (pair), never more units than k-stages (every
+  // stream-K range non-empty)
   const long long min_work = (long long)nm * p.num_n_tiles * ((K + kGemmBK - 1) / kGemmBK);
-  const int grid = (int)std::min<long long>(sms, min_work);
+  const int grid = cg * (int)std::min<long long>(sms / cg, min_work);
   p.sched = sched;
   const size_t need = collm_gemm_workspace_bytes(bn);
   CHECK_ARG(workspace && ws_bytes >= need, "gemm workspace too small: %zu < %zu", ws_bytes, need);
@@ -424,8 +449,12 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   }
   p.partials = (float*)((char*)workspace + kCounterBytes);
   cudaStream_t st = (cudaStream_t)stream;
-  if (bn == 256) return launch_gemm<256, 4>(ta, tb, th, tlb, p, grid, st);
-  return launch_gemm<128, 6>(ta, tb, th, tlb, p, grid, st);
+  if (cg == 2) {
+    if (bn == 256) return launch_gemm<256, 6, 2>(ta, tb, th, tlb, p, grid, st);
+    return launch_gemm<128, 8, 2>(ta, tb, th, tlb, p, grid, st);
+  }
+  if (bn == 256) return launch_gemm<256, 4, 1>(ta, tb, th, tlb, p, grid, st);
+  return launch_gemm<128, 6, 1>(ta, tb, th, tlb, p, grid, st);
 }
 
 // ------------------------------------------------------------------------------------ K5

@@ -12,7 +12,15 @@
 // Replaces the reference's latency stand-ins `perf.true_infer_latency` / `true_train_latency`
 // (/root/reference/pkg/src/coserve/perf.py:62-89) with the real projection arithmetic.
 //
-// Roles (256 threads, 1 CTA/SM, persistent):
+// CG = 1: one CTA per 128-row tile (tcgen05.mma.cta_group::1, 128 x BN per CTA).
+// CG = 2: a thread-block cluster of 2 CTAs per 256-row tile (tcgen05.mma.cta_group::2 issued by
+//         the leader, M = 256 across the pair): each CTA loads its own 128 rows of A and HALF of
+//         the BN rows of B, so the per-SM shared-memory operand traffic per MMA drops from
+//         (128 + BN) x 16 to (128 + BN/2) x 16 elements; both CTAs' TMA loads complete on the
+//         leader's mbarriers, the leader's commits multicast to both CTAs, both epilogues arrive
+//         on the leader's TMEM-empty barrier.
+//
+// Roles (256 threads per CTA, 1 CTA/SM, persistent):
 //   warp 0 lane 0 : TMA producer (ring of STAGES smem stages, full/empty mbarriers)
 //   warp 1 lane 0 : tcgen05.mma issuer into a double-buffered TMEM accumulator (2 x BN columns)
 //   warp 2        : TMEM allocator
@@ -54,7 +62,7 @@ struct GemmLoraParams {
   int n_sub;                     // sub-projections along N (fused q|k|v, gate|up); >= 1
   int sub_n_start[kMaxSub + 1];  // N boundaries of the sub-projections (multiples of BN)
   int sub_h_col[kMaxSub];        // first H column used by each sub-projection
-  int num_m_tiles, num_n_tiles;
+  int num_m_tiles, num_n_tiles;  // in units of (128 * CG) rows x BN columns
   int sched;  // 0 = data-parallel (round-robin tiles), 1 = hybrid data-parallel + stream-K,
               // 2 = debug: stream-K split without fix-up (timing experiments only)
   // ---- stream-K
@@ -69,10 +77,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG>
 struct GemmSmem {
-  static constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;  // 16 KB
-  static constexpr uint32_t kBBytes = BN * kGemmBK * 2;
+  static constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;  // 16 KB: this CTA's 128 rows
+  static constexpr uint32_t kBRows = BN / CG;                  // this CTA's share of the N tile
+  static constexpr uint32_t kBBytes = kBRows * kGemmBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
   static constexpr uint32_t kPrefixOffset = kBarOffset + 256;
@@ -174,13 +183,14 @@ struct StreamK {
   }
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG>
 __global__ void __launch_bounds__(256, 1)
     gemm_lora_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmLB,
                      const GemmLoraParams p) {
-  using L = GemmSmem<BN, STAGES>;
+  using L = GemmSmem<BN, STAGES, CG>;
   constexpr uint32_t BM = kGemmBM, BK = kGemmBK;
+  constexpr uint32_t UNIT_M = BM * CG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -196,15 +206,22 @@ __global__ void __launch_bounds__(256, 1)
   const int lane = threadIdx.x & 31;
   const bool has_lora = p.tile_slot_ptr != nullptr;
   const int nk = (p.K + BK - 1) / BK;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
 
-  // per-m-tile stage counts -> prefix (every role needs it for the schedule)
+  // LoRA stages of a (128*CG)-row unit: the slot list of the 256-row slot tile containing it
+  auto lora_stages = [&](int m) {
+    if (!has_lora) return 0;
+    const int st = (m * (int)UNIT_M) / kSlotTileM;
+    return (p.tile_slot_ptr[st + 1] - p.tile_slot_ptr[st]) * p.lora_chunks;
+  };
+
+  // per-unit stage counts -> prefix (every role needs it for the schedule)
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int m = 0; m < p.num_m_tiles; ++m) {
       s_prefix[m] = acc;
-      const int nl =
-          has_lora ? (p.tile_slot_ptr[m + 1] - p.tile_slot_ptr[m]) * p.lora_chunks : 0;
-      acc += nl + nk;
+      acc += lora_stages(m) + nk;
     }
     s_prefix[p.num_m_tiles] = acc;
     tma_prefetch_desc(&tmA);
@@ -219,61 +236,83 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], 4 * CG);
     }
     mbar_init(fixbar, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<L::kTmemCols>(tmem_slot);
+  if (warp == 2) tmem_alloc<L::kTmemCols, CG>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   StreamK sk;
-  sk.init(s_prefix, p.num_m_tiles, p.num_n_tiles, gridDim.x, p.sched);
-  const int cta = blockIdx.x;
-  auto lora_stages = [&](int m) {
-    return has_lora ? (p.tile_slot_ptr[m + 1] - p.tile_slot_ptr[m]) * p.lora_chunks : 0;
-  };
+  sk.init(s_prefix, p.num_m_tiles, p.num_n_tiles, gridDim.x / CG, p.sched);
+  const int unit = blockIdx.x / CG;  // CTA pair (or CTA) index in the schedule
 
   if (warp == 0 && lane == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs of a pair) =====================
     int stage = 0;
     uint32_t phase = 0;
-    sk.for_each(cta, [&](const Segment& sg) {
-      const int m0 = sg.m_blk * BM, n0 = sg.n_blk * BN;
+    const uint32_t rc = p.lora_rc;
+    sk.for_each(unit, [&](const Segment& sg) {
+      const int m0 = sg.m_blk * UNIT_M + rank * BM;  // this CTA's rows
+      const int n0 = sg.n_blk * BN;
+      const int nb0 = n0 + rank * (int)L::kBRows;   // this CTA's share of the N tile
       const int n_lora = lora_stages(sg.m_blk);
+      const int st_tile = m0 / kSlotTileM;
+      const int hrow0 = m0 % kSlotTileM;
       const int hcol = has_lora ? p.sub_h_col[sub_of_n0(p, n0)] : 0;
-      const uint32_t rc = p.lora_rc;
       for (int i = sg.k0; i < sg.k1; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * L::kStageBytes;
+        uint32_t bytes;
+        if (i < n_lora) bytes = (BM + L::kBRows) * rc * 2;
+        else bytes = L::kStageBytes;
+        if (leader) mbar_arrive_expect_tx(&full[stage], bytes * CG);
         if (i < n_lora) {
-          const int s = p.tile_slot_ptr[sg.m_blk] + i / p.lora_chunks;
+          const int s = p.tile_slot_ptr[st_tile] + i / p.lora_chunks;
           const int c = i % p.lora_chunks;
-          const int lb_row = p.slot_adapter[s] * p.lb_rows_per_adapter + n0;
-          mbar_arrive_expect_tx(&full[stage], (BM + BN) * rc * 2);
-          tma_load_2d(sa, &tmH, &full[stage], hcol + c * rc, s * BM);
-          tma_load_2d(sa + L::kABytes, &tmLB, &full[stage], c * rc, lb_row);
+          const int lb_row = p.slot_adapter[s] * p.lb_rows_per_adapter + nb0;
+          if constexpr (CG == 2) {
+            const uint32_t fb = mapa_shared(&full[stage], 0);
+            tma_load_2d_pair(sa, &tmH, fb, hcol + c * rc, s * kSlotTileM + hrow0);
+            tma_load_2d_pair(sa + L::kABytes, &tmLB, fb, c * rc, lb_row);
+          } else {
+            tma_load_2d(sa, &tmH, &full[stage], hcol + c * rc, s * kSlotTileM + hrow0);
+            tma_load_2d(sa + L::kABytes, &tmLB, &full[stage], c * rc, lb_row);
+          }
         } else {
           const int kb = i - n_lora;
-          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-          tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
-          tma_load_2d(sa + L::kABytes, &tmB, &full[stage], kb * BK, n0);
+          if constexpr (CG == 2) {
+            const uint32_t fb = mapa_shared(&full[stage], 0);
+            tma_load_2d_pair(sa, &tmA, fb, kb * BK, m0);
+            tma_load_2d_pair(sa + L::kABytes, &tmB, fb, kb * BK, nb0);
+          } else {
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
+            tma_load_2d(sa + L::kABytes, &tmB, &full[stage], kb * BK, nb0);
+          }
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     });
-  } else if (warp == 1 && lane == 0) {
-    // ===================== tcgen05.mma issuer =====================
-    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ===================== tcgen05.mma issuer (the pair's leader) =====================
+    constexpr uint32_t idesc = umma_idesc_bf16(UNIT_M, BN);
     int stage = 0;
     uint32_t phase = 0;
     uint32_t acc = 0, acc_phase = 0;
     const uint32_t smem_base = smem_u32(smem);
     const uint32_t lrow = p.lora_rc * 2, lsteps = p.lora_rc / 16;
-    sk.for_each(cta, [&](const Segment& sg) {
+    auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
+      if constexpr (CG == 2) umma_bf16_pair(d, a, b, idesc, accumulate);
+      else umma_bf16(d, a, b, idesc, accumulate);
+    };
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (CG == 2) umma_commit_pair(bar); else umma_commit(bar);
+    };
+    sk.for_each(unit, [&](const Segment& sg) {
       const int n_lora = lora_stages(sg.m_blk);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -285,48 +324,54 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t sa = smem_base + stage * L::kStageBytes;
         if (i < n_lora) {
           for (uint32_t k = 0; k < lsteps; ++k) {
-            umma_bf16(d_tmem, umma_desc_kmajor(sa + k * 32, lrow),
-                      umma_desc_kmajor(sa + L::kABytes + k * 32, lrow), idesc, accumulate);
+            mma(d_tmem, umma_desc_kmajor(sa + k * 32, lrow),
+                umma_desc_kmajor(sa + L::kABytes + k * 32, lrow), accumulate);
             accumulate = 1;
           }
         } else {
 #pragma unroll
           for (uint32_t k = 0; k < BK / 16; ++k) {
-            umma_bf16(d_tmem, umma_desc_kmajor(sa + k * 32, 128),
-                      umma_desc_kmajor(sa + L::kABytes + k * 32, 128), idesc, accumulate);
+            mma(d_tmem, umma_desc_kmajor(sa + k * 32, 128),
+                umma_desc_kmajor(sa + L::kABytes + k * 32, 128), accumulate);
             accumulate = 1;
           }
         }
-        umma_commit(&empty[stage]);
+        commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      umma_commit(&tfull[acc]);
+      commit(&tfull[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     });
   } else if (warp >= 4) {
-    // ===================== epilogue =====================
+    // ===================== epilogue (both CTAs: each its own 128 rows) =====================
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew+32)
     const int tid = threadIdx.x - 128;
     uint32_t acc = 0, acc_phase = 0, fix_phase = 0;
     int seg_i = 0;
+    const int cta = blockIdx.x;
     unsigned long long* dbg = p.dbg ? p.dbg + (size_t)cta * 16 : nullptr;
     if (dbg && tid == 0) dbg[0] = gtimer();
-    sk.for_each(cta, [&](const Segment& sg_in) {
+    sk.for_each(unit, [&](const Segment& sg_in) {
       Segment sg = sg_in;
       if (p.sched == 2) sg.mode = 0;  // debug: stream-K split without the fix-up (timing only)
       const int lrow_i = ew * 32 + lane;
-      const int row = sg.m_blk * BM + lrow_i;
+      const int row = sg.m_blk * UNIT_M + rank * BM + lrow_i;
       const int n0 = sg.n_blk * BN;
       if (dbg && tid == 0 && seg_i < 3) dbg[1 + 4 * seg_i] = gtimer() | ((unsigned long long)sg.mode << 60);
       if (sg.mode == 2) {  // wait for the earlier parts of this tile (produced first by their CTAs)
         if (tid == 0) {
-          for (int c = sg.c_first; c < cta; ++c) {
+          for (int c = sg.c_first; c < unit; ++c) {
             if (sk.bound(c) == sk.bound(c + 1)) continue;  // empty range: no part
-            const int32_t* f = p.flags + c;
+            const int32_t* f = p.flags + c * CG + rank;
             uint32_t v;
+            const unsigned long long t0 = clock64();
             do {
               asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+              if (clock64() - t0 > COLLM_MBAR_TIMEOUT_CYCLES) {
+                printf("collm: stream-K flag timeout (block %d)\n", blockIdx.x);
+                __trap();
+              }
             } while (v == 0);
           }
         }
@@ -335,12 +380,12 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (dbg && tid == 0 && seg_i < 3) dbg[2 + 4 * seg_i] = gtimer();
-      // Finishing segment = this CTA's last: the MMAs are done with the pipeline smem, so the
+      // Finishing segment = this pair's last: the MMAs are done with the pipeline smem, so the
       // first earlier part is pulled in with one bulk copy (the rest stream from L2).
       int smem_part = -1;
       if (sg.mode == 2) {
-        for (int pc = sg.c_first; pc < cta; ++pc)
-          if (sk.bound(pc) != sk.bound(pc + 1)) { smem_part = pc; break; }
+        for (int pc = sg.c_first; pc < unit; ++pc)
+          if (sk.bound(pc) != sk.bound(pc + 1)) { smem_part = pc * CG + (int)rank; break; }
         if (smem_part >= 0) {
           if (tid == 0) {
             mbar_arrive_expect_tx(fixbar, BM * BN * 4);
@@ -380,10 +425,11 @@ __global__ void __launch_bounds__(256, 1)
               r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
             }
           }
-          for (int pc = sg.c_first; pc < cta; ++pc) {
-            if (pc == smem_part || sk.bound(pc) == sk.bound(pc + 1)) continue;
+          for (int pc = sg.c_first; pc < unit; ++pc) {
+            const int pcta = pc * CG + (int)rank;
+            if (pcta == smem_part || sk.bound(pc) == sk.bound(pc + 1)) continue;
             const float4* src =
-                reinterpret_cast<const float4*>(p.partials + (size_t)pc * (BM * BN)) + tid +
+                reinterpret_cast<const float4*>(p.partials + (size_t)pcta * (BM * BN)) + tid +
                 chunk * 8 * 128;
             float4 v8[8];
 #pragma unroll
@@ -414,7 +460,10 @@ __global__ void __launch_bounds__(256, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+        else mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
       if (sg.mode == 1) {  // publish the partial
@@ -426,7 +475,7 @@ __global__ void __launch_bounds__(256, 1)
       } else if (sg.mode == 2) {  // consumed: reset the producers' flags for the next launch
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (tid == 0)
-          for (int c = sg.c_first; c < cta; ++c) p.flags[c] = 0;
+          for (int c = sg.c_first; c < unit; ++c) p.flags[c * CG + rank] = 0;
       }
       if (dbg && tid == 0 && seg_i < 3) dbg[3 + 4 * seg_i] = gtimer();
       ++seg_i;
@@ -435,10 +484,10 @@ __global__ void __launch_bounds__(256, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<L::kTmemCols>(tmem_base);
+    tmem_dealloc<L::kTmemCols, CG>(tmem_base);
   }
 }
 

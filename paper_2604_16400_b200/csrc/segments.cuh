@@ -7,7 +7,7 @@
 // which cannot mix streams — the unified layer mixes adapters by design.
 //
 //   row_adapter[t] = seg_adapter[s] for seg_start[s] <= t < seg_start[s+1]
-//   slot_of_row[t] = index (into slot_adapter) of row t's adapter within its 128-row tile, or -1
+//   slot_of_row[t] = index (into slot_adapter) of row t's adapter within its 256-row slot tile, or -1
 #pragma once
 #include "common.cuh"
 
@@ -32,7 +32,7 @@ __global__ void expand_segments_kernel(const int32_t* __restrict__ seg_start,
   if (slot_of_row) {
     int slot = -1;
     if (a >= 0) {
-      const int m = t >> 7;
+      const int m = t / kSlotTileM;
       for (int s = tile_slot_ptr[m]; s < tile_slot_ptr[m + 1]; ++s)
         if (slot_adapter[s] == a) { slot = s; break; }
     }

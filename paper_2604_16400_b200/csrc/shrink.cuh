@@ -52,9 +52,9 @@ struct ShrinkParams {
   float* H32;
   bf16* H16;
   int ldh;
-  bf16* Hslots;  // [n_slots*128, ldh] — row (slot*128 + t%128)
+  bf16* Hslots;  // [n_slots*256, ldh] — row (slot*256 + t%256)
   const int32_t* slot_of_row;
-  const int32_t* tile_slot_ptr;  // slot range of each 128-row tile (for the zero fill)
+  const int32_t* tile_slot_ptr;  // slot range of each 256-row slot tile (for the zero fill)
   int csize;                     // CTAs per cluster splitting the K range (1, 2, 4, 8)
 };
 
@@ -70,7 +70,7 @@ __device__ __forceinline__ void load_row_slots(const ShrinkParams& p, RowSlots& 
     const int i = threadIdx.x;
     int mine = -1, beg = 0, end = 0;
     if (i < n_rows && p.Hslots) {
-      const int t = row_start + i, m = t >> 7;
+      const int t = row_start + i, m = t / kSlotTileM;
       mine = has_adapter ? p.slot_of_row[t] : -1;
       beg = p.tile_slot_ptr[m];
       end = p.tile_slot_ptr[m + 1];
@@ -91,7 +91,7 @@ __device__ __forceinline__ void shrink_store(const ShrinkParams& p, const RowSlo
   if (p.Hslots) {
     const bf16 zero = __float2bfloat16_rn(0.f);
     for (int s = rs.beg[i]; s < rs.end[i]; ++s)
-      p.Hslots[((size_t)s * 128 + (t & 127)) * p.ldh + col] = (s == rs.mine[i]) ? vb : zero;
+      p.Hslots[((size_t)s * kSlotTileM + (t % kSlotTileM)) * p.ldh + col] = (s == rs.mine[i]) ? vb : zero;
   }
 }
 

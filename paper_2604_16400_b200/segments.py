@@ -22,7 +22,7 @@ import torch
 from . import _lib
 from .domain import ConfigurationError, InferenceItem, MixedBatch, RowRole, TrainItem
 
-TILE_M = 128
+TILE_M = 256  # LoRA slot-plan granularity (kSlotTileM in csrc/common.cuh)
 SHRINK_TILE = 16
 
 

@@ -28,10 +28,21 @@ def lib():
     return _lib.load()
 
 
+GEMM_VARIANTS = [("1", "dp"), ("1", "hybrid"), ("2", "dp"), ("2", "hybrid")]
+
+
+@pytest.fixture(params=GEMM_VARIANTS, ids=lambda v: f"cg{v[0]}-{v[1]}")
+def gemm_variant(request, monkeypatch):
+    """Force each kernel variant (CTA or CTA-pair tiles, data-parallel or stream-K)."""
+    monkeypatch.setenv("COLLM_GEMM_CG", request.param[0])
+    monkeypatch.setenv("COLLM_GEMM_SCHED", request.param[1])
+    return request.param
+
+
 @pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (200, 384, 320, 0), (77, 136, 200, 128),
                                       (1024, 4096, 4096, 0), (512, 1024, 12288, 128),
                                       (300, 688, 256, 128)])
-def test_gemm_plain(M, N, K, bn):
+def test_gemm_plain(M, N, K, bn, gemm_variant):
     from paper_2604_16400_b200 import ops
     g = torch.Generator().manual_seed(M * 7 + N)
     A = _bf(M, K, gen=g)
@@ -44,11 +55,12 @@ def test_gemm_plain(M, N, K, bn):
 
 @pytest.mark.parametrize("r_pad,n_sub,bn", [(16, 1, 256), (16, 3, 128), (32, 1, 128), (64, 2, 256),
                                             (48, 1, 128)])
-def test_gemm_lora_slots(r_pad, n_sub, bn):
+def test_gemm_lora_slots(r_pad, n_sub, bn, gemm_variant):
     """Forward-style LoRA K-extension: multiple slots per tile, per-sub H column offsets."""
     from paper_2604_16400_b200 import ops
     g = torch.Generator().manual_seed(r_pad * 31 + n_sub)
-    M, K = 300, 256
+    M, K = 600, 256
+    TM = 256  # slot-plan granularity
     n_each = 256 if bn == 256 else 128
     N = n_each * n_sub
     n_ad = 5
@@ -56,11 +68,12 @@ def test_gemm_lora_slots(r_pad, n_sub, bn):
     A = _bf(M, K, gen=g)
     W = _bf(N, K, scale=0.05, gen=g)
     # tile slots: tile0 adapters [0, 3], tile1 [3, 1, 4], tile2 [2]
-    row_ad = torch.tensor([0] * 100 + [3] * 60 + [1] * 50 + [4] * 46 + [2] * 44, dtype=torch.int32)
+    row_ad = torch.tensor([0] * 100 + [3] * 60 + [1] * 50 + [4] * 46 + [2] * 44 + [1] * 200 +
+                          [0] * 30 + [4] * 70, dtype=torch.int32)
     tiles_adapters = []
-    for m in range(math.ceil(M / 128)):
+    for m in range(math.ceil(M / TM)):
         seen = []
-        for a in row_ad[m * 128:(m + 1) * 128].tolist():
+        for a in row_ad[m * TM:(m + 1) * TM].tolist():
             if a not in seen:
                 seen.append(a)
         tiles_adapters.append(seen)
@@ -70,11 +83,11 @@ def test_gemm_lora_slots(r_pad, n_sub, bn):
         slots += s
         tsp.append(len(slots))
     H = torch.randn(M, R, generator=g).to(torch.bfloat16)
-    Hslots = torch.zeros(len(slots) * 128, R, dtype=torch.bfloat16)
+    Hslots = torch.zeros(len(slots) * TM, R, dtype=torch.bfloat16)
     for t in range(M):
-        m = t // 128
+        m = t // TM
         s = tsp[m] + tiles_adapters[m].index(int(row_ad[t]))
-        Hslots[s * 128 + t % 128] = H[t]
+        Hslots[s * TM + t % TM] = H[t]
     LB = (torch.randn(n_ad, N, r_pad, generator=g) * 0.1).to(torch.bfloat16)
     Y = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     sub_n = [i * n_each for i in range(n_sub + 1)]

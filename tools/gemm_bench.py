@@ -1,4 +1,5 @@
-"""Time the collm GEMM alone on Llama-7B projection shapes (CUDA events, L2-sized inputs)."""
+"""Time the collm GEMM alone on Llama-7B projection shapes (CUDA events) for several forced
+kernel variants.  VARIANTS="cg:bn:sched,..." (default: auto + all pure variants)."""
 import os
 import sys
 
@@ -10,28 +11,41 @@ from paper_2604_16400_b200 import ops  # noqa: E402
 SHAPES = [("qkv", 1024, 12288, 4096), ("o", 1024, 4096, 4096), ("gate_up", 1024, 22016, 4096),
           ("down", 1024, 4096, 11008), ("dX_qkv", 512, 4096, 12288), ("dX_o", 512, 4096, 4096),
           ("dX_gu", 512, 4096, 22016), ("dX_down", 512, 11008, 4096)]
+DEFAULT = "auto,1:256:dp,1:128:dp,1:256:hybrid,2:256:dp,2:128:dp,2:256:hybrid,2:128:hybrid"
+
+
+def set_variant(v):
+    for k in ("COLLM_GEMM_CG", "COLLM_GEMM_BN", "COLLM_GEMM_SCHED"):
+        os.environ.pop(k, None)
+    if v != "auto":
+        cg, bn, sc = v.split(":")
+        os.environ.update(COLLM_GEMM_CG=cg, COLLM_GEMM_BN=bn, COLLM_GEMM_SCHED=sc)
 
 
 def main():
-    bns = [int(b) for b in os.environ.get("BNS", "0").split(",")]
+    variants = os.environ.get("VARIANTS", DEFAULT).split(",")
+    res = {}
     for name, M, N, K in SHAPES:
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         Ws = [torch.randn(N, K, device="cuda").to(torch.bfloat16) for _ in range(3)]
         Y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        for bn in bns:
+        for v in variants:
+            set_variant(v)
             for i in range(3):
-                ops.gemm_lora(A, Ws[i % 3], Y, bn=bn)
+                ops.gemm_lora(A, Ws[i % 3], Y)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             reps = 30
             e0.record()
             for i in range(reps):
-                ops.gemm_lora(A, Ws[i % 3], Y, bn=bn)
+                ops.gemm_lora(A, Ws[i % 3], Y)
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / reps * 1e3
-            tf = 2 * M * N * K / (us * 1e-6) / 1e12
-            print(f"{os.environ.get('COLLM_GEMM_SCHED','hybrid'):6s} bn={bn:3d} {name:8s} M={M:5d} N={N:6d} K={K:6d} {us:8.1f} us {tf:7.1f} TFLOP/s")
+            res[(name, v)] = (us, 2 * M * N * K / (us * 1e-6) / 1e12)
+    print(f"{'shape':8s} " + " ".join(f"{v:>14s}" for v in variants))
+    for name, *_ in SHAPES:
+        print(f"{name:8s} " + " ".join(f"{res[(name, v)][0]:7.1f}/{res[(name, v)][1]:5.0f}" for v in variants))
 
 
 if __name__ == "__main__":
