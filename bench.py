@@ -48,6 +48,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph (debug)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="run the LoRA kernels on the GEMM stream (no side-stream overlap)")
     return ap.parse_args(argv)
 
 
@@ -253,6 +255,7 @@ def run_ours(args, cfg, workload):
     st_dev = torch.cuda.current_stream()
 
     stack = ReplicaStack(cfg, dev, seed=args.seed)
+    stack.overlap = not args.no_overlap
     train, items = cfg.batch(args.seed)
     plan = stack.plan(train, items)
     stack.allocate(plan)
@@ -333,7 +336,9 @@ def run_ours(args, cfg, workload):
         "data": "synthetic (random-init weights of the named shape; seeded synthetic rows)",
         "config": dict(workload, sync=("none (1 replica): fused AdamW" if fused_opt else
                                        "NCCL allreduce(avg) of LoRA grads each step + AdamW "
-                                       "apply")),
+                                       "apply"),
+                       streams=("GEMMs + LoRA kernels overlapped on two streams" if stack.overlap
+                                else "single stream")),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
     }

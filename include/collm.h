@@ -106,6 +106,11 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
                     const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
                     void* stream);
 
+/* Select the GEMM pipeline depth: lean != 0 -> ~128 KB shared memory per CTA so one CTA of the
+ * LoRA kernels can run on the same SM concurrently (graph branch / second stream); 0 -> deepest
+ * pipeline (default).  Process-wide setting. */
+int collm_set_gemm_lean(int lean);
+
 /* ---- K5: LoRA weight-gradient reductions with fused AdamW ------------------------------------
  * One group = one reduction C[p,q] = sum_t U[t, u_off+p] * V[t, v_off+q] (p < P, q < Q <= 64;
  * P, Q multiples of 8) and the tensors it updates.  Element (p,q) lives at fp32 index

@@ -294,6 +294,8 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
 }
 
 // ------------------------------------------------------------------------------------ K2/K3
+static bool g_gemm_lean = false;
+
 // debug-only: device pointer of the last GEMM's timeline (COLLM_GEMM_DEBUG set)
 unsigned long long* collm_debug_timeline = nullptr;
 int collm_gemm_debug_copy(void* host_dst, size_t bytes) {
@@ -342,7 +344,8 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   const int force_cg = env_int("COLLM_GEMM_CG", 0), force_bn = env_int("COLLM_GEMM_BN", bn);
   const char* sched_env = getenv("COLLM_GEMM_SCHED");
   const int force_sched = !sched_env ? -1 : strcmp(sched_env, "dp") == 0 ? 0
-                          : strcmp(sched_env, "hybrid") == 0 ? 1 : strcmp(sched_env, "sknofix") == 0 ? 2 : -1;
+                          : strcmp(sched_env, "hybrid") == 0 ? 1 : strcmp(sched_env, "sknofix") == 0 ? 2
+                          : strcmp(sched_env, "noload") == 0 ? 3 : -1;
   Cand best{0, 0, 0, 1e30};
   const double nk = (K + kGemmBK - 1) / kGemmBK;
   for (int cg : {2, 1}) {
@@ -355,7 +358,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
       const double kb = cg == 2 ? (b == 256 ? 0.43 : 0.34) : (b == 256 ? 0.48 : 0.34);
       const long long tiles = nmu * ((N + b - 1) / b);
       for (int sc : {0, 1}) {
-        if (force_sched >= 0 && (force_sched == 2 ? 1 : force_sched) != sc) continue;
+        if (force_sched >= 0 && (force_sched == 2 ? 1 : force_sched == 3 ? 0 : force_sched) != sc) continue;
         double cost;
         if (sc == 0) {
           cost = (double)((tiles + units - 1) / units) * nk * kb;
@@ -373,7 +376,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   if (best.cg == 0) return fail(COLLM_EINVAL, "no GEMM tile fits (sub-projection boundaries must be x128)");
   const int cg = best.cg;
   bn = best.bn;
-  const int sched = force_sched == 2 ? 2 : best.sched;
+  const int sched = force_sched >= 2 ? force_sched : best.sched;
   const int nm = (M + kGemmBM * cg - 1) / (kGemmBM * cg);
   CHECK_ARG(nm <= kMaxMTiles, "M=%d exceeds %d rows", M, kMaxMTiles * kGemmBM);
   CHECK_ARG(bn == 128 || bn == 256, "bn must be 0, 128 or 256");
@@ -449,12 +452,29 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   }
   p.partials = (float*)((char*)workspace + kCounterBytes);
   cudaStream_t st = (cudaStream_t)stream;
+  // "lean" pipelines (~128 KB smem, <= 128 registers) leave room on every SM for one CTA of the
+  // LoRA kernels running concurrently on a second stream (collm_set_gemm_lean / COLLM_GEMM_LEAN)
+  const char* lean_env = getenv("COLLM_GEMM_LEAN");
+  const bool lean = lean_env ? atoi(lean_env) != 0 : g_gemm_lean;
   if (cg == 2) {
+    if (lean) {
+      if (bn == 256) return launch_gemm<256, 4, 2>(ta, tb, th, tlb, p, grid, st);
+      return launch_gemm<128, 5, 2>(ta, tb, th, tlb, p, grid, st);
+    }
     if (bn == 256) return launch_gemm<256, 6, 2>(ta, tb, th, tlb, p, grid, st);
     return launch_gemm<128, 8, 2>(ta, tb, th, tlb, p, grid, st);
   }
+  if (lean) {
+    if (bn == 256) return launch_gemm<256, 3, 1>(ta, tb, th, tlb, p, grid, st);
+    return launch_gemm<128, 4, 1>(ta, tb, th, tlb, p, grid, st);
+  }
   if (bn == 256) return launch_gemm<256, 4, 1>(ta, tb, th, tlb, p, grid, st);
   return launch_gemm<128, 6, 1>(ta, tb, th, tlb, p, grid, st);
+}
+
+int collm_set_gemm_lean(int lean) {
+  g_gemm_lean = lean != 0;
+  return COLLM_OK;
 }
 
 // ------------------------------------------------------------------------------------ K5

@@ -21,8 +21,11 @@
 //         on the leader's TMEM-empty barrier.
 //
 // Roles (256 threads per CTA, 1 CTA/SM, persistent):
-//   warp 0 lane 0 : TMA producer (ring of STAGES smem stages, full/empty mbarriers)
-//   warp 1 lane 0 : tcgen05.mma issuer into a double-buffered TMEM accumulator (2 x BN columns)
+//   warp 0        : TMA producer (ring of STAGES smem stages, full/empty mbarriers; one
+//                   elected lane issues)
+//   warp 1        : tcgen05.mma issuer into a double-buffered TMEM accumulator (2 x BN columns;
+//                   the whole warp runs the loop on uniform registers, one elected lane issues
+//                   each stage's group of MMAs and its commit)
 //   warp 2        : TMEM allocator
 //   warps 4..7    : epilogue — tcgen05.ld 32x32b -> bf16 -> st.global, overlapped with the next
 //                   segment's main loop through the second accumulator buffer.
@@ -184,7 +187,7 @@ struct StreamK {
 };
 
 template <int BN, int STAGES, int CG>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can co-reside
     gemm_lora_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmLB,
                      const GemmLoraParams p) {
@@ -251,8 +254,9 @@ __global__ void __launch_bounds__(256, 1)
   sk.init(s_prefix, p.num_m_tiles, p.num_n_tiles, gridDim.x / CG, p.sched);
   const int unit = blockIdx.x / CG;  // CTA pair (or CTA) index in the schedule
 
-  if (warp == 0 && lane == 0) {
-    // ===================== TMA producer (both CTAs of a pair) =====================
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs of a pair; one elected lane issues) =====
+    const bool issuer = elect_one();
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t rc = p.lora_rc;
@@ -266,10 +270,19 @@ __global__ void __launch_bounds__(256, 1)
       const int hcol = has_lora ? p.sub_h_col[sub_of_n0(p, n0)] : 0;
       for (int i = sg.k0; i < sg.k1; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
+        if (!issuer) {
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          continue;
+        }
         uint8_t* sa = smem + stage * L::kStageBytes;
         uint32_t bytes;
         if (i < n_lora) bytes = (BM + L::kBRows) * rc * 2;
         else bytes = L::kStageBytes;
+        if (p.sched == 3) {  // debug: no operand loads (measures the MMA issue rate alone)
+          if (leader) mbar_arrive(&full[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          continue;
+        }
         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * CG);
         if (i < n_lora) {
           const int s = p.tile_slot_ptr[st_tile] + i / p.lora_chunks;
@@ -297,8 +310,9 @@ __global__ void __launch_bounds__(256, 1)
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     });
-  } else if (warp == 1 && lane == 0 && leader) {
-    // ===================== tcgen05.mma issuer (the pair's leader) =====================
+  } else if (warp == 1 && leader) {
+    // ===================== tcgen05.mma issuer (the pair's leader; the whole warp runs the loop,
+    // one elected lane issues each stage's group of MMAs + its commit) =====================
     constexpr uint32_t idesc = umma_idesc_bf16(UNIT_M, BN);
     int stage = 0;
     uint32_t phase = 0;
@@ -323,23 +337,27 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
         const uint32_t sa = smem_base + stage * L::kStageBytes;
         if (i < n_lora) {
-          for (uint32_t k = 0; k < lsteps; ++k) {
-            mma(d_tmem, umma_desc_kmajor(sa + k * 32, lrow),
-                umma_desc_kmajor(sa + L::kABytes + k * 32, lrow), accumulate);
-            accumulate = 1;
+          if (elect_one()) {
+            for (uint32_t k = 0; k < lsteps; ++k)
+              mma(d_tmem, umma_desc_kmajor(sa + k * 32, lrow),
+                  umma_desc_kmajor(sa + L::kABytes + k * 32, lrow), accumulate | k);
+            commit(&empty[stage]);
           }
         } else {
+          if (elect_one()) {
 #pragma unroll
-          for (uint32_t k = 0; k < BK / 16; ++k) {
-            mma(d_tmem, umma_desc_kmajor(sa + k * 32, 128),
-                umma_desc_kmajor(sa + L::kABytes + k * 32, 128), accumulate);
-            accumulate = 1;
+            for (uint32_t k = 0; k < BK / 16; ++k)
+              mma(d_tmem, umma_desc_kmajor(sa + k * 32, 128),
+                  umma_desc_kmajor(sa + L::kABytes + k * 32, 128), accumulate | k);
+            commit(&empty[stage]);
           }
         }
-        commit(&empty[stage]);
+        __syncwarp();
+        accumulate = 1;
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      commit(&tfull[acc]);
+      if (elect_one()) commit(&tfull[acc]);
+      __syncwarp();
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     });

@@ -218,20 +218,36 @@ class LoraProjection:
     def forward(self, X: torch.Tensor, plan: DevicePlan, Y: torch.Tensor | None = None,
                 n_train: int = 0) -> tuple[torch.Tensor, ForwardCache]:
         """K1 + K2 over all rows of the pass: Y = X.W^T + per-row s_a.(X.A_a^T).B_a^T."""
+        cache = self.forward_lora(X, plan, n_train)
+        return self.forward_gemm(cache, plan, Y), cache
+
+    def forward_lora(self, X: torch.Tensor, plan: DevicePlan, n_train: int = 0) -> ForwardCache:
+        """K1 (rank space): H16 and the GEMM's LoRA slot blocks for every row of the pass."""
         spec = self.spec
         T = plan.n_rows
         if X.shape[0] < T or X.shape[1] != spec.in_features:
             raise ConfigurationError(f"{spec.name}: X {tuple(X.shape)} vs T={T}, K={spec.in_features}")
-        if Y is None:
-            Y = torch.empty(T, spec.out_features, dtype=torch.bfloat16, device=self.device)
         H16, Hslots = self._buffers(T, plan.n_slots)
-        R, rp, K = spec.R, spec.r_pad, spec.in_features
+        R, K = spec.R, spec.in_features
         if plan.n_slots:
             Hs = Hslots[: plan.n_slots * TILE_M]
             groups = [(g, min(64, R - g), 0, K) for g in range(0, R, 64)]
             ops.lora_shrink(X, self.A, plan.shrink_tiles, plan.n_shrink_tiles, self.scale, groups,
                             R, H16=H16, Hslots=Hs, slot_of_row=plan.slot_of_row,
                             tile_slot_ptr=plan.tile_slot_ptr)
+        return ForwardCache(X=X, H16=H16, n_train=n_train)
+
+    def forward_gemm(self, cache: ForwardCache, plan: DevicePlan,
+                     Y: torch.Tensor | None = None) -> torch.Tensor:
+        """K2: the base projection with the multi-adapter expand fused into the accumulator."""
+        spec = self.spec
+        T = plan.n_rows
+        X = cache.X
+        if Y is None:
+            Y = torch.empty(T, spec.out_features, dtype=torch.bfloat16, device=self.device)
+        rp = spec.r_pad
+        if plan.n_slots:
+            Hs = self._Hslots[: plan.n_slots * TILE_M]
             bnd = spec.sub_bounds
             ops.gemm_lora(X, self.W, Y, M=T, Hslots=Hs, h_rows=Hs.shape[0],
                           LB=self.B.view(self.n_adapters * spec.out_features, rp),
@@ -241,7 +257,7 @@ class LoraProjection:
                           sub_h_col=[s * rp for s in range(len(spec.subs))])
         else:
             ops.gemm_lora(X, self.W, Y, M=T)
-        return Y, ForwardCache(X=X, H16=H16, n_train=n_train)
+        return Y
 
     def _grad_groups(self, dY=None, X_tr=None, H_tr=None, dH16=None, *, targets: str):
         """The K5 group table of this projection: dB per sub-projection (U = dY, V = H16) and
@@ -278,37 +294,63 @@ class LoraProjection:
         caller already advanced (``OptimizerState.advance``); otherwise the gradient is stored (or
         added, ``accumulate``) into the grad buffers, e.g. for a cross-replica allreduce followed
         by :meth:`apply_optimizer`."""
+        if cache.n_train <= 0:
+            return None
+        self.backward_dh(dY, cache, train_plan)
+        if need_dx:
+            dX = self.backward_dx(dY, cache, train_plan, dX)
+        self.backward_grads(dY, cache, optimizer=optimizer, accumulate=accumulate,
+                            grad_scale=grad_scale)
+        return dX
+
+    def _require_train(self) -> TrainState:
         st = self.train_state
         if st is None:
             raise ConfigurationError(f"{self.spec.name}: no trainable adapter (make_trainable)")
+        return st
+
+    def backward_dh(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan) -> torch.Tensor:
+        """K1: dH = s * dY . B_t, one rank group per sub-projection (its own N range)."""
+        st = self._require_train()
         spec = self.spec
         Ttr = cache.n_train
-        if Ttr <= 0:
-            return None
-        K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
+        rp, R = spec.r_pad, spec.R
         bnd = spec.sub_bounds
         dH16 = self._dh_buffer(Ttr)
-        # K1: dH = s * dY . B_t, one rank group per sub-projection (its own N range)
         groups = [(s * rp + g, min(64, rp - g), bnd[s], bnd[s + 1])
                   for s in range(len(spec.subs)) for g in range(0, rp, 64)]
         ops.lora_shrink(dY, st.BT16, train_plan.shrink_tiles, train_plan.n_shrink_tiles,
                         self.scale, groups, R, a_stride=0, H16=dH16)
-        # K3: dX = dY . W + dH . A_t
-        if need_dx:
-            if dX is None:
-                dX = torch.empty(Ttr, K, dtype=torch.bfloat16, device=self.device)
-            ops.gemm_lora(dY, self.WT, dX, M=Ttr, Hslots=dH16, h_rows=Ttr, LB=st.AT16, lb_rows=K,
-                          tile_slot_ptr=train_plan.tile_slot_ptr,
-                          slot_adapter=train_plan.slot_adapter, lora_rank=R,
-                          lb_rows_per_adapter=0)
-        # K5: dB = dY^T . H16 (per sub), dA^T = X^T . dH16 — one launch, fused AdamW or grad store
+        return dH16
+
+    def backward_dx(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan,
+                    dX: torch.Tensor | None = None) -> torch.Tensor:
+        """K3: dX = dY . W + dH . A_t (reads A_t^T: run before this projection's optimizer step)."""
+        st = self._require_train()
+        spec = self.spec
+        Ttr = cache.n_train
+        K, R = spec.in_features, spec.R
+        if dX is None:
+            dX = torch.empty(Ttr, K, dtype=torch.bfloat16, device=self.device)
+        dH16 = self._dh_buffer(Ttr)
+        ops.gemm_lora(dY, self.WT, dX, M=Ttr, Hslots=dH16, h_rows=Ttr, LB=st.AT16, lb_rows=K,
+                      tile_slot_ptr=train_plan.tile_slot_ptr, slot_adapter=train_plan.slot_adapter,
+                      lora_rank=R, lb_rows_per_adapter=0)
+        return dX
+
+    def backward_grads(self, dY: torch.Tensor, cache: ForwardCache, *,
+                       optimizer: OptimizerState | None = None, accumulate: bool = False,
+                       grad_scale: float = 1.0) -> None:
+        """K5: dB = dY^T . H16 (per sub), dA^T = X^T . dH16 — one launch, fused AdamW or store."""
+        self._require_train()
+        Ttr = cache.n_train
+        dH16 = self._dh_buffer(Ttr)
         rg = self._grad_groups(dY, cache.X[:Ttr], cache.H16[:Ttr], dH16,
                                targets="full" if optimizer is not None else "grad")
         mode = _lib.MODE_ADAMW if optimizer is not None else _lib.MODE_STORE_GRAD
         ops.lora_reduce(Ttr, rg, mode, accum_in=accumulate, grad_scale=grad_scale,
                         adamw=optimizer.args if optimizer is not None else None,
                         device=self.device)
-        return dX
 
     def apply_optimizer(self, optimizer: OptimizerState) -> None:
         """AdamW from the grad buffers (after a cross-replica allreduce of the gradients)."""

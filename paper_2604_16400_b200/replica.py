@@ -22,6 +22,7 @@ from dataclasses import dataclass
 
 import torch
 
+from . import _lib
 from .configs import LayerConfig
 from .domain import ConfigurationError, InferenceItem, MixedBatch, TrainItem
 from .layer import AdamWConfig, LoraProjection, OptimizerState
@@ -63,6 +64,8 @@ class ReplicaStack:
             self.init_synthetic(seed)
         self._acts: dict | None = None
         self._graph: torch.cuda.CUDAGraph | None = None
+        self._side: torch.cuda.Stream | None = None
+        self.overlap = False
 
     # ------------------------------------------------------------------ weights
     @torch.no_grad()
@@ -197,48 +200,112 @@ class ReplicaStack:
 
     # ------------------------------------------------------------------ the step
     def run_step(self, plan: StepPlan | None = None, optimizer_step: bool = True,
-                 advance: bool = True) -> torch.Tensor:
+                 advance: bool = True, overlap: bool | None = None) -> torch.Tensor:
         """Enqueue one full co-batched step on the current stream; returns the final hidden state
         buffer (device).  With ``advance`` the optimizer step counter is bumped first (keep it
-        False inside CUDA-graph capture; call ``opt.advance()`` before each replay instead)."""
+        False inside CUDA-graph capture; call ``opt.advance()`` before each replay instead).
+
+        ``overlap``: the HBM/latency-bound rank-space kernels (K1 shrink, K5 reductions) run on a
+        side stream one projection ahead of the tensor-bound GEMMs on the main stream, ordered
+        only by their true dependencies (shrink -> GEMM of the same projection; a layer's input
+        produced by the previous layer's down GEMM; the optimizer step that rewrites A_t^T after
+        the dX GEMM that reads it).  The GEMMs then use their lean pipelines so one LoRA CTA fits
+        next to each GEMM CTA."""
         plan = plan or self._plan
         a = self._acts
         if a is None:
             raise ConfigurationError("allocate() the step buffers first")
+        if overlap is None:
+            overlap = self.overlap
         L = self.cfg.model.layers
         Ttr = plan.n_train
         if advance and Ttr and optimizer_step:
             self.opt.advance()
+        main = torch.cuda.current_stream(self.device)
+        side = self._side_stream() if overlap else main
+        _lib.load().collm_set_gemm_lean(1 if overlap else 0)
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+
+        def on(stream, fn, wait=None):
+            if wait is not None and overlap:
+                stream.wait_event(wait)
+            with torch.cuda.stream(stream):
+                out = fn()
+            e = ev()
+            e.record(stream)
+            return out, e
+
         plan.device.expand()
+        e_plan = ev()
+        e_plan.record(main)
         first = self.specs[0].name
-        caches: list[dict] = []
+        # ---------------- forward: shrink(i+1) on the side stream while GEMM(i) runs
+        fwd = []  # (layer, proj, X, Y)
         for l, layer in enumerate(self.layers):
             syn = l if a["distinct_synthetic"] else 0
-            c = {}
             for proj in layer:
                 name = proj.spec.name
-                if name in ENTRY:
-                    X = a["X"][l]
-                elif name == "o":
-                    X = a["Xo"][syn]
-                else:  # down
-                    X = a["Xd"][syn]
+                X = a["X"][l] if name in ENTRY else (a["Xo"][syn] if name == "o" else a["Xd"][syn])
                 Y = a["X"][l + 1] if name == "down" else a["Y"][name]
-                _, c[name] = proj.forward(X, plan.device, Y, n_train=Ttr)
-            caches.append(c)
+                fwd.append((l, proj, X, Y))
+        caches: list[dict] = [dict() for _ in range(L)]
+        e_gemm = {}
+        pending = None  # (cache, event) of the shrink of the next projection
+
+        def shrink(i, wait):
+            l, proj, X, _ = fwd[i]
+            return on(side, lambda: proj.forward_lora(X, plan.device, n_train=Ttr), wait)
+
+        pending = shrink(0, e_plan)
+        for i, (l, proj, X, Y) in enumerate(fwd):
+            cache, e_sh = pending
+            caches[l][proj.spec.name] = cache
+            _, e_g = on(main, lambda: proj.forward_gemm(cache, plan.device, Y), e_sh)
+            e_gemm[i] = e_g
+            if i + 1 < len(fwd):
+                nl, nproj, _, _ = fwd[i + 1]
+                # the next layer's entry projections read X_{l+1} = this (down) GEMM's output
+                needs = e_g if (nl != l and nproj.spec.name in ENTRY) else None
+                pending = shrink(i + 1, needs)
         if Ttr:
             opt = self.opt if optimizer_step else None
+            bwd = []  # (layer, proj, dY, dX)
             for l in range(L - 1, -1, -1):
                 syn = l if a["distinct_synthetic"] else 0
                 for proj in reversed(self.layers[l]):
                     name = proj.spec.name
-                    if name == "down":
-                        dY = a["dY_top"] if l == L - 1 else a["dX_first"][l + 1]
-                    else:
-                        dY = a["dY"][syn][name]
+                    dY = (a["dY_top"] if l == L - 1 else a["dX_first"][l + 1]) if name == "down" \
+                        else a["dY"][syn][name]
                     dX = a["dX_first"][l] if name == first else a["dX"][name]
-                    proj.backward(dY, caches[l][name], plan.train_device, dX, optimizer=opt)
+                    bwd.append((l, proj, dY, dX))
+            e_last_gemm = e_gemm[len(fwd) - 1]
+
+            def dh(i, wait):
+                l, proj, dY, _ = bwd[i]
+                return on(side, lambda: proj.backward_dh(dY, caches[l][proj.spec.name],
+                                                         plan.train_device), wait)
+
+            _, e_dh = dh(0, e_last_gemm)
+            for i, (l, proj, dY, dX) in enumerate(bwd):
+                cache = caches[l][proj.spec.name]
+                _, e_g = on(main, lambda: proj.backward_dx(dY, cache, plan.train_device, dX), e_dh)
+                if i + 1 < len(bwd):
+                    nl, nproj, _, _ = bwd[i + 1]
+                    # down of the next (lower) layer consumes dX_first of this layer's first proj
+                    needs = e_g if nproj.spec.name == "down" else None
+                    _, e_dh = dh(i + 1, needs)
+                # the fused optimizer rewrites A_t^T, which this projection's dX GEMM reads
+                on(side, lambda: proj.backward_grads(dY, cache, optimizer=opt), e_g)
+        if overlap:
+            e_end = ev()
+            e_end.record(side)
+            main.wait_event(e_end)
         return a["X"][L]
+
+    def _side_stream(self) -> torch.cuda.Stream:
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        return self._side
 
     # ------------------------------------------------------------------ graphs
     def capture(self, plan: StepPlan | None = None, optimizer_step: bool = True) -> torch.cuda.CUDAGraph:
