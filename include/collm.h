@@ -115,8 +115,9 @@ int collm_set_gemm_lean(int lean);
  * One group = one reduction C[p,q] = sum_t U[t, u_off+p] * V[t, v_off+q] (p < P, q < Q <= 64;
  * P, Q multiples of 8) and the tensors it updates.  Element (p,q) lives at fp32 index
  * (c_row_off+p)*ldc + c_col_off+q of grad / master / m / v and of out_same (bf16), and at
- * (t_row_off+q)*ld_trans + t_col_off+p of out_trans (bf16).  One launch serves all groups of a
- * projection (dB per sub-projection: U = dY, V = H16; dA^T: U = X_tr, V = dH16).
+ * (t_row_off+q)*ld_trans + t_col_off+p of out_trans (bf16).  One launch serves up to 16 groups
+ * — all projections of a layer (per projection: dB per sub-projection, U = dY, V = H16; dA^T in
+ * <= 64-rank chunks, U = X_tr, V = dH16); all groups share T.
  * Replaces: AdapterParams.perturbed (launcher.py:43-47) and perf.train_step (perf.py:111-126). */
 typedef struct {
   const void* U;     /* bf16 [T, ldu] */

@@ -22,7 +22,7 @@
 
 namespace collm {
 
-constexpr int kReduceMaxGroups = 8;
+constexpr int kReduceMaxGroups = 16;  // a whole layer's projections (<= 14 at BASELINE shapes)
 constexpr int kReducePT = 128;     // P rows per CTA tile (8 warps x 16)
 constexpr int kReduceTC = 32;      // T rows per pipeline stage
 constexpr int kReduceStages = 4;   // cp.async ring depth

@@ -338,17 +338,23 @@ class LoraProjection:
                       lora_rank=R, lb_rows_per_adapter=0)
         return dX
 
+    def grad_groups(self, dY: torch.Tensor, cache: ForwardCache, *,
+                    optimizer: OptimizerState | None = None) -> list:
+        """This projection's K5 group table (dB per sub, dA^T chunks) for a given dY — so a caller
+        can reduce several projections (a whole layer) in ONE launch (`ops.lora_reduce`)."""
+        self._require_train()
+        Ttr = cache.n_train
+        dH16 = self._dh_buffer(Ttr)
+        return self._grad_groups(dY, cache.X[:Ttr], cache.H16[:Ttr], dH16,
+                                 targets="full" if optimizer is not None else "grad")
+
     def backward_grads(self, dY: torch.Tensor, cache: ForwardCache, *,
                        optimizer: OptimizerState | None = None, accumulate: bool = False,
                        grad_scale: float = 1.0) -> None:
         """K5: dB = dY^T . H16 (per sub), dA^T = X^T . dH16 — one launch, fused AdamW or store."""
-        self._require_train()
-        Ttr = cache.n_train
-        dH16 = self._dh_buffer(Ttr)
-        rg = self._grad_groups(dY, cache.X[:Ttr], cache.H16[:Ttr], dH16,
-                               targets="full" if optimizer is not None else "grad")
+        rg = self.grad_groups(dY, cache, optimizer=optimizer)
         mode = _lib.MODE_ADAMW if optimizer is not None else _lib.MODE_STORE_GRAD
-        ops.lora_reduce(Ttr, rg, mode, accum_in=accumulate, grad_scale=grad_scale,
+        ops.lora_reduce(cache.n_train, rg, mode, accum_in=accumulate, grad_scale=grad_scale,
                         adamw=optimizer.args if optimizer is not None else None,
                         device=self.device)
 

@@ -22,7 +22,7 @@ from dataclasses import dataclass
 
 import torch
 
-from . import _lib
+from . import _lib, ops
 from .configs import LayerConfig
 from .domain import ConfigurationError, InferenceItem, MixedBatch, TrainItem
 from .layer import AdamWConfig, LoraProjection, OptimizerState
@@ -285,17 +285,27 @@ class ReplicaStack:
                 return on(side, lambda: proj.backward_dh(dY, caches[l][proj.spec.name],
                                                          plan.train_device), wait)
 
+            mode = _lib.MODE_ADAMW if opt is not None else _lib.MODE_STORE_GRAD
             _, e_dh = dh(0, e_last_gemm)
+            layer_groups: list = []
             for i, (l, proj, dY, dX) in enumerate(bwd):
                 cache = caches[l][proj.spec.name]
                 _, e_g = on(main, lambda: proj.backward_dx(dY, cache, plan.train_device, dX), e_dh)
+                nl = bwd[i + 1][0] if i + 1 < len(bwd) else -1
                 if i + 1 < len(bwd):
-                    nl, nproj, _, _ = bwd[i + 1]
                     # down of the next (lower) layer consumes dX_first of this layer's first proj
-                    needs = e_g if nproj.spec.name == "down" else None
+                    needs = e_g if bwd[i + 1][1].spec.name == "down" else None
                     _, e_dh = dh(i + 1, needs)
-                # the fused optimizer rewrites A_t^T, which this projection's dX GEMM reads
-                on(side, lambda: proj.backward_grads(dY, cache, optimizer=opt), e_g)
+                layer_groups += proj.grad_groups(dY, cache, optimizer=opt)
+                if nl != l:
+                    # K5 of the whole layer in one launch (the weight gradients feed nothing
+                    # later in the step), after the layer's last dX GEMM: the fused optimizer
+                    # rewrites A_t^T, which those GEMMs read
+                    grp = layer_groups
+                    on(side, lambda: ops.lora_reduce(
+                        Ttr, grp, mode, adamw=opt.args if opt is not None else None,
+                        device=self.device), e_g)
+                    layer_groups = []
         if overlap:
             e_end = ev()
             e_end.record(side)
@@ -339,9 +349,14 @@ class ReplicaStack:
                    for s in self.specs) * self.cfg.model.layers
 
     def lora_bytes(self, plan: StepPlan | None = None) -> dict:
-        """Algorithmic HBM bytes of the LoRA segments per step: distinct adapters'
-        A and B once (bf16), X read by the shrink, H write+read; backward adds dY and X_tr reads
-        and the fp32 optimizer read-modify-write."""
+        """Algorithmic HBM bytes of the rank-space (LoRA) kernels per step, counted
+        as the unique minimum each pass must move (ranks unpadded, cache re-reads not counted):
+          forward  (K1): X read, every distinct adapter's A read once, H written once;
+          backward (K1 dH + K5): dY read once, X_tr and H_tr read, B_t read, dH written once,
+                   and the fused AdamW's fp32 master/m/v read+write (24 B/param) plus the four
+                   bf16 working copies it rewrites (8 B/param).
+        The adapters' B matrices of the forward expand are read by the tensor-core GEMM (fused
+        epilogue K-steps) and are counted there, not here."""
         plan = plan or self._plan
         T, Ttr = plan.n_rows, plan.n_train
         n_distinct = len({a for a in plan.batch.seg_adapter if a >= 0})
@@ -349,8 +364,10 @@ class ReplicaStack:
         for s in self.specs:
             K, N, r = s.in_features, s.out_features, s.rank
             nsub = len(s.subs)
-            fwd += n_distinct * 2 * r * (K * nsub + N) + 2 * T * K + 4 * T * s.R
+            fwd += 2 * T * K + n_distinct * 2 * nsub * r * K + 2 * T * nsub * r
             if Ttr:
-                bwd += 2 * Ttr * N + 2 * Ttr * K + 16 * r * (K * nsub + N)
+                params = r * N + nsub * r * K
+                bwd += (2 * Ttr * N + 2 * Ttr * K + 2 * Ttr * nsub * r + 2 * r * N
+                        + 2 * Ttr * nsub * r + 32 * params)
         L = self.cfg.model.layers
         return {"fwd": fwd * L, "bwd": bwd * L, "total": (fwd + bwd) * L}

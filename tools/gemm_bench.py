@@ -11,12 +11,18 @@ from paper_2604_16400_b200 import ops  # noqa: E402
 SHAPES = [("qkv", 1024, 12288, 4096), ("o", 1024, 4096, 4096), ("gate_up", 1024, 22016, 4096),
           ("down", 1024, 4096, 11008), ("dX_qkv", 512, 4096, 12288), ("dX_o", 512, 4096, 4096),
           ("dX_gu", 512, 4096, 22016), ("dX_down", 512, 11008, 4096)]
+if os.environ.get("BIG"):
+    SHAPES = SHAPES + [("big", 4096, 8192, 8192), ("big2", 8192, 8192, 8192)]
 DEFAULT = "auto,1:256:dp,1:128:dp,1:256:hybrid,2:256:dp,2:128:dp,2:256:hybrid,2:128:hybrid"
 
 
 def set_variant(v):
     for k in ("COLLM_GEMM_CG", "COLLM_GEMM_BN", "COLLM_GEMM_SCHED"):
         os.environ.pop(k, None)
+    os.environ.pop("COLLM_GEMM_LEAN", None)
+    if v.endswith("+lean"):
+        os.environ["COLLM_GEMM_LEAN"] = "1"
+        v = v[:-5]
     if v != "auto":
         cg, bn, sc = v.split(":")
         os.environ.update(COLLM_GEMM_CG=cg, COLLM_GEMM_BN=bn, COLLM_GEMM_SCHED=sc)
@@ -43,6 +49,19 @@ def main():
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / reps * 1e3
             res[(name, v)] = (us, 2 * M * N * K / (us * 1e-6) / 1e12)
+        # cuBLAS (torch.matmul) on the same shape, same W rotation (the library baseline)
+        for i in range(3):
+            torch.matmul(A, Ws[i % 3].t(), out=Y)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(30):
+            torch.matmul(A, Ws[i % 3].t(), out=Y)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 30 * 1e3
+        res[(name, "cublas")] = (us, 2 * M * N * K / (us * 1e-6) / 1e12)
+    variants = variants + ["cublas"]
     print(f"{'shape':8s} " + " ".join(f"{v:>14s}" for v in variants))
     for name, *_ in SHAPES:
         print(f"{name:8s} " + " ".join(f"{res[(name, v)][0]:7.1f}/{res[(name, v)][1]:5.0f}" for v in variants))

@@ -81,7 +81,10 @@ for f in sorted(os.listdir(SRC)):
                 "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
                 "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
                 "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-                "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_elapsed"]
+                "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+                "lts__t_sectors_srcunit_tex.sum", "lts__t_sector_hit_rate.pct",
+                "sm__cycles_elapsed.avg.per_second"]
         extra = []
         if len(rr) > 2:
             hdr, units, vals = rr[0], rr[1], rr[2]

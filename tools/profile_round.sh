@@ -3,14 +3,17 @@
 # tensor-pipe activity for the whole step, and --set full captures of the key kernels.
 # usage: bash tools/profile_round.sh r01 [config]
 TAG=${1:-r01}; CFG=${2:-llama2-7b}; OUT=gpurun_out/$TAG; mkdir -p $OUT
-N=641
+# launches per step (and per kind) from one eager step
+read N NG NS NR < <(python tools/profile_step.py --config $CFG --count 2>/dev/null | tail -1)
+echo "launches/step=$N gemm=$NG shrink=$NS reduce=$NR"
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_lora|lora_|expand_" \
     -s $N -c $N --csv --log-file $OUT/launches_$CFG.csv python tools/profile_step.py --config $CFG 2>&1 | tail -1
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,lts__throughput.avg.pct_of_peak_sustained_elapsed \
     --clock-control none -k regex:"gemm_lora|lora_|expand_" -s $N -c $N --csv --log-file $OUT/metrics_$CFG.csv \
     python tools/profile_step.py --config $CFG 2>&1 | tail -1
-# full sets: qkv forward GEMM (launch 2 of the step), its shrink (1), first dX GEMM, first reduce
-ncu --set full --clock-control none --import-source on -k regex:"gemm_lora" -s 256 -c 1 -o $OUT/full_gemm_fwd_qkv python tools/profile_step.py --config $CFG 2>&1 | tail -1
-ncu --set full --clock-control none --import-source on -k regex:"gemm_lora" -s 384 -c 1 -o $OUT/full_gemm_dx_down python tools/profile_step.py --config $CFG 2>&1 | tail -1
-ncu --set full --clock-control none --import-source on -k regex:"lora_shrink" -s 256 -c 1 -o $OUT/full_shrink_fwd_qkv python tools/profile_step.py --config $CFG 2>&1 | tail -1
-ncu --set full --clock-control none --import-source on -k regex:"lora_reduce" -s 128 -c 1 -o $OUT/full_reduce_down python tools/profile_step.py --config $CFG 2>&1 | tail -1
+# full sets: first forward GEMM (q|k|v of layer 0) and its shrink, first dX GEMM (down of the top
+# layer), first K5 reduction of the step
+ncu --set full --clock-control none --import-source on -k regex:"gemm_lora" -s $NG -c 1 -o $OUT/full_gemm_fwd_qkv python tools/profile_step.py --config $CFG 2>&1 | tail -1
+ncu --set full --clock-control none --import-source on -k regex:"gemm_lora" -s $((NG + NG / 2)) -c 1 -o $OUT/full_gemm_dx_down python tools/profile_step.py --config $CFG 2>&1 | tail -1
+ncu --set full --clock-control none --import-source on -k regex:"lora_shrink" -s $NS -c 1 -o $OUT/full_shrink_fwd_qkv python tools/profile_step.py --config $CFG 2>&1 | tail -1
+ncu --set full --clock-control none --import-source on -k regex:"lora_reduce" -s $NR -c 1 -o $OUT/full_reduce_layer python tools/profile_step.py --config $CFG 2>&1 | tail -1
