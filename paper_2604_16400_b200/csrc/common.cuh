@@ -261,6 +261,32 @@ __device__ __forceinline__ uint4 ld_global_nc_v4(const void* p) {
   return r;
 }
 
+// cp.async (LDGSTS) 16-byte global -> shared copies, L1 bypassed; zero-fill when !pred
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, bool pred) {
+  const uint32_t s = smem_u32(smem);
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// cp.async.wait_group with a runtime depth (0..7)
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+  switch (n) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    case 3: cp_async_wait<3>(); break;
+    case 4: cp_async_wait<4>(); break;
+    case 5: cp_async_wait<5>(); break;
+    case 6: cp_async_wait<6>(); break;
+    default: cp_async_wait<7>(); break;
+  }
+}
+
 // mma.sync m16n8k16 bf16 -> fp32 (legacy warp-level tensor path; used only by the HBM-bound
 // rank-space kernels where the tensor pipe is nowhere near the bound).
 __device__ __forceinline__ void mma_m16n8k16_bf16(float (&d)[4], uint32_t a0, uint32_t a1,
