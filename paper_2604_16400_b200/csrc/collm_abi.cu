@@ -107,7 +107,8 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, ui
 
 template <int BN, int STAGES, int CG>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& th,
-                const CUtensorMap& tlb, const GemmLoraParams& p, int grid, cudaStream_t stream) {
+                const CUtensorMap& tlb, const CUtensorMap& ty, const GemmLoraParams& p, int grid,
+                cudaStream_t stream) {
   using L = GemmSmem<BN, STAGES, CG>;
   static bool configured = false;
   if (!configured) {
@@ -127,7 +128,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_lora_kernel<BN, STAGES, CG>, ta, tb, th, tlb, p));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_lora_kernel<BN, STAGES, CG>, ta, tb, th, tlb, ty, p));
   return COLLM_OK;
 }
 
@@ -295,6 +296,9 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
 
 // ------------------------------------------------------------------------------------ K2/K3
 static bool g_gemm_lean = false;
+// Shared-memory budget of the K5 reduction: lean = next to a GEMM CTA on the same SM (the
+// two-stream overlap, collm_set_gemm_lean), else up to the full ring depth.
+static bool g_reduce_lean = false;
 
 // debug-only: device pointer of the last GEMM's timeline (COLLM_GEMM_DEBUG set)
 unsigned long long* collm_debug_timeline = nullptr;
@@ -395,8 +399,10 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   for (int i = 0; i <= kMaxSub; ++i) p.sub_n_start[i] = (i == 0) ? 0 : N;
   for (int i = 0; i < kMaxSub; ++i) p.sub_h_col[i] = 0;
 
-  CUtensorMap ta, tb, th, tlb;
+  CUtensorMap ta, tb, th, tlb, ty;
   int rc = make_tmap(&ta, A, K, M, lda, kGemmBK, kGemmBM);
+  if (rc) return rc;
+  rc = make_tmap(&ty, Y, N, M, ldy, 32, 32);  // epilogue TMA stores, [32 x 32] boxes
   if (rc) return rc;
   rc = make_tmap(&tb, B, K, N, ldb, kGemmBK, bn / cg);
   if (rc) return rc;
@@ -445,8 +451,8 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   {
     static unsigned long long* dbg_ptr = nullptr;
     const char* dbg_env = getenv("COLLM_GEMM_DEBUG");
-    if (dbg_env && !dbg_ptr) cudaMalloc(&dbg_ptr, 256 * 16 * 8);
-    if (dbg_env) cudaMemsetAsync(dbg_ptr, 0, 256 * 16 * 8, (cudaStream_t)stream);
+    if (dbg_env && !dbg_ptr) cudaMalloc(&dbg_ptr, 256 * 32 * 8);
+    if (dbg_env) cudaMemsetAsync(dbg_ptr, 0, 256 * 32 * 8, (cudaStream_t)stream);
     p.dbg = dbg_env ? dbg_ptr : nullptr;
     collm_debug_timeline = p.dbg;
   }
@@ -458,30 +464,67 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   const bool lean = lean_env ? atoi(lean_env) != 0 : g_gemm_lean;
   if (cg == 2) {
     if (lean) {
-      if (bn == 256) return launch_gemm<256, 4, 2>(ta, tb, th, tlb, p, grid, st);
-      return launch_gemm<128, 5, 2>(ta, tb, th, tlb, p, grid, st);
+      static const int lean_stages = [] { const char* e = getenv("COLLM_GEMM_LEAN_STAGES"); return e ? atoi(e) : 5; }();
+      if (bn == 256) {
+        if (lean_stages == 5) return launch_gemm<256, 5, 2>(ta, tb, th, tlb, ty, p, grid, st);
+        return launch_gemm<256, 4, 2>(ta, tb, th, tlb, ty, p, grid, st);
+      }
+      if (lean_stages == 5) return launch_gemm<128, 6, 2>(ta, tb, th, tlb, ty, p, grid, st);
+      return launch_gemm<128, 5, 2>(ta, tb, th, tlb, ty, p, grid, st);
     }
-    if (bn == 256) return launch_gemm<256, 6, 2>(ta, tb, th, tlb, p, grid, st);
-    return launch_gemm<128, 8, 2>(ta, tb, th, tlb, p, grid, st);
+    if (bn == 256) return launch_gemm<256, 6, 2>(ta, tb, th, tlb, ty, p, grid, st);
+    return launch_gemm<128, 8, 2>(ta, tb, th, tlb, ty, p, grid, st);
   }
   if (lean) {
-    if (bn == 256) return launch_gemm<256, 3, 1>(ta, tb, th, tlb, p, grid, st);
-    return launch_gemm<128, 4, 1>(ta, tb, th, tlb, p, grid, st);
+    if (bn == 256) return launch_gemm<256, 3, 1>(ta, tb, th, tlb, ty, p, grid, st);
+    return launch_gemm<128, 4, 1>(ta, tb, th, tlb, ty, p, grid, st);
   }
-  if (bn == 256) return launch_gemm<256, 4, 1>(ta, tb, th, tlb, p, grid, st);
-  return launch_gemm<128, 6, 1>(ta, tb, th, tlb, p, grid, st);
+  if (bn == 256) return launch_gemm<256, 4, 1>(ta, tb, th, tlb, ty, p, grid, st);
+  return launch_gemm<128, 6, 1>(ta, tb, th, tlb, ty, p, grid, st);
 }
 
 int collm_set_gemm_lean(int lean) {
   g_gemm_lean = lean != 0;
+  g_reduce_lean = lean != 0;
   return COLLM_OK;
 }
 
 // ------------------------------------------------------------------------------------ K5
-static int build_reduce_params(ReduceParams& p, const collm_reduce_group* groups, int n_groups,
-                               int& qmax, bool need_uv) {
+// ABI groups wider than kReduceMaxQ are reduced as several column chunks (same U, adjacent V
+// columns, adjacent C columns / transposed rows), each <= kReduceMaxQ and a multiple of 8.
+static int expand_reduce_groups(const collm_reduce_group* groups, int n_groups,
+                                collm_reduce_group* out, int* n_out) {
   CHECK_ARG(groups && n_groups >= 1 && n_groups <= kReduceMaxGroups, "n_groups=%d out of [1,%d]",
             n_groups, kReduceMaxGroups);
+  int n = 0;
+  for (int g = 0; g < n_groups; ++g) {
+    const collm_reduce_group& s = groups[g];
+    CHECK_ARG(s.P > 0 && s.P % 8 == 0 && s.Q > 0 && s.Q % 8 == 0 && s.Q <= 64,
+              "group %d: P=%d, Q=%d (need multiples of 8, Q <= 64)", g, s.P, s.Q);
+    const int chunks = (s.Q + kReduceMaxQ - 1) / kReduceMaxQ;
+    int off = 0;
+    for (int c = 0; c < chunks; ++c) {
+      const int q = ((s.Q / 8) * (c + 1) / chunks - (s.Q / 8) * c / chunks) * 8;
+      CHECK_ARG(n < kReduceMaxInner, "too many reduction groups after splitting (%d)", n + 1);
+      collm_reduce_group e = s;
+      e.v_off = s.v_off + off;
+      e.Q = q;
+      e.c_col_off = s.c_col_off + off;
+      e.t_row_off = s.t_row_off + off;
+      out[n++] = e;
+      off += q;
+    }
+  }
+  *n_out = n;
+  return COLLM_OK;
+}
+
+static int build_reduce_params(ReduceParams& p, const collm_reduce_group* abi_groups, int n_abi,
+                               int& qmax, bool need_uv) {
+  collm_reduce_group groups[kReduceMaxInner];
+  int n_groups = 0;
+  int rc = expand_reduce_groups(abi_groups, n_abi, groups, &n_groups);
+  if (rc) return rc;
   p.n_groups = n_groups;
   int tiles = 0;
   qmax = 0;
@@ -509,8 +552,6 @@ static int build_reduce_params(ReduceParams& p, const collm_reduce_group* groups
     gr.t_row_off = s.t_row_off;
     gr.t_col_off = s.t_col_off;
     gr.tile_begin = tiles;
-    CHECK_ARG(gr.P > 0 && gr.P % 8 == 0 && gr.Q > 0 && gr.Q % 8 == 0 && gr.Q <= 64,
-              "group %d: P=%d, Q=%d (need multiples of 8, Q <= 64)", g, gr.P, gr.Q);
     if (need_uv) {
       CHECK_ARG(gr.U && gr.V, "group %d: null U/V", g);
       CHECK_ARG(gr.u_off % 8 == 0 && gr.v_off % 8 == 0 && gr.ldu % 8 == 0 && gr.ldv % 8 == 0 &&
@@ -541,23 +582,31 @@ static int check_mode_targets(const ReduceParams& p, int mode, int accum_in) {
 
 size_t collm_reduce_workspace_bytes(const collm_reduce_group* groups, int n_groups, int tsplit) {
   if (tsplit <= 1 || !groups) return 0;
+  collm_reduce_group ex[kReduceMaxInner];
+  int n = 0;
+  if (expand_reduce_groups(groups, n_groups, ex, &n) != COLLM_OK) return 0;
   int tiles = 0;
-  for (int g = 0; g < n_groups; ++g) tiles += (groups[g].P + kReducePT - 1) / kReducePT;
+  for (int g = 0; g < n; ++g) tiles += (ex[g].P + kReducePT - 1) / kReducePT;
   return kCounterBytes + (size_t)tsplit * tiles * kReducePT * 64 * sizeof(float);
 }
 
 }  // extern "C"
 
+
 template <int QT>
-static int launch_reduce(const ReduceParams& p, cudaStream_t st) {
+static int launch_reduce(ReduceParams& p, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ReduceSmem<QT>::kTotal));
+                                  (int)ReduceSmem<QT>::total(kReduceMaxStages)));
     configured = true;
   }
+  const size_t budget = g_reduce_lean ? 44u * 1024 : 100u * 1024;
+  int stages = kReduceMaxStages;
+  while (stages > 2 && ReduceSmem<QT>::total(stages) > budget) --stages;
+  p.stages = stages;
   dim3 grid(p.n_tiles, p.tsplit);
-  lora_reduce_kernel<QT><<<grid, kReduceThreads, ReduceSmem<QT>::kTotal, st>>>(p);
+  lora_reduce_kernel<QT><<<grid, kReduceThreads, ReduceSmem<QT>::total(stages), st>>>(p);
   CUDA_TRY(cudaGetLastError());
   return COLLM_OK;
 }
@@ -594,7 +643,7 @@ int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int
   cudaStream_t st = (cudaStream_t)stream;
   if (qmax <= 16) return launch_reduce<16>(p, st);
   if (qmax <= 32) return launch_reduce<32>(p, st);
-  return launch_reduce<64>(p, st);
+  return launch_reduce<48>(p, st);
 }
 
 int collm_lora_apply(const collm_reduce_group* groups, int n_groups, int mode,

@@ -50,7 +50,7 @@ namespace collm {
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;
 constexpr int kMaxSub = 4;
-constexpr int kMaxMTiles = 2048;
+constexpr int kMaxMTiles = 512;   // rows <= 512 * 128 * CG per launch
 
 struct GemmLoraParams {
   int M, N, K;
@@ -87,8 +87,15 @@ struct GemmSmem {
   static constexpr uint32_t kBBytes = kBRows * kGemmBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
-  static constexpr uint32_t kPrefixOffset = kBarOffset + 256;
-  static constexpr uint32_t kTotal = kPrefixOffset + (kMaxMTiles + 1) * 4 + 1024;
+  static constexpr uint32_t kPrefixOffset = kBarOffset + 512;
+  // stream-K fix-up: earlier parts of a split tile stream into the idle pipeline stages as
+  // 32-column pieces (16 KB) through a ring of kFixSlots slots
+  static constexpr uint32_t kFixPiece = kGemmBM * 32 * 4;
+  static constexpr int kFixSlots = (STAGES * kStageBytes / kFixPiece) < 16 ? (STAGES * kStageBytes / kFixPiece) : 16;
+  // epilogue staging for the TMA stores: per epilogue warp 2 buffers of [32 rows x 32 cols] bf16
+  static constexpr uint32_t kEpiBuf = 32 * 32 * 2;
+  static constexpr uint32_t kEpiOffset = (kPrefixOffset + (kMaxMTiles + 1) * 4 + 1023) & ~1023u;
+  static constexpr uint32_t kTotal = kEpiOffset + 4 * 2 * kEpiBuf + 1024;
   static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
 };
 
@@ -190,7 +197,7 @@ template <int BN, int STAGES, int CG>
 __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can co-reside
     gemm_lora_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmLB,
-                     const GemmLoraParams p) {
+                     const __grid_constant__ CUtensorMap tmY, const GemmLoraParams p) {
   using L = GemmSmem<BN, STAGES, CG>;
   constexpr uint32_t BM = kGemmBM, BK = kGemmBK;
   constexpr uint32_t UNIT_M = BM * CG;
@@ -201,8 +208,8 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* fixbar = tempty + 2;  // stream-K fix-up: bulk copy of one partial into the stages
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixbar + 1);
+  uint64_t* fixbar = tempty + 2;  // stream-K fix-up ring: one barrier per 16 KB slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixbar + 16);
   int32_t* s_prefix = reinterpret_cast<int32_t*>(smem + L::kPrefixOffset);
 
   const int warp = threadIdx.x >> 5;
@@ -229,6 +236,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
     s_prefix[p.num_m_tiles] = acc;
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmY);
     if (has_lora) {
       tma_prefetch_desc(&tmH);
       tma_prefetch_desc(&tmLB);
@@ -241,7 +249,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4 * CG);
     }
-    mbar_init(fixbar, 1);
+    for (int k = 0; k < 16; ++k) mbar_init(&fixbar[k], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<L::kTmemCols, CG>(tmem_slot);
@@ -365,10 +373,12 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
     // ===================== epilogue (both CTAs: each its own 128 rows) =====================
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew+32)
     const int tid = threadIdx.x - 128;
-    uint32_t acc = 0, acc_phase = 0, fix_phase = 0;
+    uint32_t acc = 0, acc_phase = 0;
     int seg_i = 0;
+    uint32_t epi_i = 0;  // TMA-store buffer toggle
+    uint8_t* epi_buf = smem + L::kEpiOffset;
     const int cta = blockIdx.x;
-    unsigned long long* dbg = p.dbg ? p.dbg + (size_t)cta * 16 : nullptr;
+    unsigned long long* dbg = p.dbg ? p.dbg + (size_t)cta * 32 : nullptr;
     if (dbg && tid == 0) dbg[0] = gtimer();
     sk.for_each(unit, [&](const Segment& sg_in) {
       Segment sg = sg_in;
@@ -392,28 +402,33 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
               }
             } while (v == 0);
           }
+          if (dbg) dbg[14] = gtimer();
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (dbg && tid == 0 && seg_i < 3) dbg[2 + 4 * seg_i] = gtimer();
-      // Finishing segment = this pair's last: the MMAs are done with the pipeline smem, so the
-      // first earlier part is pulled in with one bulk copy (the rest stream from L2).
-      int smem_part = -1;
-      if (sg.mode == 2) {
-        for (int pc = sg.c_first; pc < unit; ++pc)
-          if (sk.bound(pc) != sk.bound(pc + 1)) { smem_part = pc * CG + (int)rank; break; }
-        if (smem_part >= 0) {
-          if (tid == 0) {
-            mbar_arrive_expect_tx(fixbar, BM * BN * 4);
-            bulk_copy_g2s(smem, p.partials + (size_t)smem_part * (BM * BN), BM * BN * 4, fixbar);
-          }
-          mbar_wait(fixbar, fix_phase);
-          fix_phase ^= 1;
-        }
-      }
-      bf16* yrow = p.Y + (size_t)row * p.ldy;
+      // Finishing segment = this CTA's last: the MMAs are done with the pipeline smem, so the
+      // earlier parts of the tile stream into it as 32-column pieces (chunk-major, parts in CTA
+      // order) through a ring of bulk copies issued ahead of their use.
+      constexpr int RS = L::kFixSlots;
+      int np = 0;
+      if (sg.mode == 2)
+        for (int pc = sg.c_first; pc < unit; ++pc) np += sk.bound(pc) != sk.bound(pc + 1);
+      auto issue_piece = [&](int q) {  // one thread; the i-th non-empty earlier part, CTA order
+        const int slot = q % RS, chunk = q / np;
+        int i = q % np, pc = sg.c_first;
+        for (;; ++pc)
+          if (sk.bound(pc) != sk.bound(pc + 1) && i-- == 0) break;
+        mbar_arrive_expect_tx(&fixbar[slot], L::kFixPiece);
+        bulk_copy_g2s(smem + slot * L::kFixPiece,
+                      p.partials + (size_t)(pc * CG + (int)rank) * (BM * BN) + (size_t)chunk * (BM * 32),
+                      L::kFixPiece, &fixbar[slot]);
+      };
+      const int n_pieces = np * (BN / 32);
+      if (np && tid == 0)
+        for (int q = 0; q < RS && q < n_pieces; ++q) issue_piece(q);
       // partial tiles are stored in the epilogue's own thread order — float4 index
       // ((chunk * 8 + j) * 128 + tid) — so writes and reads are 512 B-coalesced per warp
       float4* part_mine = reinterpret_cast<float4*>(p.partials + (size_t)cta * (BM * BN)) + tid;
@@ -423,6 +438,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c, r);
         tmem_wait_ld();
         const int chunk = c >> 5;
+        if (dbg && tid == 0 && sg.mode == 2) dbg[24 + chunk] = gtimer();
         if (sg.mode == 1) {
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -431,9 +447,11 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
           continue;
         }
-        if (sg.mode == 2) {
-          if (smem_part >= 0) {
-            const float4* src = reinterpret_cast<const float4*>(smem) + tid + chunk * 8 * 128;
+        if (sg.mode == 2 && np) {
+          for (int i = 0; i < np; ++i) {
+            const int q = chunk * np + i;
+            mbar_wait(&fixbar[q % RS], (uint32_t)(q / RS) & 1u);
+            const float4* src = reinterpret_cast<const float4*>(smem + (q % RS) * L::kFixPiece) + tid;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float4 v = src[j * 128];
@@ -443,38 +461,37 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
               r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
             }
           }
-          for (int pc = sg.c_first; pc < unit; ++pc) {
-            const int pcta = pc * CG + (int)rank;
-            if (pcta == smem_part || sk.bound(pc) == sk.bound(pc + 1)) continue;
-            const float4* src =
-                reinterpret_cast<const float4*>(p.partials + (size_t)pcta * (BM * BN)) + tid +
-                chunk * 8 * 128;
-            float4 v8[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v8[j] = __ldcg(src + j * 128);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 v = v8[j];
-              r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + v.x);
-              r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + v.y);
-              r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + v.z);
-              r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
-            }
+          // every epilogue thread is done with this chunk's slots: refill them RS pieces ahead
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (dbg && tid == 0) dbg[16 + chunk] = gtimer();
+          if (tid == 0) {
+            fence_proxy_async_smem();
+            for (int i = 0; i < np; ++i)
+              if (chunk * np + i + RS < n_pieces) issue_piece(chunk * np + i + RS);
           }
         }
-        if (row < p.M) {
+        // bf16 row chunk -> this warp's staging buffer (64-byte TMA swizzle: 16-byte chunk j of
+        // row r at j ^ ((r >> 1) & 3)), then one TMA store of the [32 rows x 32 cols] box; the
+        // tensor map clips rows >= M and columns >= N
+        uint8_t* buf = epi_buf + (ew * 2 + (epi_i & 1)) * L::kEpiBuf;
+        if (lane == 0) bulk_wait_group_read<1>();  // the store that last used this buffer has read it
+        __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int col = n0 + c + j * 8;
-            if (col + 8 <= p.N) {
-              st_global_v4(yrow + col,
-                           pack_bf16x2(__uint_as_float(r[8 * j + 0]), __uint_as_float(r[8 * j + 1])),
-                           pack_bf16x2(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3])),
-                           pack_bf16x2(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5])),
-                           pack_bf16x2(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7])));
-            }
-          }
+        for (int j = 0; j < 4; ++j) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(r[8 * j + 0]), __uint_as_float(r[8 * j + 1]));
+          v.y = pack_bf16x2(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3]));
+          v.z = pack_bf16x2(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5]));
+          v.w = pack_bf16x2(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7]));
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = v;
         }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmY, buf, n0 + c, row - lane);
+          bulk_commit_group();
+        }
+        ++epi_i;
       }
       tc_fence_before();
       __syncwarp();
@@ -498,6 +515,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
       if (dbg && tid == 0 && seg_i < 3) dbg[3 + 4 * seg_i] = gtimer();
       ++seg_i;
     });
+    if (lane == 0) bulk_wait_group<0>();  // every TMA store of this warp has completed
     if (dbg && tid == 0) dbg[13] = gtimer();
   }
 

@@ -22,10 +22,12 @@
 
 namespace collm {
 
-constexpr int kReduceMaxGroups = 16;  // a whole layer's projections (<= 14 at BASELINE shapes)
+constexpr int kReduceMaxGroups = 16;  // ABI limit per launch: a whole layer's projections
+constexpr int kReduceMaxQ = 48;       // widest group a CTA reduces (wider ABI groups are split)
+constexpr int kReduceMaxInner = 32;   // groups after that split
 constexpr int kReducePT = 128;     // P rows per CTA tile (8 warps x 16)
 constexpr int kReduceTC = 32;      // T rows per pipeline stage
-constexpr int kReduceStages = 4;   // cp.async ring depth
+constexpr int kReduceMaxStages = 4;  // cp.async ring depth (runtime: fits the smem budget)
 constexpr int kReduceThreads = 256;
 
 enum ReduceMode : int {
@@ -58,9 +60,10 @@ struct ReduceGroup {
 struct ReduceParams {
   int T;
   int n_groups;
-  ReduceGroup groups[kReduceMaxGroups];
+  ReduceGroup groups[kReduceMaxInner];
   int n_tiles;
   int tsplit;
+  int stages;
   int mode;
   int accum_in;      // add the existing grad buffer contents
   float grad_scale;  // applied to the freshly reduced C
@@ -212,22 +215,25 @@ __device__ __forceinline__ int find_group(const ReduceParams& p, int tile) {
 template <int QT>
 struct ReduceSmem {
   static constexpr int kUP = kReducePT + 8, kVP = QT + 8;  // padded rows: conflict-free ldmatrix
-  static constexpr size_t kUBytes = (size_t)kReduceStages * kReduceTC * kUP * 2;
-  static constexpr size_t kVBytes = (size_t)kReduceStages * kReduceTC * kVP * 2;
+  static constexpr size_t kUStage = (size_t)kReduceTC * kUP * 2;
+  static constexpr size_t kVStage = (size_t)kReduceTC * kVP * 2;
   static constexpr size_t kCBytes = (size_t)kReducePT * (QT + 1) * 4;
   static constexpr size_t kTBytes = (size_t)QT * (kReducePT + 8) * 2;
-  static constexpr size_t kPipe = kUBytes + kVBytes;
   static constexpr size_t kEpi = kCBytes + kTBytes;
-  static constexpr size_t kTotal = (kPipe > kEpi ? kPipe : kEpi) + 16;
+  static size_t total(int stages) {
+    const size_t pipe = (size_t)stages * (kUStage + kVStage);
+    return (pipe > kEpi ? pipe : kEpi) + 16;
+  }
 };
 
 template <int QT>
 __global__ void __launch_bounds__(kReduceThreads, 3) lora_reduce_kernel(const ReduceParams p) {
   using S = ReduceSmem<QT>;
-  constexpr int PT = kReducePT, TC = kReduceTC, ST = kReduceStages;
+  constexpr int PT = kReducePT, TC = kReduceTC;
+  const int ST = p.stages;
   extern __shared__ __align__(16) uint8_t smem[];
   bf16 (*Us)[TC][S::kUP] = reinterpret_cast<bf16 (*)[TC][S::kUP]>(smem);
-  bf16 (*Vs)[TC][S::kVP] = reinterpret_cast<bf16 (*)[TC][S::kVP]>(smem + S::kUBytes);
+  bf16 (*Vs)[TC][S::kVP] = reinterpret_cast<bf16 (*)[TC][S::kVP]>(smem + ST * S::kUStage);
   float (*Cs)[QT + 1] = reinterpret_cast<float (*)[QT + 1]>(smem);
   bf16 (*Ct)[PT + 8] = reinterpret_cast<bf16 (*)[PT + 8]>(smem + S::kCBytes);
   __shared__ int s_last;
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(kReduceThreads, 3) lora_reduce_kernel(const Re
     cp_async_commit();
   }
   for (int i = 0; i < n_ch; ++i) {
-    cp_async_wait<ST - 2>();
+    cp_async_wait_dyn(ST - 2);
     __syncthreads();
     const int stage = i % ST;
 #pragma unroll
