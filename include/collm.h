@@ -77,11 +77,17 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
  * GEMM's LoRA slot blocks, written completely: row t's value at row slot_of_row[t]*256 + t%256 and
  * zeros in the other slots of its 256-row slot tile (tile_slot_ptr).  One CTA per (tile, group) covers
  * the whole K range; the reduction is in-CTA and fixed-order (deterministic, no workspace).
+ * Optional completion signal (signal and gen both non-NULL, device memory): signal = 2 int32,
+ * zeroed once; gen = the current step generation.  When every output is written the kernel sets
+ * signal[1] = *gen (release, gpu scope) and restores signal[0] = 0: the GEMM consuming Hslots /
+ * H16 on another stream waits for exactly that (collm_gemm_lora lora_flag), so the shrink runs
+ * concurrently with that GEMM's main loop.
  * Replaces: the inference half of perf.true_infer_latency (perf.py:62-74). */
 int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
                       const int32_t* tiles, int n_tiles, const float* scale, const int32_t* groups,
                       int n_groups, float* H32, void* H16, int ldh, void* Hslots,
-                      const int32_t* slot_of_row, const int32_t* tile_slot_ptr, void* stream);
+                      const int32_t* slot_of_row, const int32_t* tile_slot_ptr, int32_t* signal,
+                      const int32_t* gen, void* stream);
 
 /* ---- K2 / K3: base projection on tcgen05 with the LoRA expand fused into the accumulator ------
  * Y[M,N] = A[M,K] . B[N,K]^T + sum over the LoRA slots s of each 256-row slot tile of
@@ -97,6 +103,9 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
  * Persistent stream-K schedule (one CTA per SM): boundary tiles are combined through fp32
  * partials in `workspace` (zero-filled once; flags are reset by their consumers) in a fixed
  * order, so results are bitwise deterministic.  collm_gemm_workspace_bytes(bn) sizes it (0 = max).
+ * Each tile runs its K/64 main blocks first and its LoRA k-stages last.  With lora_flag / gen
+ * (device, optional) the producer waits for *lora_flag == *gen before loading the LoRA operand, so
+ * the shrink writing Hslots may run concurrently on another stream (collm_lora_shrink signal).
  * Replaces: perf.true_infer_latency / true_train_latency (perf.py:62-89). */
 size_t collm_gemm_workspace_bytes(int bn);
 int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int ldy, int M, int N,
@@ -104,7 +113,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
                     int lb_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
                     int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
                     const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
-                    void* stream);
+                    const int32_t* lora_flag, const int32_t* gen, void* stream);
 
 /* Select the GEMM pipeline depth: lean != 0 -> ~128 KB shared memory per CTA so one CTA of the
  * LoRA kernels can run on the same SM concurrently (graph branch / second stream); 0 -> deepest

@@ -224,8 +224,10 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
 int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
                       const int32_t* tiles, int n_tiles, const float* scale, const int32_t* groups,
                       int n_groups, float* H32, void* H16, int ldh, void* Hslots,
-                      const int32_t* slot_of_row, const int32_t* tile_slot_ptr, void* stream) {
+                      const int32_t* slot_of_row, const int32_t* tile_slot_ptr, int32_t* signal,
+                      const int32_t* gen, void* stream) {
   CHECK_ARG(X && A && tiles && scale && groups, "null input");
+  CHECK_ARG(!signal == !gen, "signal and gen go together");
   CHECK_ARG(n_tiles >= 0, "n_tiles < 0");
   if (n_tiles == 0) return COLLM_OK;
   CHECK_ARG(n_groups >= 1 && n_groups <= kShrinkMaxGroups, "n_groups=%d out of [1,%d]", n_groups,
@@ -276,6 +278,8 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
   cfg.blockDim = dim3(kShrinkWarps * 32);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = (cudaStream_t)stream;
+  p.signal = signal;
+  p.gen = gen;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = csize;
@@ -318,8 +322,9 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
                     int lb_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
                     int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
                     const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
-                    void* stream) {
+                    const int32_t* lora_flag, const int32_t* gen, void* stream) {
   CHECK_ARG(A && B && Y, "null operand");
+  CHECK_ARG(!lora_flag == !gen, "lora_flag and gen go together");
   CHECK_ARG(M >= 1 && N >= 1 && K >= 1, "empty GEMM M=%d N=%d K=%d", M, N, K);
   CHECK_ARG(K % 8 == 0 && N % 8 == 0, "K=%d and N=%d must be multiples of 8", K, N);
   CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0 && ldy % 8 == 0 && lda >= K && ldb >= K && ldy >= N,
@@ -419,6 +424,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
     p.slot_adapter = slot_adapter;
     p.lora_rc = lrc;
     p.lora_chunks = lora_rank / lrc;
+    p.lora_per_stage = kGemmBK / lrc;
     p.lb_rows_per_adapter = lb_rows_per_adapter;
     if (sub_n_start) {
       CHECK_ARG(sub_n_start[0] == 0 && sub_n_start[n_sub] == N, "sub_n_start must span [0, N)");
@@ -445,6 +451,8 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   const long long min_work = (long long)nm * p.num_n_tiles * ((K + kGemmBK - 1) / kGemmBK);
   const int grid = cg * (int)std::min<long long>(sms / cg, min_work);
   p.sched = sched;
+  p.lora_flag = lora ? lora_flag : nullptr;
+  p.gen = gen;
   const size_t need = collm_gemm_workspace_bytes(bn);
   CHECK_ARG(workspace && ws_bytes >= need, "gemm workspace too small: %zu < %zu", ws_bytes, need);
   p.flags = (int32_t*)workspace;

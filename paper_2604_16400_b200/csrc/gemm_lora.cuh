@@ -32,7 +32,9 @@
 //
 // Hybrid data-parallel + stream-K schedule (computed on the device, identically by every role).
 // Tiles are rastered m-fastest, so the CTAs of one data-parallel wave share each W tile through
-// L2.  A tile's work is its k-stages (LoRA slot chunks first, then the K/64 main blocks).  All
+// L2.  A tile's work is its k-stages: the K/64 main blocks, then the LoRA slot chunks — so the
+// shrink producing the LoRA operand can run concurrently with this GEMM's main loop (another
+// stream); the producer waits on its readiness flag only before the first LoRA stage.  All
 // full waves but the last are data-parallel (CTA c takes tiles c, c+G, ...); the remaining tiles
 // (between one and two waves' worth, or all of them when there is less than one wave) are cut into
 // gridDim.x equal contiguous k-stage ranges ("stream-K"), which removes the wave-quantization
@@ -61,11 +63,16 @@ struct GemmLoraParams {
   const int32_t* slot_adapter;   // [n_slots] adapter id of each slot
   int lora_rc;                   // columns per LoRA chunk: 16 / 32 / 64 (one TMA box each)
   int lora_chunks;               // chunks per slot (= lora width / rc)
+  int lora_per_stage;            // (slot, chunk) items packed into one LoRA k-stage (= 64 / rc)
   int lb_rows_per_adapter;       // LB row coordinate = adapter * this + n0
   int n_sub;                     // sub-projections along N (fused q|k|v, gate|up); >= 1
   int sub_n_start[kMaxSub + 1];  // N boundaries of the sub-projections (multiples of BN)
   int sub_h_col[kMaxSub];        // first H column used by each sub-projection
   int num_m_tiles, num_n_tiles;  // in units of (128 * CG) rows x BN columns
+  // readiness of the LoRA operand written by a shrink running concurrently on another stream:
+  // before its first LoRA k-stage the producer waits for *lora_flag == *gen (null: no wait)
+  const int32_t* lora_flag;
+  const int32_t* gen;
   int sched;  // 0 = data-parallel (round-robin tiles), 1 = hybrid data-parallel + stream-K,
               // 2 = debug: stream-K split without fix-up (timing experiments only)
   // ---- stream-K
@@ -78,6 +85,25 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// Wait until the concurrently running shrink has published the LoRA operand of this launch
+// (*lora_flag == *gen, release/acquire at gpu scope), then order the TMA (async proxy) reads of it
+// after that acquire.  A shrink that never runs traps after the timeout instead of hanging.
+__device__ __forceinline__ void wait_lora_flag(const GemmLoraParams& p) {
+  const int32_t want = *p.gen;
+  int32_t v;
+  const unsigned long long t0 = clock64();
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.lora_flag) : "memory");
+    if (v == want) break;
+    if (clock64() - t0 > COLLM_MBAR_TIMEOUT_CYCLES) {
+      printf("collm: LoRA operand flag timeout (block %d: %d != %d)\n", blockIdx.x, v, want);
+      __trap();
+    }
+    __nanosleep(64);
+  }
+  asm volatile("fence.proxy.async;" ::: "memory");
 }
 
 template <int BN, int STAGES, int CG>
@@ -111,7 +137,6 @@ __device__ __forceinline__ int sub_of_n0(const GemmLoraParams& p, int n0) {
 struct Segment {
   int m_blk, n_blk;
   int k0, k1;     // stage range [k0, k1) within the tile
-  int n_lora;     // LoRA stages at the head of this tile's stage list
   int mode;       // 0 = whole tile, 1 = partial (write partials[cta]), 2 = finish (add parts)
   int c_first;    // mode 2: the CTAs [c_first, this CTA) hold the earlier parts
 };
@@ -167,7 +192,6 @@ struct StreamK {
     const bool first = s0 == t0, last = x_end == t1;
     sg.mode = (first && last) ? 0 : (last ? 2 : 1);
     sg.c_first = (sg.mode == 2) ? cta_of(t0) : c;
-    sg.n_lora = 0;
     return sg;
   }
   // Visit this CTA's work: its data-parallel tiles, then its stream-K segments in reverse.
@@ -181,8 +205,7 @@ struct StreamK {
       sg.k1 = stages_of_m(sg.m_blk);
       sg.mode = 0;
       sg.c_first = c;
-      sg.n_lora = 0;
-      f(sg);
+        f(sg);
     }
     const long long lo = bound(c);
     for (long long x_end = bound(c + 1); x_end > lo;) {
@@ -220,10 +243,15 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
   const bool leader = rank == 0;
 
   // LoRA stages of a (128*CG)-row unit: the slot list of the 256-row slot tile containing it
-  auto lora_stages = [&](int m) {
+  // (slot, chunk) items of a unit; 64/rc of them share one k-stage (one barrier round trip):
+  // the stage's A half holds their Hslots boxes side by side, its B half their adapters' B boxes
+  auto lora_items = [&](int m) {
     if (!has_lora) return 0;
     const int st = (m * (int)UNIT_M) / kSlotTileM;
     return (p.tile_slot_ptr[st + 1] - p.tile_slot_ptr[st]) * p.lora_chunks;
+  };
+  auto lora_stages = [&](int m) {
+    return has_lora ? (lora_items(m) + p.lora_per_stage - 1) / p.lora_per_stage : 0;
   };
 
   // per-unit stage counts -> prefix (every role needs it for the schedule)
@@ -268,11 +296,11 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t rc = p.lora_rc;
+    bool lora_ready = p.lora_flag == nullptr;
     sk.for_each(unit, [&](const Segment& sg) {
       const int m0 = sg.m_blk * UNIT_M + rank * BM;  // this CTA's rows
       const int n0 = sg.n_blk * BN;
       const int nb0 = n0 + rank * (int)L::kBRows;   // this CTA's share of the N tile
-      const int n_lora = lora_stages(sg.m_blk);
       const int st_tile = m0 / kSlotTileM;
       const int hrow0 = m0 % kSlotTileM;
       const int hcol = has_lora ? p.sub_h_col[sub_of_n0(p, n0)] : 0;
@@ -283,29 +311,41 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
           continue;
         }
         uint8_t* sa = smem + stage * L::kStageBytes;
-        uint32_t bytes;
-        if (i < n_lora) bytes = (BM + L::kBRows) * rc * 2;
-        else bytes = L::kStageBytes;
+        const bool lora_stage = i >= nk;  // the tile's LoRA k-stages follow its K/64 main blocks
+        if (lora_stage && !lora_ready) {
+          wait_lora_flag(p);
+          lora_ready = true;
+        }
+        int it0 = 0, n_it = 0;  // this LoRA stage's (slot, chunk) items
+        if (lora_stage) {
+          it0 = (i - nk) * p.lora_per_stage;
+          n_it = min(p.lora_per_stage, lora_items(sg.m_blk) - it0);
+        }
+        const uint32_t bytes = lora_stage ? n_it * (BM + L::kBRows) * rc * 2 : L::kStageBytes;
         if (p.sched == 3) {  // debug: no operand loads (measures the MMA issue rate alone)
           if (leader) mbar_arrive(&full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
         }
         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * CG);
-        if (i < n_lora) {
-          const int s = p.tile_slot_ptr[st_tile] + i / p.lora_chunks;
-          const int c = i % p.lora_chunks;
-          const int lb_row = p.slot_adapter[s] * p.lb_rows_per_adapter + nb0;
-          if constexpr (CG == 2) {
-            const uint32_t fb = mapa_shared(&full[stage], 0);
-            tma_load_2d_pair(sa, &tmH, fb, hcol + c * rc, s * kSlotTileM + hrow0);
-            tma_load_2d_pair(sa + L::kABytes, &tmLB, fb, c * rc, lb_row);
-          } else {
-            tma_load_2d(sa, &tmH, &full[stage], hcol + c * rc, s * kSlotTileM + hrow0);
-            tma_load_2d(sa + L::kABytes, &tmLB, &full[stage], c * rc, lb_row);
+        if (lora_stage) {
+          for (int j = 0; j < n_it; ++j) {
+            const int s = p.tile_slot_ptr[st_tile] + (it0 + j) / p.lora_chunks;
+            const int c = (it0 + j) % p.lora_chunks;
+            const int lb_row = p.slot_adapter[s] * p.lb_rows_per_adapter + nb0;
+            uint8_t* da = sa + j * (BM * rc * 2);
+            uint8_t* db = sa + L::kABytes + j * (L::kBRows * rc * 2);
+            if constexpr (CG == 2) {
+              const uint32_t fb = mapa_shared(&full[stage], 0);
+              tma_load_2d_pair(da, &tmH, fb, hcol + c * rc, s * kSlotTileM + hrow0);
+              tma_load_2d_pair(db, &tmLB, fb, c * rc, lb_row);
+            } else {
+              tma_load_2d(da, &tmH, &full[stage], hcol + c * rc, s * kSlotTileM + hrow0);
+              tma_load_2d(db, &tmLB, &full[stage], c * rc, lb_row);
+            }
           }
         } else {
-          const int kb = i - n_lora;
+          const int kb = i;
           if constexpr (CG == 2) {
             const uint32_t fb = mapa_shared(&full[stage], 0);
             tma_load_2d_pair(sa, &tmA, fb, kb * BK, m0);
@@ -335,7 +375,6 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
       if constexpr (CG == 2) umma_commit_pair(bar); else umma_commit(bar);
     };
     sk.for_each(unit, [&](const Segment& sg) {
-      const int n_lora = lora_stages(sg.m_blk);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -344,11 +383,15 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         const uint32_t sa = smem_base + stage * L::kStageBytes;
-        if (i < n_lora) {
+        if (i >= nk) {  // LoRA expand k-stage: (Hslots chunk x adapter B chunk) per item
+          const int it0 = (i - nk) * p.lora_per_stage;
+          const int n_it = min(p.lora_per_stage, lora_items(sg.m_blk) - it0);
           if (elect_one()) {
-            for (uint32_t k = 0; k < lsteps; ++k)
-              mma(d_tmem, umma_desc_kmajor(sa + k * 32, lrow),
-                  umma_desc_kmajor(sa + L::kABytes + k * 32, lrow), accumulate | k);
+            for (int j = 0; j < n_it; ++j)
+              for (uint32_t k = 0; k < lsteps; ++k)
+                mma(d_tmem, umma_desc_kmajor(sa + j * (BM * lrow) + k * 32, lrow),
+                    umma_desc_kmajor(sa + L::kABytes + j * (L::kBRows * lrow) + k * 32, lrow),
+                    (accumulate | j | k) ? 1u : 0u);
             commit(&empty[stage]);
           }
         } else {

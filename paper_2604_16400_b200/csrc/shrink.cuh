@@ -56,7 +56,27 @@ struct ShrinkParams {
   const int32_t* slot_of_row;
   const int32_t* tile_slot_ptr;  // slot range of each 256-row slot tile (for the zero fill)
   int csize;                     // CTAs per cluster splitting the K range (1, 2, 4, 8)
+  // completion signal for a consumer running concurrently on another stream (optional):
+  // signal[0] = arrival counter (0 on entry, restored), signal[1] <- *gen once all is written
+  int32_t* signal;
+  const int32_t* gen;
 };
+
+// Every CTA arrives once its outputs are written; the last one publishes *gen in signal[1]
+// (release, gpu scope) for the GEMM waiting on it (wait_lora_flag in gemm_lora.cuh).
+__device__ __forceinline__ void shrink_signal_done(const ShrinkParams& p) {
+  if (!p.signal) return;
+  __syncthreads();  // this CTA's stores happen-before thread 0's cumulative fence
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int total = (int)(gridDim.x * gridDim.y);
+    if (atomicAdd(p.signal, 1) == total - 1) {
+      __threadfence();
+      p.signal[0] = 0;
+      asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p.signal + 1), "r"(*p.gen) : "memory");
+    }
+  }
+}
 
 // Per-row output bookkeeping staged in shared memory once per CTA (no dependent global loads in
 // the store loop): own slot and the slot range of the row's 128-row tile.
@@ -200,6 +220,7 @@ __global__ void __launch_bounds__(kShrinkWarps * 32, 2)
       }
     }
     cl.sync();  // peers keep their shared memory alive until rank 0 has read it
+    shrink_signal_done(p);
     return;
   }
   __syncthreads();
@@ -209,6 +230,7 @@ __global__ void __launch_bounds__(kShrinkWarps * 32, 2)
     if (i < n_rows)
       shrink_store(p, rs, i, row_start + i, grp.rank_off + j, red[0][i][j] * sc, has_adapter);
   }
+  shrink_signal_done(p);
 }
 
 }  // namespace collm

@@ -221,8 +221,11 @@ class LoraProjection:
         cache = self.forward_lora(X, plan, n_train)
         return self.forward_gemm(cache, plan, Y), cache
 
-    def forward_lora(self, X: torch.Tensor, plan: DevicePlan, n_train: int = 0) -> ForwardCache:
-        """K1 (rank space): H16 and the GEMM's LoRA slot blocks for every row of the pass."""
+    def forward_lora(self, X: torch.Tensor, plan: DevicePlan, n_train: int = 0,
+                     signal: tuple | None = None) -> ForwardCache:
+        """K1 (rank space): H16 and the GEMM's LoRA slot blocks for every row of the pass.
+        ``signal`` = (int32[2] device signal, device step generation): publish completion so this
+        projection's GEMM can run concurrently on another stream (``forward_gemm(wait=...)``)."""
         spec = self.spec
         T = plan.n_rows
         if X.shape[0] < T or X.shape[1] != spec.in_features:
@@ -234,12 +237,15 @@ class LoraProjection:
             groups = [(g, min(64, R - g), 0, K) for g in range(0, R, 64)]
             ops.lora_shrink(X, self.A, plan.shrink_tiles, plan.n_shrink_tiles, self.scale, groups,
                             R, H16=H16, Hslots=Hs, slot_of_row=plan.slot_of_row,
-                            tile_slot_ptr=plan.tile_slot_ptr)
+                            tile_slot_ptr=plan.tile_slot_ptr,
+                            signal=signal[0] if signal else None, gen=signal[1] if signal else None)
         return ForwardCache(X=X, H16=H16, n_train=n_train)
 
     def forward_gemm(self, cache: ForwardCache, plan: DevicePlan,
-                     Y: torch.Tensor | None = None) -> torch.Tensor:
-        """K2: the base projection with the multi-adapter expand fused into the accumulator."""
+                     Y: torch.Tensor | None = None, wait: tuple | None = None) -> torch.Tensor:
+        """K2: the base projection with the multi-adapter expand fused into the accumulator.
+        ``wait`` = the shrink's (signal, generation): this GEMM may run before that shrink has
+        finished (another stream); it loads the LoRA operand only after the signal."""
         spec = self.spec
         T = plan.n_rows
         X = cache.X
@@ -254,7 +260,8 @@ class LoraProjection:
                           lb_rows=self.n_adapters * spec.out_features,
                           tile_slot_ptr=plan.tile_slot_ptr, slot_adapter=plan.slot_adapter,
                           lora_rank=rp, lb_rows_per_adapter=spec.out_features, sub_n_start=bnd,
-                          sub_h_col=[s * rp for s in range(len(spec.subs))])
+                          sub_h_col=[s * rp for s in range(len(spec.subs))],
+                          lora_flag=wait[0][1:] if wait else None, gen=wait[1] if wait else None)
         else:
             ops.gemm_lora(X, self.W, Y, M=T)
         return Y
@@ -309,7 +316,8 @@ class LoraProjection:
             raise ConfigurationError(f"{self.spec.name}: no trainable adapter (make_trainable)")
         return st
 
-    def backward_dh(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan) -> torch.Tensor:
+    def backward_dh(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan,
+                    signal: tuple | None = None) -> torch.Tensor:
         """K1: dH = s * dY . B_t, one rank group per sub-projection (its own N range)."""
         st = self._require_train()
         spec = self.spec
@@ -320,11 +328,12 @@ class LoraProjection:
         groups = [(s * rp + g, min(64, rp - g), bnd[s], bnd[s + 1])
                   for s in range(len(spec.subs)) for g in range(0, rp, 64)]
         ops.lora_shrink(dY, st.BT16, train_plan.shrink_tiles, train_plan.n_shrink_tiles,
-                        self.scale, groups, R, a_stride=0, H16=dH16)
+                        self.scale, groups, R, a_stride=0, H16=dH16,
+                        signal=signal[0] if signal else None, gen=signal[1] if signal else None)
         return dH16
 
     def backward_dx(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan,
-                    dX: torch.Tensor | None = None) -> torch.Tensor:
+                    dX: torch.Tensor | None = None, wait: tuple | None = None) -> torch.Tensor:
         """K3: dX = dY . W + dH . A_t (reads A_t^T: run before this projection's optimizer step)."""
         st = self._require_train()
         spec = self.spec
@@ -335,7 +344,8 @@ class LoraProjection:
         dH16 = self._dh_buffer(Ttr)
         ops.gemm_lora(dY, self.WT, dX, M=Ttr, Hslots=dH16, h_rows=Ttr, LB=st.AT16, lb_rows=K,
                       tile_slot_ptr=train_plan.tile_slot_ptr, slot_adapter=train_plan.slot_adapter,
-                      lora_rank=R, lb_rows_per_adapter=0)
+                      lora_rank=R, lb_rows_per_adapter=0,
+                      lora_flag=wait[0][1:] if wait else None, gen=wait[1] if wait else None)
         return dX
 
     def grad_groups(self, dY: torch.Tensor, cache: ForwardCache, *,

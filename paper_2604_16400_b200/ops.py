@@ -112,8 +112,10 @@ def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: 
                 a_stride: int | None = None, H32: torch.Tensor | None = None,
                 H16: torch.Tensor | None = None, Hslots: torch.Tensor | None = None,
                 slot_of_row: torch.Tensor | None = None,
-                tile_slot_ptr: torch.Tensor | None = None) -> None:
-    """K1: H[t, ranks of g] = scale[a] * X[t, K-range of g] . A_a[ranks of g]^T (see collm.h)."""
+                tile_slot_ptr: torch.Tensor | None = None, signal: torch.Tensor | None = None,
+                gen: torch.Tensor | None = None) -> None:
+    """K1: H[t, ranks of g] = scale[a] * X[t, K-range of g] . A_a[ranks of g]^T (see collm.h).
+    ``signal``/``gen``: publish completion for a GEMM consuming the output on another stream."""
     _need(X, torch.bfloat16, "X")
     _need(A, torch.bfloat16, "A")
     if n_tiles == 0 or not _launch("lora"):
@@ -124,7 +126,8 @@ def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: 
     flat = [v for g in groups for v in g]
     _lib.call("collm_lora_shrink", X.data_ptr(), X.stride(0), A.data_ptr(), int(a_stride), lda,
               tiles.data_ptr(), n_tiles, scale.data_ptr(), _lib.int_array(flat), len(groups),
-              _p(H32), _p(H16), ldh, _p(Hslots), _p(slot_of_row), _p(tile_slot_ptr), _stream())
+              _p(H32), _p(H16), ldh, _p(Hslots), _p(slot_of_row), _p(tile_slot_ptr), _p(signal),
+              _p(gen), _stream())
 
 
 def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | None = None,
@@ -132,8 +135,11 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
               lb_rows: int = 0, tile_slot_ptr: torch.Tensor | None = None,
               slot_adapter: torch.Tensor | None = None, lora_rank: int = 0,
               lb_rows_per_adapter: int = 0, sub_n_start: list[int] | None = None,
-              sub_h_col: list[int] | None = None, bn: int = 0) -> None:
-    """K2/K3: Y[M,N] = A[M,K] . B[N,K]^T (+ fused multi-adapter LoRA expand), bf16 -> bf16."""
+              sub_h_col: list[int] | None = None, bn: int = 0,
+              lora_flag: torch.Tensor | None = None, gen: torch.Tensor | None = None) -> None:
+    """K2/K3: Y[M,N] = A[M,K] . B[N,K]^T (+ fused multi-adapter LoRA expand), bf16 -> bf16.
+    ``lora_flag``/``gen``: wait for a concurrently running shrink's signal before the LoRA
+    stages (see collm.h)."""
     for t, n in ((A, "A"), (B, "B"), (Y, "Y")):
         _need(t, torch.bfloat16, n)
     M = A.shape[0] if M is None else M
@@ -144,6 +150,8 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
     if not _launch("gemm"):
         return
     lora = tile_slot_ptr is not None
+    if not enabled("lora"):  # a GEMM-only timing graph skips the shrinks: nothing to wait for
+        lora_flag = gen = None
     n_sub = len(sub_n_start) - 1 if (lora and sub_n_start) else 1
     ws = _gemm_ws.get(_lib.load().collm_gemm_workspace_bytes(0), A.device)
     _lib.call(
@@ -154,7 +162,8 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
         _p(tile_slot_ptr), _p(slot_adapter), lora_rank, lb_rows_per_adapter, n_sub,
         _lib.int_array(sub_n_start) if (lora and sub_n_start) else None,
         _lib.int_array(sub_h_col) if (lora and sub_h_col) else None, bn, _p(ws),
-        0 if ws is None else ws.numel(), _stream())
+        0 if ws is None else ws.numel(), _p(lora_flag) if lora else None,
+        _p(gen) if lora else None, _stream())
 
 
 def reduce_tsplit(T: int, n_tiles: int, device: torch.device) -> int:

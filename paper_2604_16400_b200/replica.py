@@ -66,6 +66,10 @@ class ReplicaStack:
         self._graph: torch.cuda.CUDAGraph | None = None
         self._side: torch.cuda.Stream | None = None
         self.overlap = False
+        self._gen: torch.Tensor | None = None
+        self._gen_host: torch.Tensor | None = None
+        self._gen_count = 0
+        self._sig: torch.Tensor | None = None
 
     # ------------------------------------------------------------------ weights
     @torch.no_grad()
@@ -202,15 +206,17 @@ class ReplicaStack:
     def run_step(self, plan: StepPlan | None = None, optimizer_step: bool = True,
                  advance: bool = True, overlap: bool | None = None) -> torch.Tensor:
         """Enqueue one full co-batched step on the current stream; returns the final hidden state
-        buffer (device).  With ``advance`` the optimizer step counter is bumped first (keep it
-        False inside CUDA-graph capture; call ``opt.advance()`` before each replay instead).
+        buffer (device).  With ``advance`` the optimizer step counter and the step generation are
+        bumped first (keep it False inside CUDA-graph capture; ``replay()`` bumps them).
 
-        ``overlap``: the HBM/latency-bound rank-space kernels (K1 shrink, K5 reductions) run on a
-        side stream one projection ahead of the tensor-bound GEMMs on the main stream, ordered
-        only by their true dependencies (shrink -> GEMM of the same projection; a layer's input
-        produced by the previous layer's down GEMM; the optimizer step that rewrites A_t^T after
-        the dX GEMM that reads it).  The GEMMs then use their lean pipelines so one LoRA CTA fits
-        next to each GEMM CTA."""
+        Projections run in data-flow order: a projection's shrink (K1) and GEMM (K2/K3) start
+        only after the previous projection's GEMM (its input exists only then, as in the real
+        model).  ``overlap``: the shrink runs on a side stream CONCURRENTLY with its own GEMM's
+        base main loop (which needs only X); the GEMM's LoRA k-stages come last and wait for the
+        shrink's completion signal (device flag == step generation).  The weight-gradient
+        reductions + fused AdamW (K5) of a layer run on the side stream after the layer's last
+        dX GEMM, queued behind the next projection's dH shrink.  The GEMMs then use their lean
+        pipelines so one rank-space CTA fits next to each GEMM CTA."""
         plan = plan or self._plan
         a = self._acts
         if a is None:
@@ -219,102 +225,114 @@ class ReplicaStack:
             overlap = self.overlap
         L = self.cfg.model.layers
         Ttr = plan.n_train
-        if advance and Ttr and optimizer_step:
-            self.opt.advance()
+        if advance:
+            self.advance_step(optimizer_step and Ttr > 0)
         main = torch.cuda.current_stream(self.device)
         side = self._side_stream() if overlap else main
         _lib.load().collm_set_gemm_lean(1 if overlap else 0)
-        ev = lambda: torch.cuda.Event()  # noqa: E731
+        n_sig = 0
 
-        def on(stream, fn, wait=None):
-            if wait is not None and overlap:
-                stream.wait_event(wait)
-            with torch.cuda.stream(stream):
-                out = fn()
-            e = ev()
-            e.record(stream)
-            return out, e
+        def signal():
+            nonlocal n_sig
+            if not overlap:
+                return None
+            sig = (self._signals(n_sig + 1)[n_sig], self._gen)
+            n_sig += 1
+            return sig
+
+        def after(stream_from) -> torch.cuda.Event:
+            e = torch.cuda.Event()
+            e.record(stream_from)
+            return e
+
+        def on_side(fn, wait_ev):
+            if overlap:
+                side.wait_event(wait_ev)
+            with torch.cuda.stream(side):
+                fn()
 
         plan.device.expand()
-        e_plan = ev()
-        e_plan.record(main)
+        prev = after(main)
         first = self.specs[0].name
-        # ---------------- forward: shrink(i+1) on the side stream while GEMM(i) runs
-        fwd = []  # (layer, proj, X, Y)
+        # ---------------- forward of every row: K1 on the side stream || K2 main loop
+        caches: list[dict] = [dict() for _ in range(L)]
         for l, layer in enumerate(self.layers):
             syn = l if a["distinct_synthetic"] else 0
             for proj in layer:
                 name = proj.spec.name
                 X = a["X"][l] if name in ENTRY else (a["Xo"][syn] if name == "o" else a["Xd"][syn])
                 Y = a["X"][l + 1] if name == "down" else a["Y"][name]
-                fwd.append((l, proj, X, Y))
-        caches: list[dict] = [dict() for _ in range(L)]
-        e_gemm = {}
-        pending = None  # (cache, event) of the shrink of the next projection
-
-        def shrink(i, wait):
-            l, proj, X, _ = fwd[i]
-            return on(side, lambda: proj.forward_lora(X, plan.device, n_train=Ttr), wait)
-
-        pending = shrink(0, e_plan)
-        for i, (l, proj, X, Y) in enumerate(fwd):
-            cache, e_sh = pending
-            caches[l][proj.spec.name] = cache
-            _, e_g = on(main, lambda: proj.forward_gemm(cache, plan.device, Y), e_sh)
-            e_gemm[i] = e_g
-            if i + 1 < len(fwd):
-                nl, nproj, _, _ = fwd[i + 1]
-                # the next layer's entry projections read X_{l+1} = this (down) GEMM's output
-                needs = e_g if (nl != l and nproj.spec.name in ENTRY) else None
-                pending = shrink(i + 1, needs)
+                sig = signal()
+                box = {}
+                on_side(lambda: box.setdefault("c", proj.forward_lora(X, plan.device, n_train=Ttr,
+                                                                    signal=sig)), prev)
+                caches[l][name] = box["c"]
+                proj.forward_gemm(box["c"], plan.device, Y, wait=sig)
+                prev = after(main)
         if Ttr:
             opt = self.opt if optimizer_step else None
-            bwd = []  # (layer, proj, dY, dX)
+            mode = _lib.MODE_ADAMW if opt is not None else _lib.MODE_STORE_GRAD
+            pending = None  # (groups, event) of the last finished layer's K5
+
+            def flush_k5():
+                nonlocal pending
+                if pending is not None:
+                    grp, ev = pending
+                    # K5 of a whole layer in one launch, after the layer's last dX GEMM: the
+                    # fused optimizer rewrites A_t^T, which those GEMMs read
+                    on_side(lambda: ops.lora_reduce(Ttr, grp, mode,
+                                                    adamw=opt.args if opt is not None else None,
+                                                    device=self.device), ev)
+                    pending = None
+
             for l in range(L - 1, -1, -1):
                 syn = l if a["distinct_synthetic"] else 0
+                groups: list = []
                 for proj in reversed(self.layers[l]):
                     name = proj.spec.name
                     dY = (a["dY_top"] if l == L - 1 else a["dX_first"][l + 1]) if name == "down" \
                         else a["dY"][syn][name]
                     dX = a["dX_first"][l] if name == first else a["dX"][name]
-                    bwd.append((l, proj, dY, dX))
-            e_last_gemm = e_gemm[len(fwd) - 1]
-
-            def dh(i, wait):
-                l, proj, dY, _ = bwd[i]
-                return on(side, lambda: proj.backward_dh(dY, caches[l][proj.spec.name],
-                                                         plan.train_device), wait)
-
-            mode = _lib.MODE_ADAMW if opt is not None else _lib.MODE_STORE_GRAD
-            _, e_dh = dh(0, e_last_gemm)
-            layer_groups: list = []
-            for i, (l, proj, dY, dX) in enumerate(bwd):
-                cache = caches[l][proj.spec.name]
-                _, e_g = on(main, lambda: proj.backward_dx(dY, cache, plan.train_device, dX), e_dh)
-                nl = bwd[i + 1][0] if i + 1 < len(bwd) else -1
-                if i + 1 < len(bwd):
-                    # down of the next (lower) layer consumes dX_first of this layer's first proj
-                    needs = e_g if bwd[i + 1][1].spec.name == "down" else None
-                    _, e_dh = dh(i + 1, needs)
-                layer_groups += proj.grad_groups(dY, cache, optimizer=opt)
-                if nl != l:
-                    # K5 of the whole layer in one launch (the weight gradients feed nothing
-                    # later in the step), after the layer's last dX GEMM: the fused optimizer
-                    # rewrites A_t^T, which those GEMMs read
-                    grp = layer_groups
-                    on(side, lambda: ops.lora_reduce(
-                        Ttr, grp, mode, adamw=opt.args if opt is not None else None,
-                        device=self.device), e_g)
-                    layer_groups = []
+                    cache = caches[l][name]
+                    sig = signal()
+                    on_side(lambda: proj.backward_dh(dY, cache, plan.train_device, signal=sig), prev)
+                    flush_k5()  # the previous layer's K5 queues behind this dH shrink
+                    proj.backward_dx(dY, cache, plan.train_device, dX, wait=sig)
+                    prev = after(main)
+                    groups += proj.grad_groups(dY, cache, optimizer=opt)
+                pending = (groups, prev)
+            flush_k5()
         if overlap:
-            e_end = ev()
-            e_end.record(side)
-            main.wait_event(e_end)
+            main.wait_stream(side)
         return a["X"][L]
+
+    # ------------------------------------------------------------------ step generation
+    def advance_step(self, optimizer_step: bool = True) -> None:
+        """Per-step host->device bookkeeping (outside any captured graph, on the current stream):
+        the optimizer's step block and the step generation the shrink->GEMM signals carry."""
+        if optimizer_step:
+            self.opt.advance()
+        if self._gen is None:
+            self._gen = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self._gen_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self._gen_count += 1
+        self._gen_host.fill_(self._gen_count)
+        self._gen.copy_(self._gen_host, non_blocking=True)
+
+    def _signals(self, n: int) -> torch.Tensor:
+        """int32 [n, 2] shrink->GEMM completion signals (zeroed once; the kernels restore the
+        counters and the flags carry the step generation).  Sized before graph capture."""
+        if self._sig is None or self._sig.shape[0] < n:
+            if torch.cuda.is_current_stream_capturing():
+                raise ConfigurationError("run one eager step before capturing (signal buffers)")
+            n_max = max(n, 2 * sum(1 for _ in self.projections()))
+            self._sig = torch.zeros(n_max, 2, dtype=torch.int32, device=self.device)
+        return self._sig
 
     def _side_stream(self) -> torch.cuda.Stream:
         if self._side is None:
-            self._side = torch.cuda.Stream(self.device)
+            # high priority: the rank-space CTAs a spinning GEMM waits for are scheduled first
+            self._side = torch.cuda.Stream(self.device, priority=-1)
         return self._side
 
     # ------------------------------------------------------------------ graphs
@@ -335,8 +353,7 @@ class ReplicaStack:
     def replay(self, optimizer_step: bool = True) -> torch.Tensor:
         if self._graph is None:
             raise ConfigurationError("capture() first")
-        if optimizer_step and self._plan.n_train:
-            self.opt.advance()
+        self.advance_step(optimizer_step and self._plan.n_train > 0)
         self._graph.replay()
         return self._acts["X"][self.cfg.model.layers]
 
