@@ -75,12 +75,7 @@ class MeasuredLatencyBackend:
         torch.cuda.synchronize()
         e0.record()
         for _ in range(self.reps):
-            if train:
-                st.run_step(plan, optimizer_step=opt)
-            else:
-                from . import ops
-                with ops.only("plan", "lora", "gemm"):
-                    st.run_step(plan, optimizer_step=False)
+            st.run_step(plan, optimizer_step=opt, backward=train)
         e1.record()
         torch.cuda.synchronize()
         sec = e0.elapsed_time(e1) / self.reps / 1e3

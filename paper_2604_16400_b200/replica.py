@@ -204,10 +204,12 @@ class ReplicaStack:
 
     # ------------------------------------------------------------------ the step
     def run_step(self, plan: StepPlan | None = None, optimizer_step: bool = True,
-                 advance: bool = True, overlap: bool | None = None) -> torch.Tensor:
+                 advance: bool = True, overlap: bool | None = None,
+                 backward: bool = True) -> torch.Tensor:
         """Enqueue one full co-batched step on the current stream; returns the final hidden state
         buffer (device).  With ``advance`` the optimizer step counter and the step generation are
         bumped first (keep it False inside CUDA-graph capture; ``replay()`` bumps them).
+        ``backward=False``: forward of every row only (an inference-only pass).
 
         Projections run in data-flow order: a projection's shrink (K1) and GEMM (K2/K3) start
         only after the previous projection's GEMM (its input exists only then, as in the real
@@ -226,7 +228,7 @@ class ReplicaStack:
         L = self.cfg.model.layers
         Ttr = plan.n_train
         if advance:
-            self.advance_step(optimizer_step and Ttr > 0)
+            self.advance_step(optimizer_step and backward and Ttr > 0)
         main = torch.cuda.current_stream(self.device)
         side = self._side_stream() if overlap else main
         _lib.load().collm_set_gemm_lean(1 if overlap else 0)
@@ -269,7 +271,7 @@ class ReplicaStack:
                 caches[l][name] = box["c"]
                 proj.forward_gemm(box["c"], plan.device, Y, wait=sig)
                 prev = after(main)
-        if Ttr:
+        if Ttr and backward:
             opt = self.opt if optimizer_step else None
             mode = _lib.MODE_ADAMW if opt is not None else _lib.MODE_STORE_GRAD
             pending = None  # (groups, event) of the last finished layer's K5

@@ -73,3 +73,19 @@ def test_stack_forward_matches_oracle():
     Y = st._acts["Y"][proj.spec.name][: plan.n_rows].float().cpu().numpy()
     err = np.abs(Y - Y_ref).max()
     assert err <= 1e-2 * np.abs(Y_ref).max() + 1e-3
+
+
+def test_measured_latency_backend():
+    """The engine seam's measured backend (backend.MeasuredLatencyBackend) answers the reference's
+    (B, b) latency interface with real CUDA-event times: positive, cached, and a training step
+    (forward + backward + AdamW) costs more than the forward-only pass of the same rows."""
+    from types import SimpleNamespace
+
+    from paper_2604_16400_b200.backend import MeasuredLatencyBackend
+    from paper_2604_16400_b200.configs import CONFIGS
+    be = MeasuredLatencyBackend(CONFIGS["tiny"], reps=2)
+    cfg = SimpleNamespace(train_batch=2, infer_batch=8)
+    t_inf = be.true_infer_latency(None, cfg)
+    t_tr = be.true_train_latency(None, cfg)
+    assert 0 < t_inf < t_tr < 1.0
+    assert be.true_infer_latency(None, cfg) == t_inf  # cached per (B, b)
