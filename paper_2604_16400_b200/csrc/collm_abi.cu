@@ -306,6 +306,15 @@ static bool g_reduce_lean = false;
 
 // debug-only: device pointer of the last GEMM's timeline (COLLM_GEMM_DEBUG set)
 unsigned long long* collm_debug_timeline = nullptr;
+// debug-only: total ns / count of LoRA-operand flag waits since the last call (COLLM_GEMM_DEBUG)
+int collm_gemm_wait_stats(unsigned long long* ns, unsigned long long* waits) {
+  CUDA_TRY(cudaMemcpyFromSymbol(ns, g_lora_wait_ns, sizeof(*ns)));
+  CUDA_TRY(cudaMemcpyFromSymbol(waits, g_lora_waits, sizeof(*waits)));
+  const unsigned long long z = 0;
+  CUDA_TRY(cudaMemcpyToSymbol(g_lora_wait_ns, &z, sizeof(z)));
+  CUDA_TRY(cudaMemcpyToSymbol(g_lora_waits, &z, sizeof(z)));
+  return COLLM_OK;
+}
 int collm_gemm_debug_copy(void* host_dst, size_t bytes) {
   if (!collm_debug_timeline) return fail(COLLM_EINVAL, "no GEMM debug timeline (COLLM_GEMM_DEBUG)");
   CUDA_TRY(cudaMemcpy(host_dst, collm_debug_timeline, bytes, cudaMemcpyDeviceToHost));

@@ -81,19 +81,25 @@ struct GemmLoraParams {
   unsigned long long* dbg;  // optional timeline [gridDim.x][16] (globaltimer ns), debug only
 };
 
+
+
+// Wait until the concurrently running shrink has published the LoRA operand of this launch
+// (*lora_flag == *gen, release/acquire at gpu scope), then order the TMA (async proxy) reads of it
+// after that acquire.  A shrink that never runs traps after the timeout instead of hanging.
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
 
-// Wait until the concurrently running shrink has published the LoRA operand of this launch
-// (*lora_flag == *gen, release/acquire at gpu scope), then order the TMA (async proxy) reads of it
-// after that acquire.  A shrink that never runs traps after the timeout instead of hanging.
+// debug counters (collm_gemm_wait_stats): total ns producers spent waiting for the flag, waits
+__device__ unsigned long long g_lora_wait_ns = 0, g_lora_waits = 0;
+
 __device__ __forceinline__ void wait_lora_flag(const GemmLoraParams& p) {
   const int32_t want = *p.gen;
   int32_t v;
   const unsigned long long t0 = clock64();
+  const unsigned long long g0 = gtimer();
   for (;;) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.lora_flag) : "memory");
     if (v == want) break;
@@ -104,6 +110,10 @@ __device__ __forceinline__ void wait_lora_flag(const GemmLoraParams& p) {
     __nanosleep(64);
   }
   asm volatile("fence.proxy.async;" ::: "memory");
+  if (p.dbg) {
+    atomicAdd(&g_lora_wait_ns, gtimer() - g0);
+    atomicAdd(&g_lora_waits, 1ull);
+  }
 }
 
 template <int BN, int STAGES, int CG>

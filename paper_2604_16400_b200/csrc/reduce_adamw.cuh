@@ -249,19 +249,31 @@ __global__ void __launch_bounds__(kReduceThreads, 3) lora_reduce_kernel(const Re
   const int ch_lo = ts * per, ch_hi = min(chunks, ch_lo + per);
   const int n_ch = max(0, ch_hi - ch_lo);
 
+  // per-thread copy geometry, hoisted out of the chunk loop: U chunk = TC x PT (2 16-byte vectors
+  // per thread), V chunk = TC x QT (<= 1 vector per thread)
+  const bf16* u_base = gr.U + gr.u_off + p0;
+  const bf16* v_base = gr.V + gr.v_off;
+  const size_t ldu = gr.ldu, ldv = gr.ldv;
+  const int T = p.T;
+  static_assert(TC * (PT / 8) == 2 * kReduceThreads, "U chunk: two vectors per thread");
+  static_assert(TC * (QT / 8) <= kReduceThreads, "V chunk: at most one vector per thread");
+  const int u_r = threadIdx.x / (PT / 8), u_c = (threadIdx.x % (PT / 8)) * 8;
+  const bool u_col_ok = p0 + u_c < gr.P;
+  const bool v_on = threadIdx.x < TC * (QT / 8);
+  const int v_r = threadIdx.x / (QT / 8), v_c = (threadIdx.x % (QT / 8)) * 8;
+  const bool v_col_ok = v_on && v_c < gr.Q;
   auto load_chunk = [&](int stage, int ch) {
     const int t0 = ch * TC;
-    for (int i = threadIdx.x; i < TC * (PT / 8); i += kReduceThreads) {
-      const int r = i / (PT / 8), cc = (i % (PT / 8)) * 8;
-      const int t = t0 + r, pp = p0 + cc;
-      const bool ok = t < p.T && pp < gr.P;
-      cp_async_16(&Us[stage][r][cc], ok ? gr.U + (size_t)t * gr.ldu + gr.u_off + pp : gr.U, ok);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int r = u_r + k * (TC / 2), t = t0 + r;
+      const bool ok = t < T && u_col_ok;
+      cp_async_16(&Us[stage][r][u_c], ok ? u_base + (size_t)t * ldu + u_c : gr.U, ok);
     }
-    for (int i = threadIdx.x; i < TC * (QT / 8); i += kReduceThreads) {
-      const int r = i / (QT / 8), cc = (i % (QT / 8)) * 8;
-      const int t = t0 + r;
-      const bool ok = t < p.T && cc < gr.Q;
-      cp_async_16(&Vs[stage][r][cc], ok ? gr.V + (size_t)t * gr.ldv + gr.v_off + cc : gr.V, ok);
+    if (v_on) {
+      const int t = t0 + v_r;
+      const bool ok = t < T && v_col_ok;
+      cp_async_16(&Vs[stage][v_r][v_c], ok ? v_base + (size_t)t * ldv + v_c : gr.V, ok);
     }
   };
 
@@ -269,15 +281,14 @@ __global__ void __launch_bounds__(kReduceThreads, 3) lora_reduce_kernel(const Re
 #pragma unroll
   for (int j = 0; j < QT / 8; ++j) d[j][0] = d[j][1] = d[j][2] = d[j][3] = 0.f;
 
-#pragma unroll
   for (int i = 0; i < ST - 1; ++i) {
     if (i < n_ch) load_chunk(i, ch_lo + i);
     cp_async_commit();
   }
+  int stage = 0, fill = ST - 1;  // ring slots of the chunk consumed / refilled (no divisions)
   for (int i = 0; i < n_ch; ++i) {
     cp_async_wait_dyn(ST - 2);
     __syncthreads();
-    const int stage = i % ST;
 #pragma unroll
     for (int kk = 0; kk < TC; kk += 16) {
       uint32_t a0, a1, a2, a3;
@@ -302,8 +313,10 @@ __global__ void __launch_bounds__(kReduceThreads, 3) lora_reduce_kernel(const Re
         }
       }
     }
-    if (i + ST - 1 < n_ch) load_chunk((i + ST - 1) % ST, ch_lo + i + ST - 1);
+    if (i + ST - 1 < n_ch) load_chunk(fill, ch_lo + i + ST - 1);
     cp_async_commit();
+    if (++stage == ST) stage = 0;
+    if (++fill == ST) fill = 0;
   }
   cp_async_wait<0>();
   __syncthreads();

@@ -39,7 +39,9 @@ def only(*kinds: str):
 
 
 def enabled(kind: str) -> bool:
-    return _filter.kinds is None or kind in _filter.kinds
+    """'lora' stands for both rank-space kinds ('shrink' = K1, 'reduce' = K5 + apply)."""
+    k = _filter.kinds
+    return k is None or kind in k or (kind in ("shrink", "reduce") and "lora" in k)
 
 
 def launch_count() -> int:
@@ -118,7 +120,7 @@ def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: 
     ``signal``/``gen``: publish completion for a GEMM consuming the output on another stream."""
     _need(X, torch.bfloat16, "X")
     _need(A, torch.bfloat16, "A")
-    if n_tiles == 0 or not _launch("lora"):
+    if n_tiles == 0 or not _launch("shrink"):
         return
     lda = A.stride(-2)
     if a_stride is None:
@@ -150,7 +152,7 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
     if not _launch("gemm"):
         return
     lora = tile_slot_ptr is not None
-    if not enabled("lora"):  # a GEMM-only timing graph skips the shrinks: nothing to wait for
+    if not enabled("shrink"):  # a timing graph without the shrinks: nothing to wait for
         lora_flag = gen = None
     n_sub = len(sub_n_start) - 1 if (lora and sub_n_start) else 1
     ws = _gemm_ws.get(_lib.load().collm_gemm_workspace_bytes(0), A.device)
@@ -187,7 +189,7 @@ def lora_reduce(T: int, groups: list, mode: int, *, accum_in: bool = False,
                 grad_scale: float = 1.0, adamw: torch.Tensor | None = None,
                 tsplit: int | None = None, device: torch.device | None = None) -> None:
     """K5: C = U^T V per group -> grad store or fused AdamW, one launch (see collm.h)."""
-    if not _launch("lora"):
+    if not _launch("reduce"):
         return
     arr = (_lib.ReduceGroup * len(groups))(*groups)
     device = device or torch.device("cuda", torch.cuda.current_device())
@@ -201,7 +203,7 @@ def lora_reduce(T: int, groups: list, mode: int, *, accum_in: bool = False,
 
 
 def lora_apply(groups: list, mode: int, *, adamw: torch.Tensor | None = None) -> None:
-    if not _launch("lora"):
+    if not _launch("reduce"):
         return
     arr = (_lib.ReduceGroup * len(groups))(*groups)
     _lib.call("collm_lora_apply", arr, len(groups), mode, _p(adamw), _stream())
