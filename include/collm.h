@@ -46,6 +46,10 @@ enum { COLLM_MODE_STORE_GRAD = 0, COLLM_MODE_ADAMW = 1, COLLM_MODE_COPY_ONLY = 2
 /* ---- library / device --------------------------------------------------------------------- */
 int collm_version(void);
 const char* collm_last_error(void);
+/* Load every kernel of the library now (call once per process before the first step): CUDA lazy
+ * loading would load a kernel at its first launch, which can implicitly synchronize the device —
+ * a deadlock when a running GEMM waits for the shrink being launched on another stream. */
+int collm_preload(void);
 /* Fills compute capability and SM count; COLLM_EUNSUPPORTED unless sm_100. */
 int collm_device_info(int device, int* sm_major, int* sm_minor, int* num_sms);
 

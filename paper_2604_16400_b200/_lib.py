@@ -43,6 +43,7 @@ SIGNATURES: dict[str, tuple] = {
     "collm_version": (_I, []),
     "collm_last_error": (C.c_char_p, []),
     "collm_device_info": (_I, [_I, _IP, _IP, _IP]),
+    "collm_preload": (_I, []),
     "collm_plan_segments": (_I, [_IP, _IP, _I, _I, _IP, _IP, _I, _IP, _IP, _I, _IP]),
     "collm_expand_segments": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P]),
     "collm_lora_shrink": (_I, [_P, _I, _P, _LL, _I, _P, _I, _P, _IP, _I, _P, _P, _I, _P, _P,
@@ -81,6 +82,12 @@ def load(path: Path | None = None) -> C.CDLL:
             fn.restype = res
             fn.argtypes = args
         _lib = lib
+        try:  # force-load the kernels (lazy loading can deadlock the two-stream overlap)
+            import torch
+            if torch.cuda.is_available():
+                lib.collm_preload()
+        except ImportError:  # pragma: no cover
+            pass
         return lib
 
 

@@ -114,6 +114,12 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   if (!configured) {
     CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
+    // the whole unified L1/shared array as shared memory: the SM then has room for a rank-space
+    // CTA next to this GEMM CTA (the two-stream overlap); the default carveout is the smallest
+    // one that fits the GEMM alone
+    CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG>,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
     configured = true;
   }
   cudaLaunchConfig_t cfg{};
@@ -286,7 +292,17 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = csize > 1 ? 1 : 0;  // no cluster launch unless the K range is split
+  {
+    static bool configured = false;
+    if (!configured) {
+      CUDA_TRY(cudaFuncSetAttribute(lora_shrink_kernel<2, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+      CUDA_TRY(cudaFuncSetAttribute(lora_shrink_kernel<4, 3>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+      CUDA_TRY(cudaFuncSetAttribute(lora_shrink_kernel<6, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+      CUDA_TRY(cudaFuncSetAttribute(lora_shrink_kernel<8, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+      configured = true;
+    }
+  }
   if (max_ranks <= 16)
     CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_kernel<2, 4>, p));
   else if (max_ranks <= 32)
@@ -500,6 +516,35 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   return launch_gemm<128, 6, 1>(ta, tb, th, tlb, ty, p, grid, st);
 }
 
+// Force-load every kernel of the library now (CUDA lazy module loading would otherwise load a
+// kernel at its first launch, which can implicitly synchronize the device — fatal when a GEMM is
+// already running and waiting for the very shrink being launched on another stream).
+int collm_preload(void) {
+  cudaFuncAttributes a;
+#define COLLM_PRELOAD(k) CUDA_TRY(cudaFuncGetAttributes(&a, k))
+  COLLM_PRELOAD(expand_segments_kernel);
+  COLLM_PRELOAD((lora_shrink_kernel<2, 4>));
+  COLLM_PRELOAD((lora_shrink_kernel<4, 3>));
+  COLLM_PRELOAD((lora_shrink_kernel<6, 2>));
+  COLLM_PRELOAD((lora_shrink_kernel<8, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 6, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 8, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 5, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 6, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 4, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 5, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 4, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 6, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 3, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 4, 1>));
+  COLLM_PRELOAD(lora_reduce_kernel<16>);
+  COLLM_PRELOAD(lora_reduce_kernel<32>);
+  COLLM_PRELOAD(lora_reduce_kernel<48>);
+  COLLM_PRELOAD(lora_apply_kernel);
+#undef COLLM_PRELOAD
+  return COLLM_OK;
+}
+
 int collm_set_gemm_lean(int lean) {
   g_gemm_lean = lean != 0;
   g_reduce_lean = lean != 0;
@@ -616,6 +661,8 @@ static int launch_reduce(ReduceParams& p, cudaStream_t st) {
   if (!configured) {
     CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ReduceSmem<QT>::total(kReduceMaxStages)));
+    CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
     configured = true;
   }
   const size_t budget = g_reduce_lean ? 44u * 1024 : 100u * 1024;

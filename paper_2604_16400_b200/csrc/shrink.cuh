@@ -116,7 +116,7 @@ __device__ __forceinline__ void shrink_store(const ShrinkParams& p, const RowSlo
 }
 
 template <int NT, int UNR>  // NT: n8 rank tiles per warp (n_ranks <= 8*NT); UNR: K steps in flight
-__global__ void __launch_bounds__(kShrinkWarps * 32, 2)
+__global__ void __launch_bounds__(kShrinkWarps * 32, 3)
     lora_shrink_kernel(const ShrinkParams p) {
   namespace cg = cooperative_groups;
   constexpr int W2 = kShrinkWarps / 2;

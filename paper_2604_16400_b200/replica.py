@@ -18,6 +18,7 @@ fused AdamW step, as the metric's FLOP count assumes.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -334,7 +335,8 @@ class ReplicaStack:
     def _side_stream(self) -> torch.cuda.Stream:
         if self._side is None:
             # high priority: the rank-space CTAs a spinning GEMM waits for are scheduled first
-            self._side = torch.cuda.Stream(self.device, priority=-1)
+            prio = int(os.environ.get("COLLM_SIDE_PRIORITY", "-1"))
+            self._side = torch.cuda.Stream(self.device, priority=prio)
         return self._side
 
     # ------------------------------------------------------------------ graphs
