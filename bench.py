@@ -354,8 +354,10 @@ def run_ours(args, cfg, workload):
         with torch.cuda.stream(s):
             with ops.only("gemm"), torch.cuda.graph(gg, stream=s):
                 stack.run_step(plan, optimizer_step=fused_opt, advance=False)
+            # the rank-space kernels alone, serialized on one stream with their standalone
+            # launch configuration (in the overlapped step they share SMs with the GEMMs)
             with ops.only("lora", "plan"), torch.cuda.graph(gl, stream=s):
-                stack.run_step(plan, optimizer_step=fused_opt, advance=False)
+                stack.run_step(plan, optimizer_step=fused_opt, advance=False, overlap=False)
         st_dev.wait_stream(s)
         reps = max(3, min(20, args.steps))
         gg.replay()

@@ -116,7 +116,8 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
     // the whole unified L1/shared array as shared memory: the SM then has room for a rank-space
     // CTA next to this GEMM CTA (the two-stream overlap); the default carveout is the smallest
-    // one that fits the GEMM alone
+    // one that fits the GEMM alone.  (The rank-space kernels keep the default: alone on an SM
+    // they profit from L1; next to a GEMM CTA the SM is already configured this way.)
     CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG>,
                                   cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
@@ -224,6 +225,13 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
   return COLLM_OK;
 }
 
+// Overlap mode (collm_set_gemm_lean): GEMMs run "lean" pipelines and the rank-space kernels are
+// sized and launched to fit next to a GEMM CTA on the same SM.
+static bool g_gemm_lean = false;
+// Shared-memory budget of the K5 reduction: lean = next to a GEMM CTA on the same SM (the
+// two-stream overlap, collm_set_gemm_lean), else up to the full ring depth.
+static bool g_reduce_lean = false;
+
 // ------------------------------------------------------------------------------------ K1
 
 
@@ -286,23 +294,24 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
   cfg.stream = (cudaStream_t)stream;
   p.signal = signal;
   p.gen = gen;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = csize;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = csize > 1 ? 1 : 0;  // no cluster launch unless the K range is split
-  {
-    static bool configured = false;
-    if (!configured) {
-      CUDA_TRY(cudaFuncSetAttribute(lora_shrink_kernel<2, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-      CUDA_TRY(cudaFuncSetAttribute(lora_shrink_kernel<4, 3>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-      CUDA_TRY(cudaFuncSetAttribute(lora_shrink_kernel<6, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-      CUDA_TRY(cudaFuncSetAttribute(lora_shrink_kernel<8, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-      configured = true;
-    }
+  // next to a lean GEMM (the two-stream overlap) ask for the max-shared carveout: an SM this
+  // kernel reaches first must still fit a GEMM CTA; alone, keep the default (more L1)
+  attr[1].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+  attr[1].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
+  cudaLaunchAttribute* ap = attr;
+  int na = 0;
+  if (csize > 1) ++na;  // no cluster launch unless the K range is split
+  if (g_gemm_lean) {
+    if (na == 0) ap = attr + 1;
+    ++na;
   }
+  cfg.attrs = ap;
+  cfg.numAttrs = na;
   if (max_ranks <= 16)
     CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_kernel<2, 4>, p));
   else if (max_ranks <= 32)
@@ -315,10 +324,7 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
 }
 
 // ------------------------------------------------------------------------------------ K2/K3
-static bool g_gemm_lean = false;
-// Shared-memory budget of the K5 reduction: lean = next to a GEMM CTA on the same SM (the
-// two-stream overlap, collm_set_gemm_lean), else up to the full ring depth.
-static bool g_reduce_lean = false;
+
 
 // debug-only: device pointer of the last GEMM's timeline (COLLM_GEMM_DEBUG set)
 unsigned long long* collm_debug_timeline = nullptr;
@@ -661,17 +667,23 @@ static int launch_reduce(ReduceParams& p, cudaStream_t st) {
   if (!configured) {
     CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ReduceSmem<QT>::total(kReduceMaxStages)));
-    CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  cudaSharedmemCarveoutMaxShared));
     configured = true;
   }
   const size_t budget = g_reduce_lean ? 44u * 1024 : 100u * 1024;
   int stages = kReduceMaxStages;
   while (stages > 2 && ReduceSmem<QT>::total(stages) > budget) --stages;
   p.stages = stages;
-  dim3 grid(p.n_tiles, p.tsplit);
-  lora_reduce_kernel<QT><<<grid, kReduceThreads, ReduceSmem<QT>::total(stages), st>>>(p);
-  CUDA_TRY(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.n_tiles, p.tsplit);
+  cfg.blockDim = dim3(kReduceThreads);
+  cfg.dynamicSmemBytes = ReduceSmem<QT>::total(stages);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePreferredSharedMemoryCarveout;  // see collm_lora_shrink
+  attr[0].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_reduce_lean ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_reduce_kernel<QT>, p));
   return COLLM_OK;
 }
 
