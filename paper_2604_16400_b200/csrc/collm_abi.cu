@@ -385,9 +385,12 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   const char* sched_env = getenv("COLLM_GEMM_SCHED");
   const int force_sched = !sched_env ? -1 : strcmp(sched_env, "dp") == 0 ? 0
                           : strcmp(sched_env, "hybrid") == 0 ? 1 : strcmp(sched_env, "sknofix") == 0 ? 2
-                          : strcmp(sched_env, "noload") == 0 ? 3 : -1;
+                          : strcmp(sched_env, "noload") == 0 ? 3
+                          : strcmp(sched_env, "split2") == 0 ? 4 : -1;
   Cand best{0, 0, 0, 1e30};
   const double nk = (K + kGemmBK - 1) / kGemmBK;
+  int force_sched_eff = force_sched;
+  for (int attempt = 0; attempt < 2 && best.cg == 0; ++attempt, force_sched_eff = -1)
   for (int cg : {2, 1}) {
     if (force_cg && cg != force_cg) continue;
     const long long units = sms / cg;
@@ -397,10 +400,15 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
       if (!aligned_to(b) || (b == 256 && N <= 128 && !force_bn)) continue;
       const double kb = cg == 2 ? (b == 256 ? 0.43 : 0.34) : (b == 256 ? 0.48 : 0.34);
       const long long tiles = nmu * ((N + b - 1) / b);
-      for (int sc : {0, 1}) {
-        if (force_sched >= 0 && (force_sched == 2 ? 1 : force_sched == 3 ? 0 : force_sched) != sc) continue;
+      for (int sc : {0, 1, 4}) {
+        if (force_sched_eff >= 0 && (force_sched_eff == 2 ? 1 : force_sched_eff == 3 ? 0 : force_sched_eff) != sc) continue;
         double cost;
-        if (sc == 0) {
+        if (sc == 4) {
+          // split-2: every tile's K halved over two units that swap half-tile partials (2-CTA
+          // pairs only, needs 2 x tiles <= units); calibrated swap cost ~4 us
+          if (cg != 2 || 2 * tiles > units || nk < 2) continue;  // both halves non-empty
+          cost = std::ceil(nk / 2.0) * kb + 4.0;
+        } else if (sc == 0) {
           cost = (double)((tiles + units - 1) / units) * nk * kb;
         } else {
           const long long waves = tiles / units;
@@ -416,7 +424,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   if (best.cg == 0) return fail(COLLM_EINVAL, "no GEMM tile fits (sub-projection boundaries must be x128)");
   const int cg = best.cg;
   bn = best.bn;
-  const int sched = force_sched >= 2 ? force_sched : best.sched;
+  const int sched = (force_sched == 2 || force_sched == 3) ? force_sched : best.sched;
   const int nm = (M + kGemmBM * cg - 1) / (kGemmBM * cg);
   CHECK_ARG(nm <= kMaxMTiles, "M=%d exceeds %d rows", M, kMaxMTiles * kGemmBM);
   CHECK_ARG(bn == 128 || bn == 256, "bn must be 0, 128 or 256");
@@ -480,7 +488,8 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   // persistent grid: one CTA (pair) per SM (pair), never more units than k-stages (every
   // stream-K range non-empty)
   const long long min_work = (long long)nm * p.num_n_tiles * ((K + kGemmBK - 1) / kGemmBK);
-  const int grid = cg * (int)std::min<long long>(sms / cg, min_work);
+  const int grid = sched == 4 ? cg * 2 * nm * p.num_n_tiles
+                              : cg * (int)std::min<long long>(sms / cg, min_work);
   p.sched = sched;
   p.lora_flag = lora ? lora_flag : nullptr;
   p.gen = gen;

@@ -109,7 +109,7 @@ __device__ __forceinline__ void wait_lora_flag(const GemmLoraParams& p) {
     }
     __nanosleep(64);
   }
-  asm volatile("fence.proxy.async;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
   if (p.dbg) {
     atomicAdd(&g_lora_wait_ns, gtimer() - g0);
     atomicAdd(&g_lora_waits, 1ull);
@@ -147,7 +147,8 @@ __device__ __forceinline__ int sub_of_n0(const GemmLoraParams& p, int n0) {
 struct Segment {
   int m_blk, n_blk;
   int k0, k1;     // stage range [k0, k1) within the tile
-  int mode;       // 0 = whole tile, 1 = partial (write partials[cta]), 2 = finish (add parts)
+  int mode;       // 0 = whole tile, 1 = partial (write partials[cta]), 2 = finish (add parts),
+                  // 3 = split-2 half (the two halves exchange each other's columns)
   int c_first;    // mode 2: the CTAs [c_first, this CTA) hold the earlier parts
 };
 
@@ -157,12 +158,16 @@ struct StreamK {
   int G;
   int dp_tiles;           // tiles [0, dp_tiles) are data-parallel
   long long W_lo, W;      // stream-K region [W_lo, W_lo + W) of the global stage line
+  bool split2;            // sched 4: unit u computes half (u & 1) of tile (u >> 1)
+  int n_tiles;
 
   __device__ void init(const int32_t* pre, int nm, int nn, int grid, int sched) {
     prefix = pre;
     num_m = nm;
     sum_s = pre[nm];
     G = grid;
+    split2 = sched == 4;
+    n_tiles = nm * nn;
     const int tiles = nm * nn;
     const int waves = tiles / grid;
     dp_tiles = sched == 0 ? tiles : (waves >= 1 ? (waves - 1) * grid : 0);
@@ -207,6 +212,20 @@ struct StreamK {
   // Visit this CTA's work: its data-parallel tiles, then its stream-K segments in reverse.
   template <class F>
   __device__ void for_each(int c, F&& f) const {
+    if (split2) {  // one half-tile per unit, halves of a tile in adjacent units
+      const int t = c >> 1;
+      if (t >= n_tiles) return;
+      Segment sg;
+      sg.m_blk = t % num_m;
+      sg.n_blk = t / num_m;
+      const int S = stages_of_m(sg.m_blk);
+      sg.k0 = (c & 1) ? S / 2 : 0;  // the LoRA stages (last) fall in half 1
+      sg.k1 = (c & 1) ? S : S / 2;
+      sg.mode = 3;
+      sg.c_first = c ^ 1;
+      f(sg);
+      return;
+    }
     for (int t = c; t < dp_tiles; t += G) {
       Segment sg;
       sg.m_blk = t % num_m;
@@ -455,6 +474,9 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
               }
             } while (v == 0);
           }
+          // the parts' generic-proxy stores, acquired above, are read below by bulk copies
+          // (async proxy): order them
+          asm volatile("fence.proxy.async.global;" ::: "memory");
           if (dbg) dbg[14] = gtimer();
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -485,6 +507,105 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
       // partial tiles are stored in the epilogue's own thread order — float4 index
       // ((chunk * 8 + j) * 128 + tid) — so writes and reads are 512 B-coalesced per warp
       float4* part_mine = reinterpret_cast<float4*>(p.partials + (size_t)cta * (BM * BN)) + tid;
+      // bf16 row chunk -> this warp's staging buffer (64-byte TMA swizzle: 16-byte chunk j of
+      // row r at j ^ ((r >> 1) & 3)), then one TMA store of the [32 rows x 32 cols] box; the
+      // tensor map clips rows >= M and columns >= N
+      auto store_chunk = [&](const uint32_t (&r)[32], int c) {
+        uint8_t* buf = epi_buf + (ew * 2 + (epi_i & 1)) * L::kEpiBuf;
+        if (lane == 0) bulk_wait_group_read<1>();  // the store that last used it has read it
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(r[8 * j + 0]), __uint_as_float(r[8 * j + 1]));
+          v.y = pack_bf16x2(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3]));
+          v.z = pack_bf16x2(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5]));
+          v.w = pack_bf16x2(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7]));
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = v;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmY, buf, n0 + c, row - lane);
+          bulk_commit_group();
+        }
+        ++epi_i;
+      };
+      if (sg.mode == 3) {
+        // split-2 tile: both halves finish together; each writes the fp32 partial of the OTHER
+        // half's columns, then adds the partner's partial of its own columns (streamed into the
+        // idle pipeline smem) and stores them.  acc_0 + acc_1 is commutative: bitwise the same
+        // whichever half adds.
+        constexpr int NCH = BN / 32;
+        const int half = unit & 1;
+        const int own_lo = half ? NCH / 2 : 0, own_hi = half ? NCH : NCH / 2;
+        const int partner = sg.c_first * CG + (int)rank;
+#pragma unroll 1
+        for (int chunk = 0; chunk < NCH; ++chunk) {
+          if (chunk >= own_lo && chunk < own_hi) continue;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + chunk * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            __stcg(part_mine + (chunk * 8 + j) * 128,
+                   make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (tid == 0) {
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.flags + cta), "r"(1u) : "memory");
+          const int32_t* f = p.flags + partner;
+          uint32_t v;
+          const unsigned long long t0 = clock64();
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if (clock64() - t0 > COLLM_MBAR_TIMEOUT_CYCLES) {
+              printf("collm: split-2 flag timeout (block %d)\n", blockIdx.x);
+              __trap();
+            }
+          } while (v == 0);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk reads
+          for (int chunk = own_lo; chunk < own_hi; ++chunk) {  // one ring slot per own chunk
+            const int slot = chunk - own_lo;
+            mbar_arrive_expect_tx(&fixbar[slot], L::kFixPiece);
+            bulk_copy_g2s(smem + slot * L::kFixPiece,
+                          p.partials + (size_t)partner * (BM * BN) + (size_t)chunk * (BM * 32),
+                          L::kFixPiece, &fixbar[slot]);
+          }
+        }
+#pragma unroll 1
+        for (int chunk = own_lo; chunk < own_hi; ++chunk) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + chunk * 32, r);
+          tmem_wait_ld();
+          const int slot = chunk - own_lo;
+          mbar_wait(&fixbar[slot], 0);
+          const float4* src = reinterpret_cast<const float4*>(smem + slot * L::kFixPiece) + tid;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 v = src[j * 128];
+            r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + v.x);
+            r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + v.y);
+            r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + v.z);
+            r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
+          }
+          store_chunk(r, chunk * 32);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+          else mbar_arrive(&tempty[acc]);
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the partner's partial is consumed
+        if (tid == 0) p.flags[partner] = 0;                // ready for the next launch
+        ++seg_i;
+        return;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -523,28 +644,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
               if (chunk * np + i + RS < n_pieces) issue_piece(chunk * np + i + RS);
           }
         }
-        // bf16 row chunk -> this warp's staging buffer (64-byte TMA swizzle: 16-byte chunk j of
-        // row r at j ^ ((r >> 1) & 3)), then one TMA store of the [32 rows x 32 cols] box; the
-        // tensor map clips rows >= M and columns >= N
-        uint8_t* buf = epi_buf + (ew * 2 + (epi_i & 1)) * L::kEpiBuf;
-        if (lane == 0) bulk_wait_group_read<1>();  // the store that last used this buffer has read it
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(r[8 * j + 0]), __uint_as_float(r[8 * j + 1]));
-          v.y = pack_bf16x2(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3]));
-          v.z = pack_bf16x2(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5]));
-          v.w = pack_bf16x2(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7]));
-          *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = v;
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tmY, buf, n0 + c, row - lane);
-          bulk_commit_group();
-        }
-        ++epi_i;
+        store_chunk(r, c);
       }
       tc_fence_before();
       __syncwarp();

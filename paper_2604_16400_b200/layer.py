@@ -89,12 +89,13 @@ class OptimizerState:
         self.cfg = cfg or AdamWConfig()
         self.step = 0
         self.args = torch.zeros(7, dtype=torch.float32, device=device)
-        self._host = torch.zeros(7, dtype=torch.float32).pin_memory()
 
     def advance(self) -> None:
         self.step += 1
-        self._host.copy_(torch.tensor(self.cfg.args(self.step), dtype=torch.float32))
-        self.args.copy_(self._host, non_blocking=True)
+        # a fresh pinned staging tensor per step: the caching host allocator keeps it alive until
+        # the async copy has run, so a CPU running steps ahead never overwrites a pending copy
+        host = torch.tensor(self.cfg.args(self.step), dtype=torch.float32).pin_memory()
+        self.args.copy_(host, non_blocking=True)
 
 
 @dataclass

@@ -68,7 +68,6 @@ class ReplicaStack:
         self._side: torch.cuda.Stream | None = None
         self.overlap = False
         self._gen: torch.Tensor | None = None
-        self._gen_host: torch.Tensor | None = None
         self._gen_count = 0
         self._sig: torch.Tensor | None = None
 
@@ -317,10 +316,10 @@ class ReplicaStack:
             self.opt.advance()
         if self._gen is None:
             self._gen = torch.zeros(1, dtype=torch.int32, device=self.device)
-            self._gen_host = torch.zeros(1, dtype=torch.int32).pin_memory()
         self._gen_count += 1
-        self._gen_host.fill_(self._gen_count)
-        self._gen.copy_(self._gen_host, non_blocking=True)
+        # fresh pinned staging per step (see OptimizerState.advance)
+        host = torch.tensor([self._gen_count], dtype=torch.int32).pin_memory()
+        self._gen.copy_(host, non_blocking=True)
 
     def _signals(self, n: int) -> torch.Tensor:
         """int32 [n, 2] shrink->GEMM completion signals (zeroed once; the kernels restore the

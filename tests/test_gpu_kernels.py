@@ -28,12 +28,14 @@ def lib():
     return _lib.load()
 
 
-GEMM_VARIANTS = [("1", "dp"), ("1", "hybrid"), ("2", "dp"), ("2", "hybrid")]
+GEMM_VARIANTS = [("1", "dp"), ("1", "hybrid"), ("2", "dp"), ("2", "hybrid"), ("2", "split2")]
 
 
 @pytest.fixture(params=GEMM_VARIANTS, ids=lambda v: f"cg{v[0]}-{v[1]}")
 def gemm_variant(request, monkeypatch):
-    """Force each kernel variant (CTA or CTA-pair tiles, data-parallel or stream-K)."""
+    """Force each kernel variant (CTA or CTA-pair tiles; data-parallel, stream-K, or split-2
+    where every tile's K is halved over two CTA pairs that swap half-tile partials — shapes
+    with too many tiles for split-2 fall back to the cost model's choice)."""
     monkeypatch.setenv("COLLM_GEMM_CG", request.param[0])
     monkeypatch.setenv("COLLM_GEMM_SCHED", request.param[1])
     return request.param

@@ -10,10 +10,21 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _stack(overlap, cfg_key="tiny", seed=0):
+def _config(cfg_key):
+    """A BASELINE config, optionally cut to its first layers ('llama2-7b:2')."""
+    import dataclasses
+
     from paper_2604_16400_b200.configs import CONFIGS
+    key, _, layers = cfg_key.partition(":")
+    cfg = CONFIGS[key]
+    if layers:
+        cfg = dataclasses.replace(cfg, model=dataclasses.replace(cfg.model, layers=int(layers)))
+    return cfg
+
+
+def _stack(overlap, cfg_key="tiny", seed=0):
     from paper_2604_16400_b200.replica import ReplicaStack
-    cfg = CONFIGS[cfg_key]
+    cfg = _config(cfg_key)
     st = ReplicaStack(cfg, "cuda", seed=seed)
     st.overlap = overlap
     plan = st.plan(*cfg.batch(0))
@@ -29,8 +40,12 @@ def _state(st):
     return out
 
 
-@pytest.mark.parametrize("cfg_key", ["tiny"])
+@pytest.mark.parametrize("cfg_key", ["tiny", "llama2-7b:2", "llama3-8b:1", "llama2-13b:1"])
 def test_overlap_and_graph_bitwise(cfg_key):
+    """At the tiny shape and at the real 7B/8B/13B shapes (few layers): the two-stream overlap
+    (shrink || its GEMM's main loop, flag-signalled LoRA stages; K5 on the side stream) and CUDA
+    graph replay give bitwise the serialized results — and never deadlock (a GEMM waiting on a
+    shrink that cannot start would trap after the timeout)."""
     ref, plan = _stack(False, cfg_key)
     for _ in range(2):
         ref.run_step(plan)
@@ -89,3 +104,39 @@ def test_measured_latency_backend():
     t_tr = be.true_train_latency(None, cfg)
     assert 0 < t_inf < t_tr < 1.0
     assert be.true_infer_latency(None, cfg) == t_inf  # cached per (B, b)
+
+
+def test_stack_backward_matches_oracle():
+    """The stack's training-row backward through the overlapped step — dH shrinks, dX GEMMs and
+    the per-layer batched K5 launch (STORE_GRAD mode) — against the oracle on the stack's own
+    buffers, for every projection of the first and last layer of the tiny stack."""
+    import oracle
+    st, plan = _stack(True)
+    st.run_step(plan, optimizer_step=False)
+    torch.cuda.synchronize()
+    a = st._acts
+    L = len(st.layers)
+    Ttr = plan.n_train
+    f = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
+    for l in (0, L - 1):
+        for proj in st.layers[l]:
+            name = proj.spec.name
+            t = proj.train_state.adapter
+            X = a["X"][l] if name in ("qkv", "q", "k", "v", "gate_up", "gate", "up") else \
+                (a["Xo"][l] if name == "o" else a["Xd"][l])
+            dY = (a["dY_top"] if l == L - 1 else a["dX_first"][l + 1]) if name == "down" \
+                else a["dY"][l][name]
+            H16 = proj._H16[:Ttr]
+            dH16 = proj._dH16[:Ttr]
+            # dB from the oracle formula on the device's H16; dA^T on the device's dH16
+            _, dB_ref, _, dH_ref = oracle.lora_backward(
+                f(dY), f(X[:Ttr]), f(H16), f(proj.W), f(proj.A[t]), f(proj.B[t]),
+                float(proj.scale[t]), proj.spec.subs, proj.spec.r_pad)
+            dAT_ref = f(X[:Ttr]).T @ f(dH16)
+            gB, gAT = f(proj.train_state.grad_B), f(proj.train_state.grad_AT)
+            for got, ref, what in ((gB, dB_ref, "dB"), (gAT, dAT_ref, "dA^T")):
+                rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+                assert rel < 1e-4, f"layer {l} {name} {what}: rel err {rel}"
+            # the device dH16 is the bf16 rounding of the oracle's (summation order aside)
+            err = np.abs(f(dH16) - dH_ref).max()
+            assert err <= 1e-2 * np.abs(dH_ref).max() + 1e-6, f"layer {l} {name} dH: {err}"
