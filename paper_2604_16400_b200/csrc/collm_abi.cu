@@ -128,13 +128,20 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = L::kTotal;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // PDL (opt-in, COLLM_GEMM_PDL=1): the prologue overlaps the previous grid of the stream (the
+  // kernel waits for it with griddepcontrol.wait before touching global memory).  Measured: GEMM
+  // chains -0.3 ms/step, but the full overlapped step no faster (early-resident GEMM CTAs hold SM
+  // space the rank-space kernels want), so it is off by default.
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool pdl = [] { const char* e = getenv("COLLM_GEMM_PDL"); return e && atoi(e) != 0; }();
+  cfg.numAttrs = pdl ? 2 : 1;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_lora_kernel<BN, STAGES, CG>, ta, tb, th, tlb, ty, p));
   return COLLM_OK;
 }

@@ -314,6 +314,12 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
   if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch (GEMM after GEMM on one stream): everything above — barrier
+  // init, TMEM allocation, descriptor prefetch, the schedule prefix — overlapped the previous
+  // grid's tail; no global memory the previous grid may still write is touched before this wait.
+  // The next grid may launch as SMs free up (its own prologue then waits here in turn).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   StreamK sk;
   sk.init(s_prefix, p.num_m_tiles, p.num_n_tiles, gridDim.x / CG, p.sched);
