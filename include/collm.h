@@ -110,6 +110,9 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
  * Each tile runs its K/64 main blocks first and its LoRA k-stages last.  With lora_flag / gen
  * (device, optional) the producer waits for *lora_flag == *gen before loading the LoRA operand, so
  * the shrink writing Hslots may run concurrently on another stream (collm_lora_shrink signal).
+ * Alternatively lora_pdl = 1: the GEMM is launched programmatically dependent on the preceding
+ * kernel of the SAME stream (that shrink, which lets it start at once) and its LoRA stages wait
+ * for that grid's completion (griddepcontrol.wait) — the same overlap with no flag.
  * Replaces: perf.true_infer_latency / true_train_latency (perf.py:62-89). */
 size_t collm_gemm_workspace_bytes(int bn);
 int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int ldy, int M, int N,
@@ -117,7 +120,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
                     int lb_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
                     int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
                     const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
-                    const int32_t* lora_flag, const int32_t* gen, void* stream);
+                    const int32_t* lora_flag, const int32_t* gen, int lora_pdl, void* stream);
 
 /* Select the GEMM pipeline depth: lean != 0 -> ~128 KB shared memory per CTA so one CTA of the
  * LoRA kernels can run on the same SM concurrently (graph branch / second stream); 0 -> deepest

@@ -140,8 +140,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  static const bool pdl = [] { const char* e = getenv("COLLM_GEMM_PDL"); return e && atoi(e) != 0; }();
-  cfg.numAttrs = pdl ? 2 : 1;
+  cfg.numAttrs = p.pdl_mode ? 2 : 1;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_lora_kernel<BN, STAGES, CG>, ta, tb, th, tlb, ty, p));
   return COLLM_OK;
 }
@@ -285,10 +284,10 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
   p.Hslots = (bf16*)Hslots;
   p.slot_of_row = slot_of_row;
   p.tile_slot_ptr = tile_slot_ptr;
-  // cluster size: split K across up to 8 CTAs so the grid fills two resident CTAs per SM
+  // cluster size: split K across up to 8 CTAs so the grid fills about three resident CTAs per SM
   int csize = 1;
   const int sms = num_sms_cached();
-  while (csize < 8 && (long long)n_tiles * n_groups * csize * 2 <= 2LL * sms) csize *= 2;
+  while (csize < 8 && (long long)n_tiles * n_groups * csize * 2 <= 3LL * sms) csize *= 2;
   {
     const char* env = getenv("COLLM_SHRINK_CLUSTER");
     if (env) csize = std::max(1, std::min(8, atoi(env)));
@@ -360,7 +359,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
                     int lb_rows, const int32_t* tile_slot_ptr, const int32_t* slot_adapter,
                     int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
                     const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
-                    const int32_t* lora_flag, const int32_t* gen, void* stream) {
+                    const int32_t* lora_flag, const int32_t* gen, int lora_pdl, void* stream) {
   CHECK_ARG(A && B && Y, "null operand");
   CHECK_ARG(!lora_flag == !gen, "lora_flag and gen go together");
   CHECK_ARG(M >= 1 && N >= 1 && K >= 1, "empty GEMM M=%d N=%d K=%d", M, N, K);
@@ -500,6 +499,10 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   p.sched = sched;
   p.lora_flag = lora ? lora_flag : nullptr;
   p.gen = gen;
+  {
+    static const bool prologue_pdl = [] { const char* e = getenv("COLLM_GEMM_PDL"); return e && atoi(e) != 0; }();
+    p.pdl_mode = (lora && lora_pdl) ? 2 : (prologue_pdl ? 1 : 0);
+  }
   const size_t need = collm_gemm_workspace_bytes(bn);
   CHECK_ARG(workspace && ws_bytes >= need, "gemm workspace too small: %zu < %zu", ws_bytes, need);
   p.flags = (int32_t*)workspace;

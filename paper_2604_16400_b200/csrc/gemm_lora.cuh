@@ -73,6 +73,10 @@ struct GemmLoraParams {
   // before its first LoRA k-stage the producer waits for *lora_flag == *gen (null: no wait)
   const int32_t* lora_flag;
   const int32_t* gen;
+  // programmatic dependent launch: 1 = the whole kernel waits for the previous grid after its
+  // prologue (GEMM after GEMM); 2 = only the LoRA stages wait (the previous grid is the shrink
+  // producing the LoRA operand, launched just before on the same stream)
+  int pdl_mode;
   int sched;  // 0 = data-parallel (round-robin tiles), 1 = hybrid data-parallel + stream-K,
               // 2 = debug: stream-K split without fix-up (timing experiments only)
   // ---- stream-K
@@ -318,8 +322,10 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
   // init, TMEM allocation, descriptor prefetch, the schedule prefix — overlapped the previous
   // grid's tail; no global memory the previous grid may still write is touched before this wait.
   // The next grid may launch as SMs free up (its own prologue then waits here in turn).
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.pdl_mode == 1) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
 
   StreamK sk;
   sk.init(s_prefix, p.num_m_tiles, p.num_n_tiles, gridDim.x / CG, p.sched);
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t rc = p.lora_rc;
-    bool lora_ready = p.lora_flag == nullptr;
+    bool lora_ready = p.lora_flag == nullptr && p.pdl_mode != 2;
     sk.for_each(unit, [&](const Segment& sg) {
       const int m0 = sg.m_blk * UNIT_M + rank * BM;  // this CTA's rows
       const int n0 = sg.n_blk * BN;
@@ -348,7 +354,12 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
         uint8_t* sa = smem + stage * L::kStageBytes;
         const bool lora_stage = i >= nk;  // the tile's LoRA k-stages follow its K/64 main blocks
         if (lora_stage && !lora_ready) {
-          wait_lora_flag(p);
+          if (p.pdl_mode == 2) {  // the shrink grid (launched just before) completed + visible
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          } else {
+            wait_lora_flag(p);
+          }
           lora_ready = true;
         }
         int it0 = 0, n_it = 0;  // this LoRA stage's (slot, chunk) items

@@ -119,6 +119,9 @@ template <int NT, int UNR>  // NT: n8 rank tiles per warp (n_ranks <= 8*NT); UNR
 __global__ void __launch_bounds__(kShrinkWarps * 32, 3)
     lora_shrink_kernel(const ShrinkParams p) {
   namespace cg = cooperative_groups;
+  // a GEMM launched programmatically dependent on this shrink (same stream, pdl_mode 2) may
+  // start right away: its main loop overlaps this grid, its LoRA stages wait for our completion
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int W2 = kShrinkWarps / 2;
   constexpr int LD = 8 * NT + 1;
   __shared__ float red[W2][16][LD];

@@ -243,10 +243,13 @@ class LoraProjection:
         return ForwardCache(X=X, H16=H16, n_train=n_train)
 
     def forward_gemm(self, cache: ForwardCache, plan: DevicePlan,
-                     Y: torch.Tensor | None = None, wait: tuple | None = None) -> torch.Tensor:
+                     Y: torch.Tensor | None = None, wait: tuple | None = None,
+                     pdl: bool = False) -> torch.Tensor:
         """K2: the base projection with the multi-adapter expand fused into the accumulator.
         ``wait`` = the shrink's (signal, generation): this GEMM may run before that shrink has
-        finished (another stream); it loads the LoRA operand only after the signal."""
+        finished (another stream); it loads the LoRA operand only after the signal.  ``pdl``: the
+        shrink was the previous launch on this stream; overlap it by programmatic dependent launch
+        instead (the LoRA stages wait for that grid)."""
         spec = self.spec
         T = plan.n_rows
         X = cache.X
@@ -262,7 +265,8 @@ class LoraProjection:
                           tile_slot_ptr=plan.tile_slot_ptr, slot_adapter=plan.slot_adapter,
                           lora_rank=rp, lb_rows_per_adapter=spec.out_features, sub_n_start=bnd,
                           sub_h_col=[s * rp for s in range(len(spec.subs))],
-                          lora_flag=wait[0][1:] if wait else None, gen=wait[1] if wait else None)
+                          lora_flag=wait[0][1:] if wait else None, gen=wait[1] if wait else None,
+                          lora_pdl=pdl)
         else:
             ops.gemm_lora(X, self.W, Y, M=T)
         return Y
@@ -334,7 +338,8 @@ class LoraProjection:
         return dH16
 
     def backward_dx(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan,
-                    dX: torch.Tensor | None = None, wait: tuple | None = None) -> torch.Tensor:
+                    dX: torch.Tensor | None = None, wait: tuple | None = None,
+                    pdl: bool = False) -> torch.Tensor:
         """K3: dX = dY . W + dH . A_t (reads A_t^T: run before this projection's optimizer step)."""
         st = self._require_train()
         spec = self.spec
@@ -346,7 +351,8 @@ class LoraProjection:
         ops.gemm_lora(dY, self.WT, dX, M=Ttr, Hslots=dH16, h_rows=Ttr, LB=st.AT16, lb_rows=K,
                       tile_slot_ptr=train_plan.tile_slot_ptr, slot_adapter=train_plan.slot_adapter,
                       lora_rank=R, lb_rows_per_adapter=0,
-                      lora_flag=wait[0][1:] if wait else None, gen=wait[1] if wait else None)
+                      lora_flag=wait[0][1:] if wait else None, gen=wait[1] if wait else None,
+                      lora_pdl=pdl)
         return dX
 
     def grad_groups(self, dY: torch.Tensor, cache: ForwardCache, *,

@@ -55,6 +55,8 @@ def _launch(kind: str) -> bool:
     return True
 
 NUM_SMS_DEFAULT = 148
+# timing experiments only: GEMMs ignore the shrink completion flag (results are then undefined)
+_NO_WAIT = __import__("os").environ.get("COLLM_DEBUG_NO_FLAG_WAIT") == "1"
 _sms_cache: dict[int, int] = {}
 
 
@@ -138,10 +140,12 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
               slot_adapter: torch.Tensor | None = None, lora_rank: int = 0,
               lb_rows_per_adapter: int = 0, sub_n_start: list[int] | None = None,
               sub_h_col: list[int] | None = None, bn: int = 0,
-              lora_flag: torch.Tensor | None = None, gen: torch.Tensor | None = None) -> None:
+              lora_flag: torch.Tensor | None = None, gen: torch.Tensor | None = None,
+              lora_pdl: bool = False) -> None:
     """K2/K3: Y[M,N] = A[M,K] . B[N,K]^T (+ fused multi-adapter LoRA expand), bf16 -> bf16.
     ``lora_flag``/``gen``: wait for a concurrently running shrink's signal before the LoRA
-    stages (see collm.h)."""
+    stages (see collm.h); ``lora_pdl``: launch programmatically dependent on the shrink launched
+    just before on the same stream instead (see collm.h)."""
     for t, n in ((A, "A"), (B, "B"), (Y, "Y")):
         _need(t, torch.bfloat16, n)
     M = A.shape[0] if M is None else M
@@ -152,8 +156,9 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
     if not _launch("gemm"):
         return
     lora = tile_slot_ptr is not None
-    if not enabled("shrink"):  # a timing graph without the shrinks: nothing to wait for
+    if not enabled("shrink") or _NO_WAIT:  # a timing graph without the shrinks: nothing to wait for
         lora_flag = gen = None
+        lora_pdl = False
     n_sub = len(sub_n_start) - 1 if (lora and sub_n_start) else 1
     ws = _gemm_ws.get(_lib.load().collm_gemm_workspace_bytes(0), A.device)
     _lib.call(
@@ -165,7 +170,7 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
         _lib.int_array(sub_n_start) if (lora and sub_n_start) else None,
         _lib.int_array(sub_h_col) if (lora and sub_h_col) else None, bn, _p(ws),
         0 if ws is None else ws.numel(), _p(lora_flag) if lora else None,
-        _p(gen) if lora else None, _stream())
+        _p(gen) if lora else None, int(bool(lora_pdl and lora)), _stream())
 
 
 def reduce_tsplit(T: int, n_tiles: int, device: torch.device) -> int:

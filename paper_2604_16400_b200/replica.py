@@ -67,6 +67,10 @@ class ReplicaStack:
         self._graph: torch.cuda.CUDAGraph | None = None
         self._side: torch.cuda.Stream | None = None
         self.overlap = False
+        # how a projection's shrink overlaps its GEMM: "pdl" (default) = same stream, the GEMM
+        # launched programmatically dependent on the shrink (deadlock-free by construction,
+        # 2-3 % faster); "flag" = shrink on the side stream + a device completion flag
+        self.overlap_mode = os.environ.get("COLLM_OVERLAP_MODE", "pdl")
         self._gen: torch.Tensor | None = None
         self._gen_count = 0
         self._sig: torch.Tensor | None = None
@@ -234,9 +238,11 @@ class ReplicaStack:
         _lib.load().collm_set_gemm_lean(1 if overlap else 0)
         n_sig = 0
 
+        pdl = overlap and self.overlap_mode == "pdl"
+
         def signal():
             nonlocal n_sig
-            if not overlap:
+            if not overlap or pdl:
                 return None
             sig = (self._signals(n_sig + 1)[n_sig], self._gen)
             n_sig += 1
@@ -265,6 +271,11 @@ class ReplicaStack:
                 X = a["X"][l] if name in ENTRY else (a["Xo"][syn] if name == "o" else a["Xd"][syn])
                 Y = a["X"][l + 1] if name == "down" else a["Y"][name]
                 sig = signal()
+                if pdl:
+                    cache = proj.forward_lora(X, plan.device, n_train=Ttr)
+                    proj.forward_gemm(cache, plan.device, Y, pdl=True)
+                    caches[l][name] = cache
+                    continue
                 box = {}
                 on_side(lambda: box.setdefault("c", proj.forward_lora(X, plan.device, n_train=Ttr,
                                                                     signal=sig)), prev)
@@ -297,10 +308,17 @@ class ReplicaStack:
                     dX = a["dX_first"][l] if name == first else a["dX"][name]
                     cache = caches[l][name]
                     sig = signal()
-                    on_side(lambda: proj.backward_dh(dY, cache, plan.train_device, signal=sig), prev)
-                    flush_k5()  # the previous layer's K5 queues behind this dH shrink
-                    proj.backward_dx(dY, cache, plan.train_device, dX, wait=sig)
-                    prev = after(main)
+                    if pdl:
+                        proj.backward_dh(dY, cache, plan.train_device)
+                        proj.backward_dx(dY, cache, plan.train_device, dX, pdl=True)
+                        flush_k5()
+                        prev = after(main)
+                    else:
+                        on_side(lambda: proj.backward_dh(dY, cache, plan.train_device, signal=sig),
+                                prev)
+                        flush_k5()  # the previous layer's K5 queues behind this dH shrink
+                        proj.backward_dx(dY, cache, plan.train_device, dX, wait=sig)
+                        prev = after(main)
                     groups += proj.grad_groups(dY, cache, optimizer=opt)
                 pending = (groups, prev)
             flush_k5()
