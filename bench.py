@@ -247,10 +247,19 @@ def run_ours(args, cfg, workload):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py (ours) needs a CUDA device")
+    # test hooks (not used by the driver): run every rank on cuda:0 with gloo, to exercise the
+    # multi-replica path on a one-GPU box
+    one_gpu = os.environ.get("COLLM_BENCH_ONE_GPU") == "1"
+    backend = os.environ.get("COLLM_BENCH_DIST_BACKEND", "nccl")
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _lib.load()
     st_dev = torch.cuda.current_stream()
 
@@ -267,7 +276,11 @@ def run_ours(args, cfg, workload):
         flat_grad = stack.flatten_grads()
 
     def sync_and_apply():
-        dist.all_reduce(flat_grad, op=dist.ReduceOp.AVG)
+        if backend == "nccl":
+            dist.all_reduce(flat_grad, op=dist.ReduceOp.AVG)
+        else:  # gloo has no AVG
+            dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM)
+            flat_grad.div_(world)
         apply_graph.replay()
 
     # eager step sizes the workspaces; then capture
@@ -335,10 +348,11 @@ def run_ours(args, cfg, workload):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights of the named shape; seeded synthetic rows)",
         "config": dict(workload, sync=("none (1 replica): fused AdamW" if fused_opt else
-                                       "NCCL allreduce(avg) of LoRA grads each step + AdamW "
-                                       "apply"),
-                       streams=("GEMMs + LoRA kernels overlapped on two streams" if stack.overlap
-                                else "single stream")),
+                                       f"{backend} allreduce(avg) of the flat LoRA-gradient "
+                                       "buffer each step + AdamW apply kernels"),
+                       streams=(f"overlapped ({stack.overlap_mode}): each shrink || its GEMM's "
+                                "main loop, K5 on a side stream" if stack.overlap
+                                else "single stream, serialized")),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
     }
