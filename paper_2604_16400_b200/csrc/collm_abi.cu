@@ -502,6 +502,8 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   {
     static const bool prologue_pdl = [] { const char* e = getenv("COLLM_GEMM_PDL"); return e && atoi(e) != 0; }();
     p.pdl_mode = (lora && lora_pdl) ? 2 : (prologue_pdl ? 1 : 0);
+    static const bool no_wait = getenv("COLLM_DEBUG_GEMM_NO_LORA_WAIT") != nullptr;
+    p.debug_no_wait = no_wait ? 1 : 0;
   }
   const size_t need = collm_gemm_workspace_bytes(bn);
   CHECK_ARG(workspace && ws_bytes >= need, "gemm workspace too small: %zu < %zu", ws_bytes, need);

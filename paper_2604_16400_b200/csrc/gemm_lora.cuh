@@ -77,6 +77,7 @@ struct GemmLoraParams {
   // prologue (GEMM after GEMM); 2 = only the LoRA stages wait (the previous grid is the shrink
   // producing the LoRA operand, launched just before on the same stream)
   int pdl_mode;
+  int debug_no_wait;  // timing experiments only: skip that wait (results undefined)
   int sched;  // 0 = data-parallel (round-robin tiles), 1 = hybrid data-parallel + stream-K,
               // 2 = debug: stream-K split without fix-up (timing experiments only)
   // ---- stream-K
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
         const bool lora_stage = i >= nk;  // the tile's LoRA k-stages follow its K/64 main blocks
         if (lora_stage && !lora_ready) {
           if (p.pdl_mode == 2) {  // the shrink grid (launched just before) completed + visible
-            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (!p.debug_no_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
             asm volatile("fence.proxy.async.global;" ::: "memory");
           } else {
             wait_lora_flag(p);
