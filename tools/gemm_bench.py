@@ -35,31 +35,36 @@ def main():
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         Ws = [torch.randn(N, K, device="cuda").to(torch.bfloat16) for _ in range(3)]
         Y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        for v in variants:
-            set_variant(v)
+        reps = 30
+
+        def graph_time(fn):
+            """us per launch of fn(i) over `reps` launches replayed from one CUDA graph (no host
+            launch overhead between kernels)."""
             for i in range(3):
-                ops.gemm_lora(A, Ws[i % 3], Y)
+                fn(i)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st), torch.cuda.graph(g, stream=st):
+                for i in range(reps):
+                    fn(i)
+            torch.cuda.current_stream().wait_stream(st)
+            g.replay()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 30
             e0.record()
-            for i in range(reps):
-                ops.gemm_lora(A, Ws[i % 3], Y)
+            g.replay()
             e1.record()
             torch.cuda.synchronize()
-            us = e0.elapsed_time(e1) / reps * 1e3
+            return e0.elapsed_time(e1) / reps * 1e3
+
+        for v in variants:
+            set_variant(v)
+            us = graph_time(lambda i: ops.gemm_lora(A, Ws[i % 3], Y))
             res[(name, v)] = (us, 2 * M * N * K / (us * 1e-6) / 1e12)
         # cuBLAS (torch.matmul) on the same shape, same W rotation (the library baseline)
-        for i in range(3):
-            torch.matmul(A, Ws[i % 3].t(), out=Y)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(30):
-            torch.matmul(A, Ws[i % 3].t(), out=Y)
-        e1.record()
-        torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) / 30 * 1e3
+        us = graph_time(lambda i: torch.matmul(A, Ws[i % 3].t(), out=Y))
         res[(name, "cublas")] = (us, 2 * M * N * K / (us * 1e-6) / 1e12)
     variants = variants + ["cublas"]
     print(f"{'shape':8s} " + " ".join(f"{v:>14s}" for v in variants))
