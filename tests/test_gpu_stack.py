@@ -22,11 +22,12 @@ def _config(cfg_key):
     return cfg
 
 
-def _stack(overlap, cfg_key="tiny", seed=0):
+def _stack(overlap, cfg_key="tiny", seed=0, mode="pdl"):
     from paper_2604_16400_b200.replica import ReplicaStack
     cfg = _config(cfg_key)
     st = ReplicaStack(cfg, "cuda", seed=seed)
     st.overlap = overlap
+    st.overlap_mode = mode
     plan = st.plan(*cfg.batch(0))
     st.allocate(plan, distinct_synthetic=True)
     return st, plan
@@ -140,3 +141,22 @@ def test_stack_backward_matches_oracle():
             # the device dH16 is the bf16 rounding of the oracle's (summation order aside)
             err = np.abs(f(dH16) - dH_ref).max()
             assert err <= 1e-2 * np.abs(dH_ref).max() + 1e-6, f"layer {l} {name} dH: {err}"
+
+
+@pytest.mark.parametrize("cfg_key", ["tiny", "llama2-7b:1"])
+def test_flag_overlap_mode_bitwise(cfg_key):
+    """The two-stream variant of the overlap (shrink on a side stream, the GEMM's LoRA stages
+    wait on a device flag carrying the step generation) gives bitwise the serialized results."""
+    ref, plan = _stack(False, cfg_key)
+    for _ in range(2):
+        ref.run_step(plan)
+    torch.cuda.synchronize()
+    want = _state(ref)
+    del ref
+    fl, plan = _stack(True, cfg_key, mode="flag")
+    fl.run_step(plan)
+    fl.capture(plan)
+    fl.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(want, _state(fl)):
+        assert torch.equal(a, b)
