@@ -11,6 +11,8 @@ from paper_2604_16400_b200 import ops  # noqa: E402
 SHAPES = [("qkv", 1024, 12288, 4096), ("o", 1024, 4096, 4096), ("gate_up", 1024, 22016, 4096),
           ("down", 1024, 4096, 11008), ("dX_qkv", 512, 4096, 12288), ("dX_o", 512, 4096, 4096),
           ("dX_gu", 512, 4096, 22016), ("dX_down", 512, 11008, 4096)]
+if os.environ.get("TINY"):
+    SHAPES = [("t256", 256, 256, 64), ("t256k4k", 256, 256, 4096), ("t512x4kx64", 512, 4096, 64)]
 if os.environ.get("BIG"):
     SHAPES = SHAPES + [("big", 4096, 8192, 8192), ("big2", 8192, 8192, 8192)]
 DEFAULT = "auto,1:256:dp,1:128:dp,1:256:hybrid,2:256:dp,2:128:dp,2:256:hybrid,2:128:hybrid"
