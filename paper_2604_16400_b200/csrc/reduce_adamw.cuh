@@ -227,7 +227,7 @@ struct ReduceSmem {
 };
 
 template <int QT>
-__global__ void __launch_bounds__(kReduceThreads, 3) lora_reduce_kernel(const ReduceParams p) {
+__global__ void __launch_bounds__(kReduceThreads, 4) lora_reduce_kernel(const ReduceParams p) {
   using S = ReduceSmem<QT>;
   constexpr int PT = kReducePT, TC = kReduceTC;
   const int ST = p.stages;
