@@ -105,23 +105,65 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, ui
   return COLLM_OK;
 }
 
-template <int BN, int STAGES, int CG>
-int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& th,
-                const CUtensorMap& tlb, const CUtensorMap& ty, const GemmLoraParams& p, int grid,
-                cudaStream_t stream) {
+template <int BN, int STAGES, int CG, int MC>
+int configure_gemm() {
   using L = GemmSmem<BN, STAGES, CG>;
   static bool configured = false;
   if (!configured) {
-    CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG>,
+    CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG, MC>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
     // the whole unified L1/shared array as shared memory: the SM then has room for a rank-space
     // CTA next to this GEMM CTA (the two-stream overlap); the default carveout is the smallest
     // one that fits the GEMM alone.  (The rank-space kernels keep the default: alone on an SM
     // they profit from L1; next to a GEMM CTA the SM is already configured this way.)
-    CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG>,
+    CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG, MC>,
                                   cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
     configured = true;
+  }
+  return COLLM_OK;
+}
+
+// Clusters of CG*MC CTAs of this variant that can be co-resident (the persistent schedule's
+// flag waits need every CTA resident): 4-CTA clusters must fit inside one GPC.
+template <int BN, int STAGES, int CG, int MC>
+int max_gemm_clusters() {
+  static int n = -1;
+  if (n < 0) {
+    if (configure_gemm<BN, STAGES, CG, MC>()) return 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(num_sms_cached() / (CG * MC) * (CG * MC));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = GemmSmem<BN, STAGES, CG>::kTotal;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG * MC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, gemm_lora_kernel<BN, STAGES, CG, MC>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      c = num_sms_cached() / (CG * MC);
+    }
+    n = c;
+  }
+  return n;
+}
+
+template <int BN, int STAGES, int CG, int MC = 1>
+int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& th,
+                const CUtensorMap& tlb, const CUtensorMap& ty, const GemmLoraParams& p, int grid,
+                cudaStream_t stream) {
+  using L = GemmSmem<BN, STAGES, CG>;
+  int rc = configure_gemm<BN, STAGES, CG, MC>();
+  if (rc) return rc;
+  if (MC > 1) {
+    const int cap = (CG * MC) * max_gemm_clusters<BN, STAGES, CG, MC>();
+    if (grid > cap)
+      return fail(COLLM_EINVAL, "GEMM grid %d exceeds co-resident %d-CTA clusters (%d CTAs)", grid,
+                  CG * MC, cap);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -130,7 +172,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CG * MC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   // PDL (opt-in, COLLM_GEMM_PDL=1): the prologue overlaps the previous grid of the stream (the
@@ -141,7 +183,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = p.pdl_mode ? 2 : 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_lora_kernel<BN, STAGES, CG>, ta, tb, th, tlb, ty, p));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_lora_kernel<BN, STAGES, CG, MC>, ta, tb, th, tlb, ty, p));
   return COLLM_OK;
 }
 
@@ -234,6 +276,7 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
 // Overlap mode (collm_set_gemm_lean): GEMMs run "lean" pipelines and the rank-space kernels are
 // sized and launched to fit next to a GEMM CTA on the same SM.
 static bool g_gemm_lean = false;
+static unsigned long long* g_shrink_dbg = nullptr;  // debug only (COLLM_SHRINK_DEBUG)
 // Shared-memory budget of the K5 reduction: lean = next to a GEMM CTA on the same SM (the
 // two-stream overlap, collm_set_gemm_lean), else up to the full ring depth.
 static bool g_reduce_lean = false;
@@ -300,23 +343,28 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
   cfg.stream = (cudaStream_t)stream;
   p.signal = signal;
   p.gen = gen;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = csize;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  // next to a lean GEMM (the two-stream overlap) ask for the max-shared carveout: an SM this
-  // kernel reaches first must still fit a GEMM CTA; alone, keep the default (more L1)
-  attr[1].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
-  attr[1].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
-  cudaLaunchAttribute* ap = attr;
+  {  // debug only: per-CTA start/end stamps (COLLM_SHRINK_DEBUG), read by collm_shrink_debug_copy
+    static const bool dbg_on = getenv("COLLM_SHRINK_DEBUG") != nullptr;
+    if (dbg_on && !g_shrink_dbg) cudaMalloc(&g_shrink_dbg, 4096 * 16);
+    p.dbg = dbg_on ? g_shrink_dbg : nullptr;
+  }
+  cudaLaunchAttribute attr[3];
   int na = 0;
-  if (csize > 1) ++na;  // no cluster launch unless the K range is split
-  if (g_gemm_lean) {
-    if (na == 0) ap = attr + 1;
+  if (csize > 1) {  // no cluster launch unless the K range is split
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = csize;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  cfg.attrs = ap;
+  if (g_gemm_lean) {
+    // next to a lean GEMM ask for the max-shared carveout: an SM this kernel reaches first must
+    // still fit a GEMM CTA; alone, keep the default (more L1)
+    attr[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+    attr[na].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
+    ++na;
+  }
+  cfg.attrs = attr;
   cfg.numAttrs = na;
   if (max_ranks <= 16)
     CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_kernel<2, 4>, p));
@@ -332,6 +380,11 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
 // ------------------------------------------------------------------------------------ K2/K3
 
 
+int collm_shrink_debug_copy(void* host_dst, size_t bytes) {
+  if (!g_shrink_dbg) return fail(COLLM_EINVAL, "no shrink debug timeline (COLLM_SHRINK_DEBUG)");
+  CUDA_TRY(cudaMemcpy(host_dst, g_shrink_dbg, bytes, cudaMemcpyDeviceToHost));
+  return COLLM_OK;
+}
 // debug-only: device pointer of the last GEMM's timeline (COLLM_GEMM_DEBUG set)
 unsigned long long* collm_debug_timeline = nullptr;
 // debug-only: total ns / count of LoRA-operand flag waits since the last call (COLLM_GEMM_DEBUG)
@@ -385,20 +438,27 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   // 256x256: 0.43, CTA-pair 256x128: 0.34 — times the k-blocks on the critical path;
   // data-parallel: waves x k-blocks; hybrid stream-K: (full waves - 1) data-parallel + the rest
   // split evenly, plus a fix-up of ~12 + 8 x (parts per split tile) µs.
-  struct Cand { int cg, bn, sched; double cost; };
+  // MC = 2: split-2 in 4-CTA clusters — the two pairs halving a tile's K swap their partials
+  // through distributed shared memory (~1.5 us) instead of global memory + flags (~4 us); needs
+  // every tile's cluster co-resident (tiles <= co-resident 4-CTA clusters, 33 on B200).
+  struct Cand { int cg, mc, bn, sched; double cost; };
   auto env_int = [](const char* k, int d) { const char* e = getenv(k); return e ? atoi(e) : d; };
   const int force_cg = env_int("COLLM_GEMM_CG", 0), force_bn = env_int("COLLM_GEMM_BN", bn);
+  const int force_mc = env_int("COLLM_GEMM_MC", 0);
   const char* sched_env = getenv("COLLM_GEMM_SCHED");
   const int force_sched = !sched_env ? -1 : strcmp(sched_env, "dp") == 0 ? 0
                           : strcmp(sched_env, "hybrid") == 0 ? 1 : strcmp(sched_env, "sknofix") == 0 ? 2
                           : strcmp(sched_env, "noload") == 0 ? 3
                           : strcmp(sched_env, "split2") == 0 ? 4 : -1;
-  Cand best{0, 0, 0, 1e30};
+  Cand best{0, 0, 0, 0, 1e30};
   const double nk = (K + kGemmBK - 1) / kGemmBK;
   int force_sched_eff = force_sched;
   for (int attempt = 0; attempt < 2 && best.cg == 0; ++attempt, force_sched_eff = -1)
-  for (int cg : {2, 1}) {
+  for (int cg : {2, 1})
+  for (int mc : {1, 2}) {
     if (force_cg && cg != force_cg) continue;
+    if (mc == 2 && cg != 2) continue;
+    if (force_mc && mc != force_mc && attempt == 0) continue;  // retry: any, like the schedule
     const long long units = sms / cg;
     const long long nmu = (M + kGemmBM * cg - 1) / (kGemmBM * cg);
     for (int b : {256, 128}) {
@@ -413,7 +473,12 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
           // split-2: every tile's K halved over two units that swap half-tile partials (2-CTA
           // pairs only, needs 2 x tiles <= units); calibrated swap cost ~4 us
           if (cg != 2 || 2 * tiles > units || nk < 2) continue;  // both halves non-empty
-          cost = std::ceil(nk / 2.0) * kb + 4.0;
+          if (mc == 2 && tiles > (b == 256 ? max_gemm_clusters<256, 6, 2, 2>()
+                                           : max_gemm_clusters<128, 8, 2, 2>()))
+            continue;
+          cost = std::ceil(nk / 2.0) * kb + (mc == 2 ? 1.5 : 4.0);
+        } else if (mc == 2) {
+          continue;  // 4-CTA clusters only for split-2
         } else if (sc == 0) {
           cost = (double)((tiles + units - 1) / units) * nk * kb;
         } else {
@@ -423,12 +488,12 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
           const double parts = std::min(3.0, std::max(1.0, (double)units / sk_tiles));
           cost = dp_waves * nk * kb + (double)sk_tiles * nk * kb / units + 12.0 + 8.0 * parts;
         }
-        if (cost < best.cost) best = {cg, b, sc, cost};
+        if (cost < best.cost) best = {cg, mc, b, sc, cost};
       }
     }
   }
   if (best.cg == 0) return fail(COLLM_EINVAL, "no GEMM tile fits (sub-projection boundaries must be x128)");
-  const int cg = best.cg;
+  const int cg = best.cg, mc = best.mc;
   bn = best.bn;
   const int sched = (force_sched == 2 || force_sched == 3) ? force_sched : best.sched;
   const int nm = (M + kGemmBM * cg - 1) / (kGemmBM * cg);
@@ -511,8 +576,14 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   {
     static unsigned long long* dbg_ptr = nullptr;
     const char* dbg_env = getenv("COLLM_GEMM_DEBUG");
-    if (dbg_env && !dbg_ptr) cudaMalloc(&dbg_ptr, 256 * 32 * 8);
-    if (dbg_env) cudaMemsetAsync(dbg_ptr, 0, 256 * 32 * 8, (cudaStream_t)stream);
+    if (dbg_env && !dbg_ptr) {
+      cudaMalloc(&dbg_ptr, 256 * 32 * 8);
+      fprintf(stderr, "collm: co-resident GEMM clusters: pairs %d, 4-CTA %d (lean %d)\n",
+              max_gemm_clusters<256, 6, 2, 1>(), max_gemm_clusters<256, 6, 2, 2>(),
+              max_gemm_clusters<256, 5, 2, 2>());
+    }
+    // (COLLM_GEMM_DEBUG=2: no memset node, which would break a programmatic launch overlap)
+    if (dbg_env && atoi(dbg_env) != 2) cudaMemsetAsync(dbg_ptr, 0, 256 * 32 * 8, (cudaStream_t)stream);
     p.dbg = dbg_env ? dbg_ptr : nullptr;
     collm_debug_timeline = p.dbg;
   }
@@ -522,6 +593,14 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   // LoRA kernels running concurrently on a second stream (collm_set_gemm_lean / COLLM_GEMM_LEAN)
   const char* lean_env = getenv("COLLM_GEMM_LEAN");
   const bool lean = lean_env ? atoi(lean_env) != 0 : g_gemm_lean;
+  if (mc == 2) {
+    if (lean) {
+      if (bn == 256) return launch_gemm<256, 5, 2, 2>(ta, tb, th, tlb, ty, p, grid, st);
+      return launch_gemm<128, 6, 2, 2>(ta, tb, th, tlb, ty, p, grid, st);
+    }
+    if (bn == 256) return launch_gemm<256, 6, 2, 2>(ta, tb, th, tlb, ty, p, grid, st);
+    return launch_gemm<128, 8, 2, 2>(ta, tb, th, tlb, ty, p, grid, st);
+  }
   if (cg == 2) {
     if (lean) {
       static const int lean_stages = [] { const char* e = getenv("COLLM_GEMM_LEAN_STAGES"); return e ? atoi(e) : 5; }();
@@ -554,16 +633,20 @@ int collm_preload(void) {
   COLLM_PRELOAD((lora_shrink_kernel<4, 3>));
   COLLM_PRELOAD((lora_shrink_kernel<6, 2>));
   COLLM_PRELOAD((lora_shrink_kernel<8, 2>));
-  COLLM_PRELOAD((gemm_lora_kernel<256, 6, 2>));
-  COLLM_PRELOAD((gemm_lora_kernel<128, 8, 2>));
-  COLLM_PRELOAD((gemm_lora_kernel<256, 5, 2>));
-  COLLM_PRELOAD((gemm_lora_kernel<128, 6, 2>));
-  COLLM_PRELOAD((gemm_lora_kernel<256, 4, 2>));
-  COLLM_PRELOAD((gemm_lora_kernel<128, 5, 2>));
-  COLLM_PRELOAD((gemm_lora_kernel<256, 4, 1>));
-  COLLM_PRELOAD((gemm_lora_kernel<128, 6, 1>));
-  COLLM_PRELOAD((gemm_lora_kernel<256, 3, 1>));
-  COLLM_PRELOAD((gemm_lora_kernel<128, 4, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 6, 2, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 8, 2, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 5, 2, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 6, 2, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 4, 2, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 5, 2, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 6, 2, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 8, 2, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 5, 2, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 6, 2, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 4, 1, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 6, 1, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 3, 1, 1>));
+  COLLM_PRELOAD((gemm_lora_kernel<128, 4, 1, 1>));
   COLLM_PRELOAD(lora_reduce_kernel<16>);
   COLLM_PRELOAD(lora_reduce_kernel<32>);
   COLLM_PRELOAD(lora_reduce_kernel<48>);

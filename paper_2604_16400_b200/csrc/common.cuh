@@ -154,6 +154,16 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorM
       : "memory");
 }
 
+// Bulk copy from this CTA's shared memory into another CTA's (cluster addresses of the
+// destination and of its mbarrier, which receives the byte count).
+__device__ __forceinline__ void bulk_copy_s2cluster(uint32_t dst_cluster, const void* src,
+                                                    uint32_t bytes, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst_cluster), "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05 / TMEM
 template <uint32_t kCols, int CG = 1>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
@@ -209,6 +219,14 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(smem_u32(bar)),
       "h"((uint16_t)3)
+      : "memory");
+}
+// cta_group::2 commit arriving on `bar`'s offset in every CTA of the cluster mask
+__device__ __forceinline__ void umma_commit_pair_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 // Arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete.

@@ -250,7 +250,7 @@ struct StreamK {
   }
 };
 
-template <int BN, int STAGES, int CG>
+template <int BN, int STAGES, int CG, int MC>
 __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can co-reside
     gemm_lora_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmLB,
@@ -266,14 +266,23 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* fixbar = tempty + 2;  // stream-K fix-up ring: one barrier per 16 KB slot
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixbar + 16);
+  uint64_t* xfree = fixbar + 16;  // cluster split-2: the partner's smem may receive ours
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixbar + 17);
   int32_t* s_prefix = reinterpret_cast<int32_t*>(smem + L::kPrefixOffset);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const bool has_lora = p.tile_slot_ptr != nullptr;
   const int nk = (p.K + BK - 1) / BK;
-  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;
+  // MC == 2 (split-2 only): a cluster of the two CTA pairs computing the two K halves of one
+  // tile, which swap their half-tile partials through distributed shared memory
+  constexpr int CL = CG * MC;  // CTAs per cluster
+  static_assert(MC == 1 || CG == 2, "split-2 clusters are built from CTA pairs");
+  const uint32_t crank = (CL > 1) ? cluster_ctarank() : 0;
+  const uint32_t rank = (CG == 2) ? (crank & 1u) : 0;  // position in the pair
+  const uint32_t q = crank >> 1;                        // pair within the cluster (MC == 2)
+  const uint32_t leader_rank = crank & ~1u;             // this pair's MMA issuer
+  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * q));
   const bool leader = rank == 0;
 
   // LoRA stages of a (128*CG)-row unit: the slot list of the 256-row slot tile containing it
@@ -324,7 +333,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4 * CG);
     }
-    for (int k = 0; k < 16; ++k) mbar_init(&fixbar[k], 1);
+    for (int k = 0; k < 17; ++k) mbar_init(&fixbar[k], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<L::kTmemCols, CG>(tmem_slot);
@@ -371,6 +380,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
           if (p.pdl_mode == 2) {  // the shrink grid (launched just before) completed + visible
             if (!p.debug_no_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
             asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (p.dbg) p.dbg[(size_t)blockIdx.x * 32 + 20] = gtimer();
           } else {
             wait_lora_flag(p);
           }
@@ -388,6 +398,8 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
           continue;
         }
         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * CG);
+        if (p.dbg && i == sg.k0 && p.dbg[(size_t)blockIdx.x * 32 + 15] == 0)
+          p.dbg[(size_t)blockIdx.x * 32 + 15] = gtimer();
         if (lora_stage) {
           for (int j = 0; j < n_it; ++j) {
             const int s = p.tile_slot_ptr[st_tile] + (it0 + j) / p.lora_chunks;
@@ -396,7 +408,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
             uint8_t* da = sa + j * (BM * rc * 2);
             uint8_t* db = sa + L::kABytes + j * (L::kBRows * rc * 2);
             if constexpr (CG == 2) {
-              const uint32_t fb = mapa_shared(&full[stage], 0);
+              const uint32_t fb = mapa_shared(&full[stage], leader_rank);
               tma_load_2d_pair(da, &tmH, fb, hcol + c * rc, s * kSlotTileM + hrow0);
               tma_load_2d_pair(db, &tmLB, fb, c * rc, lb_row);
             } else {
@@ -407,7 +419,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
         } else {
           const int kb = i;
           if constexpr (CG == 2) {
-            const uint32_t fb = mapa_shared(&full[stage], 0);
+            const uint32_t fb = mapa_shared(&full[stage], leader_rank);
             tma_load_2d_pair(sa, &tmA, fb, kb * BK, m0);
             tma_load_2d_pair(sa + L::kABytes, &tmB, fb, kb * BK, nb0);
           } else {
@@ -427,12 +439,17 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
     uint32_t acc = 0, acc_phase = 0;
     const uint32_t smem_base = smem_u32(smem);
     const uint32_t lrow = p.lora_rc * 2, lsteps = p.lora_rc / 16;
+    // debug timeline (COLLM_GEMM_DEBUG): [4] first stage ready, [8] 32nd stage, [12] last issue
+    unsigned long long* mdbg = p.dbg ? p.dbg + (size_t)blockIdx.x * 32 : nullptr;
+    int kbi = 0;
     auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
       if constexpr (CG == 2) umma_bf16_pair(d, a, b, idesc, accumulate);
       else umma_bf16(d, a, b, idesc, accumulate);
     };
-    auto commit = [&](uint64_t* bar) {
-      if constexpr (CG == 2) umma_commit_pair(bar); else umma_commit(bar);
+    auto commit = [&](uint64_t* bar) {  // both CTAs of this pair
+      if constexpr (MC == 2) umma_commit_pair_mask(bar, pair_mask);
+      else if constexpr (CG == 2) umma_commit_pair(bar);
+      else umma_commit(bar);
     };
     sk.for_each(unit, [&](const Segment& sg) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -442,6 +459,11 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
       for (int i = sg.k0; i < sg.k1; ++i) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (mdbg && lane == 0) {
+          if (kbi == 0) mdbg[4] = gtimer();
+          else if (kbi == 32) mdbg[8] = gtimer();
+        }
+        ++kbi;
         const uint32_t sa = smem_base + stage * L::kStageBytes;
         if (i >= nk) {  // LoRA expand k-stage: (Hslots chunk x adapter B chunk) per item
           const int it0 = (i - nk) * p.lora_per_stage;
@@ -467,6 +489,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
         accumulate = 1;
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (mdbg && lane == 0) mdbg[12] = gtimer();
       if (elect_one()) commit(&tfull[acc]);
       __syncwarp();
       acc ^= 1;
@@ -570,6 +593,73 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
         constexpr int NCH = BN / 32;
         const int half = unit & 1;
         const int own_lo = half ? NCH / 2 : 0, own_hi = half ? NCH : NCH / 2;
+        if constexpr (MC == 2) {
+          // cluster split-2: the two halves are the two pairs of this cluster.  Each of the other
+          // half's 32-column chunks goes TMEM -> this CTA's idle pipeline smem (16 KB piece,
+          // float4 index j * 128 + tid) -> a DSMEM bulk copy into the partner CTA (same position,
+          // other pair; once it reports its smem idle), completing on the partner's piece
+          // barrier; the partner adds piece i to its own chunk i as soon as it lands.  No global
+          // memory, no gpu-scope fences.
+          constexpr uint32_t kPiece = BM * 32 * 4, kX = kPiece * (NCH / 2);
+          static_assert(2 * kX <= STAGES * L::kStageBytes, "split-2 exchange exceeds the pipeline smem");
+          uint64_t* xr = fixbar;  // one barrier per incoming piece (the stream-K ring is unused)
+          const uint32_t peer = crank ^ 2u;
+          if (tid == 0) {
+            for (int i = 0; i < NCH / 2; ++i) mbar_arrive_expect_tx(&xr[i], kPiece);
+            mbar_arrive_cluster(mapa_shared(xfree, peer));  // our pipeline smem is idle
+          }
+          int lc = 0;
+#pragma unroll 1
+          for (int chunk = 0; chunk < NCH; ++chunk) {
+            if (chunk >= own_lo && chunk < own_hi) continue;
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + chunk * 32, r);
+            tmem_wait_ld();
+            float4* s_out = reinterpret_cast<float4*>(smem + lc * kPiece) + tid;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              s_out[j * 128] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                           __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            fence_proxy_async_smem();  // generic smem writes -> the bulk copy (async proxy)
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (tid == 0) {
+              if (lc == 0) {
+                if (dbg) dbg[16] = gtimer();
+                mbar_wait(xfree, 0);
+                if (dbg) dbg[17] = gtimer();
+              }
+              bulk_copy_s2cluster(mapa_shared(smem + kX + lc * kPiece, peer), smem + lc * kPiece,
+                                  kPiece, mapa_shared(&xr[lc], peer));
+            }
+            ++lc;
+          }
+#pragma unroll 1
+          for (int chunk = own_lo; chunk < own_hi; ++chunk) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + chunk * 32, r);
+            tmem_wait_ld();
+            mbar_wait(&xr[chunk - own_lo], 0);
+            if (dbg && tid == 0 && chunk == own_lo) dbg[18] = gtimer();
+            const float4* src = reinterpret_cast<const float4*>(smem + kX + (chunk - own_lo) * kPiece) + tid;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 v = src[j * 128];
+              r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + v.x);
+              r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + v.y);
+              r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + v.z);
+              r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
+            }
+            store_chunk(r, chunk * 32);
+          }
+          if (dbg && tid == 0) dbg[19] = gtimer();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(&tempty[acc], leader_rank));
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+          ++seg_i;
+          return;
+        }
         const int partner = sg.c_first * CG + (int)rank;
 #pragma unroll 1
         for (int chunk = 0; chunk < NCH; ++chunk) {
@@ -583,8 +673,10 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
                    make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
         }
+        if (dbg && tid == 0) dbg[16] = gtimer();
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (dbg && tid == 0) dbg[17] = gtimer();
         if (tid == 0) {
           asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.flags + cta), "r"(1u) : "memory");
           const int32_t* f = p.flags + partner;
@@ -598,6 +690,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
             }
           } while (v == 0);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk reads
+          if (dbg) dbg[18] = gtimer();
           for (int chunk = own_lo; chunk < own_hi; ++chunk) {  // one ring slot per own chunk
             const int slot = chunk - own_lo;
             mbar_arrive_expect_tx(&fixbar[slot], L::kFixPiece);
@@ -613,6 +706,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
           tmem_wait_ld();
           const int slot = chunk - own_lo;
           mbar_wait(&fixbar[slot], 0);
+          if (dbg && tid == 0) dbg[19 + slot] = gtimer();
           const float4* src = reinterpret_cast<const float4*>(smem + slot * L::kFixPiece) + tid;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -627,7 +721,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+          if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(&tempty[acc], leader_rank));
           else mbar_arrive(&tempty[acc]);
         }
         acc ^= 1;
@@ -680,7 +774,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(&tempty[acc], leader_rank));
         else mbar_arrive(&tempty[acc]);
       }
       acc ^= 1;

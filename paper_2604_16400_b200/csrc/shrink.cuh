@@ -60,11 +60,17 @@ struct ShrinkParams {
   // signal[0] = arrival counter (0 on entry, restored), signal[1] <- *gen once all is written
   int32_t* signal;
   const int32_t* gen;
+  unsigned long long* dbg;  // debug only: [CTA][2] globaltimer at start / end
 };
 
 // Every CTA arrives once its outputs are written; the last one publishes *gen in signal[1]
 // (release, gpu scope) for the GEMM waiting on it (wait_lora_flag in gemm_lora.cuh).
 __device__ __forceinline__ void shrink_signal_done(const ShrinkParams& p) {
+  if (p.dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    p.dbg[2 * (blockIdx.y * gridDim.x + blockIdx.x) + 1] = t;
+  }
   if (!p.signal) return;
   __syncthreads();  // this CTA's stores happen-before thread 0's cumulative fence
   if (threadIdx.x == 0) {
@@ -122,6 +128,11 @@ __global__ void __launch_bounds__(kShrinkWarps * 32, 3)
   // a GEMM launched programmatically dependent on this shrink (same stream, pdl_mode 2) may
   // start right away: its main loop overlaps this grid, its LoRA stages wait for our completion
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    p.dbg[2 * (blockIdx.y * gridDim.x + blockIdx.x)] = t;
+  }
   constexpr int W2 = kShrinkWarps / 2;
   constexpr int LD = 8 * NT + 1;
   __shared__ float red[W2][16][LD];

@@ -156,6 +156,8 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
     if not _launch("gemm"):
         return
     lora = tile_slot_ptr is not None
+    if _filter.kinds is not None and "nolora" in _filter.kinds:  # timing only: base GEMM alone
+        lora = False
     if not enabled("shrink") or _NO_WAIT:  # a timing graph without the shrinks: nothing to wait for
         lora_flag = gen = None
         lora_pdl = False
@@ -166,7 +168,8 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
         Y.stride(0), M, N, K,
         _p(Hslots) if lora else None, Hslots.stride(0) if lora else 0, h_rows,
         _p(LB) if lora else None, LB.stride(-2) if lora else 0, lb_rows,
-        _p(tile_slot_ptr), _p(slot_adapter), lora_rank, lb_rows_per_adapter, n_sub,
+        _p(tile_slot_ptr) if lora else None, _p(slot_adapter) if lora else None, lora_rank,
+        lb_rows_per_adapter, n_sub,
         _lib.int_array(sub_n_start) if (lora and sub_n_start) else None,
         _lib.int_array(sub_h_col) if (lora and sub_h_col) else None, bn, _p(ws),
         0 if ws is None else ws.numel(), _p(lora_flag) if lora else None,

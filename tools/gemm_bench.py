@@ -19,15 +19,17 @@ DEFAULT = "auto,1:256:dp,1:128:dp,1:256:hybrid,2:256:dp,2:128:dp,2:256:hybrid,2:
 
 
 def set_variant(v):
-    for k in ("COLLM_GEMM_CG", "COLLM_GEMM_BN", "COLLM_GEMM_SCHED"):
+    for k in ("COLLM_GEMM_CG", "COLLM_GEMM_BN", "COLLM_GEMM_SCHED", "COLLM_GEMM_MC"):
         os.environ.pop(k, None)
     os.environ.pop("COLLM_GEMM_LEAN", None)
     if v.endswith("+lean"):
         os.environ["COLLM_GEMM_LEAN"] = "1"
         v = v[:-5]
     if v != "auto":
-        cg, bn, sc = v.split(":")
+        cg, bn, sc, *mc = v.split(":")
         os.environ.update(COLLM_GEMM_CG=cg, COLLM_GEMM_BN=bn, COLLM_GEMM_SCHED=sc)
+        if mc:
+            os.environ["COLLM_GEMM_MC"] = mc[0]
 
 
 def main():

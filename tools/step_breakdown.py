@@ -18,7 +18,8 @@ plan = st.plan(*cfg.batch(0))
 st.allocate(plan)
 st.run_step(plan)
 torch.cuda.synchronize()
-variants = [("full", None), ("gemm only", ("gemm", "plan")), ("gemm+shrink", ("gemm", "plan", "shrink")),
+variants = [("full", None), ("gemm only", ("gemm", "plan")),
+            ("base gemm", ("gemm", "plan", "nolora")), ("gemm+shrink", ("gemm", "plan", "shrink")),
             ("gemm+reduce", ("gemm", "plan", "reduce")), ("lora only", ("plan", "lora"))]
 graphs = {}
 for name, kinds in variants:
