@@ -47,6 +47,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--no-lm-head", action="store_true",
+                    help="skip the separate LM-head + CE (K7) measurement")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph (debug)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="run the LoRA kernels on the GEMM stream (no side-stream overlap)")
@@ -403,6 +405,51 @@ def run_ours(args, cfg, workload):
             "algorithmic_bytes_per_step": lb["total"], "lora_ms_per_step": lora_ms,
             "share_of_step": lora_ms / ms_max, "peak_source": f"{peaks_src} hbm_gbs"}
         del gg, gl
+
+    # ---------------- the LM head of the training rows (K2 logits + K7 CE + K3 dX), timed apart:
+    # the training-loss path; not part of the LoRA-stack tokens/s metric
+    if not args.no_lm_head and use_graph and Ttr and world == 1:
+        from paper_2604_16400_b200 import layer as _layer
+        V, h = cfg.model.vocab, cfg.model.hidden
+        head = _layer.LMHead(h, V, dev)
+        gh = torch.Generator(device=dev)
+        gh.manual_seed(args.seed + 11)
+        head.W.normal_(0.0, 0.02, generator=gh)
+        head.refresh_transpose()
+        Xt = stack._acts["X"][cfg.model.layers][:Ttr]
+        labels = torch.randint(0, V, (Ttr,), device=dev, generator=gh, dtype=torch.int32)
+        dXt = torch.empty(Ttr, h, dtype=torch.bfloat16, device=dev)
+        loss = head.forward_backward(Xt, labels, dXt)
+        torch.cuda.synchronize()
+        hb = head._buffers(Ttr)
+        ghead, gce = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(st_dev)
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(ghead, stream=s):
+                head.forward_backward(Xt, labels, dXt)
+            with torch.cuda.graph(gce, stream=s):
+                ops.cross_entropy(hb["logits"], labels, V, loss_rows=hb["loss_rows"],
+                                  loss_mean=hb["loss"], counter=hb["counter"],
+                                  dlogits=hb["dlogits"], grad_scale=1.0 / Ttr)
+        st_dev.wait_stream(s)
+        ghead.replay()
+        gce.replay()
+        reps = max(3, min(20, args.steps))
+        head_ms = timed(ghead.replay, reps, st_dev)
+        ce_ms = timed(gce.replay, reps, st_dev)
+        ce_bytes = 4 * Ttr * V + 8 * Ttr  # logits read once + dlogits written (bf16), labels/loss
+        hflops = 2 * 2 * Ttr * V * h
+        out["lm_head"] = {
+            "what": "frozen LM head on the training rows: logits GEMM + K7 softmax-CE fwd/bwd + "
+                    "dX GEMM (the real training loss and the top layer's dY); timed apart, not "
+                    "in the tokens/s metric",
+            "rows": Ttr, "vocab": V, "ms": head_ms, "loss": float(loss.item()),
+            "gemm_tflops": hflops / ((head_ms - ce_ms) / 1e3) / 1e12,
+            "ce_kernel": {"us": ce_ms * 1e3, "algorithmic_bytes": ce_bytes,
+                          "achieved_gbs": ce_bytes / (ce_ms / 1e3) / 1e9,
+                          "frac_hbm": ce_bytes / (ce_ms / 1e3) / 1e9 / peaks.get("hbm_gbs", 1)}}
+        del ghead, gce, head
 
     # ---------------- e2e: host buffers, copies inside the timed region
     if not args.no_e2e and use_graph:

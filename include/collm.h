@@ -13,6 +13,7 @@
  *   fedavg                       launcher.py:68-80 -> NCCL allreduce(avg) + collm_lora_apply(COPY)
  *   domain.Batch / pop_up_to     domain.py:64-86, dispatcher.py:66-82
  *                                                  -> collm_plan_segments + collm_expand_segments
+ *   TrainState.loss / train_step perf.py:92-126    -> collm_cross_entropy (real LM-head loss)
  *
  * Conventions: plain C types, device pointers for tensors (bf16 = 2-byte bfloat16, row-major,
  * leading dimensions in ELEMENTS), `stream` is a cudaStream_t passed as void*.  All launches are
@@ -164,6 +165,20 @@ int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int
  * fedavg's result hand-back, launcher.py:68-80 / :226). */
 int collm_lora_apply(const collm_reduce_group* groups, int n_groups, int mode,
                      const float* adamw, void* stream);
+
+/* ---- K7: softmax cross-entropy forward + backward over LM-head logits ------------------------
+ * For each row t of logits [T, ld] (bf16, V used columns, V and ld multiples of 8):
+ *   loss_rows[t] = logsumexp(z_t) - z_t[labels[t]]  (0 when labels[t] < 0 or >= V: ignored)
+ *   dlogits[t, v] = grad_scale * (softmax(z_t)[v] - [v == labels[t]])  (bf16; 0 for ignored rows;
+ *                   dlogits may be NULL = forward only; it must not alias logits)
+ *   *loss_mean = mean of loss_rows over the valid rows, summed in row order by the last CTA
+ *                (loss_mean may be NULL; otherwise `counter` = 1 device int32, zeroed once,
+ *                restored by the kernel).  fp32 softmax arithmetic, deterministic.
+ * Replaces: the convergence stand-in perf.train_step (perf.py:111-126) — TrainState.loss becomes
+ * the measured next-token cross-entropy of the training rows. */
+int collm_cross_entropy(const void* logits, int ld, int T, int V, const int32_t* labels,
+                        float* loss_rows, float* loss_mean, int32_t* counter, void* dlogits,
+                        int ld_d, float grad_scale, void* stream);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ import numpy as np
 __all__ = [
     "bf16_round", "bf16_to_bits", "bits_to_f32", "build_rows", "expand_segments", "tile_slots",
     "slot_of_row", "shrink_tiles", "lora_forward", "lora_backward", "adamw_step", "AdamWState",
-    "fedavg", "AggregationError", "projection_flops",
+    "fedavg", "AggregationError", "projection_flops", "cross_entropy",
 ]
 
 
@@ -211,6 +211,32 @@ def adamw_step(p, g, st: AdamWState, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, 
     denom = np.sqrt(st.v) / np.float32(math.sqrt(bc2)) + np.float32(eps)
     p -= np.float32(lr / bc1) * st.m / denom
     return p
+
+
+# --------------------------------------------------------------------------- LM-head CE (K7)
+def cross_entropy(logits, labels, grad_scale=None):
+    """Next-token softmax cross-entropy of the training rows — the real loss behind the
+    reference's convergence stand-in (perf.py:92-126: TrainState.loss / train_step); the paper's
+    fine-tuning uses the HF Trainer's causal-LM loss.  ``logits`` [T, V] (the bf16
+    GEMM output, as float), ``labels`` [T] int (< 0 or >= V: ignored row).  Returns float64
+    (loss_rows [T], mean over valid rows, dlogits [T, V] = grad_scale * (softmax - onehot), zero
+    for ignored rows; grad_scale defaults to 1 / #valid, the gradient of the mean)."""
+    z = np.asarray(logits, dtype=np.float64)
+    y = np.asarray(labels).astype(np.int64)
+    T, V = z.shape
+    valid = (y >= 0) & (y < V)
+    m = z.max(axis=1, keepdims=True)
+    lse = (m + np.log(np.exp(z - m).sum(axis=1, keepdims=True)))[:, 0]
+    picked = np.where(valid, z[np.arange(T), np.clip(y, 0, V - 1)], 0.0)
+    loss_rows = np.where(valid, lse - picked, 0.0)
+    n = int(valid.sum())
+    mean = loss_rows[valid].sum() / n if n else 0.0
+    g = (1.0 / max(n, 1)) if grad_scale is None else grad_scale
+    d = np.exp(z - lse[:, None])
+    d[np.arange(T)[valid], y[valid]] -= 1.0
+    d *= g
+    d[~valid] = 0.0
+    return loss_rows, mean, d
 
 
 # --------------------------------------------------------------------------- FedAvg

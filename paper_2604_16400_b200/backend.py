@@ -93,10 +93,56 @@ class MeasuredLatencyBackend:
         return self._measure(cfg.train_batch, cfg.infer_batch, train=True)
 
 
+@dataclass
+class RealTrainingBackend(MeasuredLatencyBackend):
+    """Also replaces the convergence stand-in ``train_step`` (perf.py:111-126, called at
+    engine.py:395): every call runs a real co-batched training step (B sequences of the trainable
+    adapter, LM head + next-token CE, fused AdamW) and returns the reference's ``TrainState`` with
+    the MEASURED loss — ``last_decrement`` = previous loss - new loss, so the coordinator's
+    record_decrement / record_noise_scale (engine.py:396-397) consume real training signal;
+    ``noise_scale`` keeps the reference's own definition on top of the real loss."""
+
+    optimizer: object = None    # layer.AdamWConfig (None: its defaults)
+    _train_stack: object = None
+    _train_plans: dict = field(default_factory=dict)
+
+    def _trainer(self):
+        if self._train_stack is None:
+            from .replica import ReplicaStack
+            self._train_stack = ReplicaStack(self.cfg, self.device, seed=self.seed,
+                                             optimizer=self.optimizer, lm_head=True)
+        return self._train_stack
+
+    def train_step(self, state, batch: int, rng=None):
+        import dataclasses
+
+        from .domain import TrainItem
+        if batch < 1:
+            raise ConfigurationError("training batch must be >= 1")
+        st = self._trainer()
+        if batch not in self._train_plans:
+            plan = st.plan(TrainItem(self.cfg.train_adapter, batch, self.cfg.train_seq), [])
+            st.allocate(plan, distinct_synthetic=False)
+            self._train_plans[batch] = plan
+        plan = self._train_plans[batch]
+        if st._plan is not plan:
+            st.allocate(plan, distinct_synthetic=False)
+        st.run_step(plan, optimizer_step=True)
+        loss = st.last_loss()
+        if state.steps == 0:  # the stand-in's initial loss is a guess: anchor it to the real one
+            return dataclasses.replace(state, loss=loss, initial_loss=loss, steps=1,
+                                       last_decrement=0.0)
+        return dataclasses.replace(state, loss=loss, steps=state.steps + 1,
+                                   last_decrement=state.loss - loss)
+
+
 @contextlib.contextmanager
 def install(engine_module, backend):
-    """Rebind the engine module's imported latency functions to ``backend`` for the block."""
-    names = ("true_infer_latency", "true_train_latency")
+    """Rebind the engine module's imported latency functions (and, when the backend provides
+    it, ``train_step``) to ``backend`` for the block."""
+    names = ["true_infer_latency", "true_train_latency"]
+    if hasattr(backend, "train_step"):
+        names.append("train_step")
     saved = {n: getattr(engine_module, n) for n in names}
     try:
         for n in names:

@@ -23,6 +23,7 @@ class ModelShape:
     hidden: int
     intermediate: int
     kv_dim: int
+    vocab: int = 32000  # LM head (K7 training loss)
 
     def projections(self, rank: int, alpha: float, fuse: bool = True) -> list[ProjectionSpec]:
         """Per-layer projections.  q|k|v and gate|up are fused into one GEMM when their boundaries
@@ -49,10 +50,10 @@ class ModelShape:
         return per_layer * self.layers
 
 
-TINY = ModelShape("tiny-llama", 2, 256, 688, 256)
-LLAMA2_7B = ModelShape("llama-2-7b", 32, 4096, 11008, 4096)
-LLAMA3_8B = ModelShape("llama-3-8b", 32, 4096, 14336, 1024)
-LLAMA2_13B = ModelShape("llama-2-13b", 40, 5120, 13824, 5120)
+TINY = ModelShape("tiny-llama", 2, 256, 688, 256, 512)
+LLAMA2_7B = ModelShape("llama-2-7b", 32, 4096, 11008, 4096, 32000)
+LLAMA3_8B = ModelShape("llama-3-8b", 32, 4096, 14336, 1024, 128256)
+LLAMA2_13B = ModelShape("llama-2-13b", 40, 5120, 13824, 5120, 32000)
 
 
 @dataclass(frozen=True)

@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "gemm_lora.cuh"
 #include "reduce_adamw.cuh"
+#include "ce.cuh"
 #include "segments.cuh"
 #include "shrink.cuh"
 
@@ -651,6 +652,8 @@ int collm_preload(void) {
   COLLM_PRELOAD(lora_reduce_kernel<32>);
   COLLM_PRELOAD(lora_reduce_kernel<48>);
   COLLM_PRELOAD(lora_apply_kernel);
+  COLLM_PRELOAD((cross_entropy_kernel<8, 512>));
+  COLLM_PRELOAD((cross_entropy_kernel<0, 256>));
 #undef COLLM_PRELOAD
   return COLLM_OK;
 }
@@ -844,6 +847,39 @@ int collm_lora_apply(const collm_reduce_group* groups, int n_groups, int mode,
   for (int g = 0; g < n_groups; ++g) total += (long long)p.groups[g].P * p.groups[g].Q;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 4LL * num_sms_cached());
   lora_apply_kernel<<<std::max(blocks, 1), 256, 0, (cudaStream_t)stream>>>(p, total);
+  CUDA_TRY(cudaGetLastError());
+  return COLLM_OK;
+}
+
+// ------------------------------------------------------------------------------------ K7
+int collm_cross_entropy(const void* logits, int ld, int T, int V, const int32_t* labels,
+                        float* loss_rows, float* loss_mean, int32_t* counter, void* dlogits,
+                        int ld_d, float grad_scale, void* stream) {
+  CHECK_ARG(logits && labels && loss_rows, "null input");
+  CHECK_ARG(T >= 0, "T=%d", T);
+  if (T == 0) return COLLM_OK;
+  CHECK_ARG(V >= 8 && V % 8 == 0 && ld % 8 == 0 && ld >= V, "V=%d / ld=%d must be multiples of 8",
+            V, ld);
+  CHECK_ARG(aligned16(logits), "logits must be 16-byte aligned");
+  CHECK_ARG(!loss_mean || counter, "loss_mean needs the arrival counter");
+  CHECK_ARG(!dlogits || (aligned16(dlogits) && ld_d % 8 == 0 && ld_d >= V),
+            "dlogits must be 16-byte aligned with ld_d >= V, a multiple of 8");
+  CeParams p{};
+  p.logits = (const bf16*)logits;
+  p.ld = ld;
+  p.T = T;
+  p.V = V;
+  p.labels = labels;
+  p.loss_rows = loss_rows;
+  p.loss_mean = loss_mean;
+  p.counter = counter;
+  p.dlogits = (bf16*)dlogits;
+  p.ld_d = ld_d;
+  p.grad_scale = grad_scale;
+  if (V <= 8 * 8 * 512)  // the row fits in registers: 8 vectors per thread x 512 threads
+    cross_entropy_kernel<8, 512><<<T, 512, 0, (cudaStream_t)stream>>>(p);
+  else
+    cross_entropy_kernel<0, 256><<<T, 256, 0, (cudaStream_t)stream>>>(p);
   CUDA_TRY(cudaGetLastError());
   return COLLM_OK;
 }

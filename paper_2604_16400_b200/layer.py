@@ -383,3 +383,55 @@ class LoraProjection:
         """Rewrite every bf16 copy of the trainable adapter from the fp32 masters (after a
         parameter average across replicas — the reference's fedavg, launcher.py:68-80)."""
         ops.lora_apply(self._grad_groups(targets="full"), _lib.MODE_COPY_ONLY)
+
+
+class LMHead:
+    """Frozen LM head + next-token cross-entropy of the training rows: the
+    real training signal behind the reference's convergence stand-in (`perf.train_step`,
+    perf.py:92-126).  logits = X_top . W^T (K2 GEMM, no LoRA), K7 softmax-CE forward + backward,
+    dX_top = dlogits . W (K3-shaped GEMM on the kept W^T) — the dY that enters the top layer's
+    LoRA backward.  W [V, h] bf16 (nn.Linear layout), W^T [h, V] bf16."""
+
+    def __init__(self, hidden: int, vocab: int, device: torch.device | str = "cuda",
+                 weight: torch.Tensor | None = None):
+        if hidden % 8 or vocab % 8:
+            raise ConfigurationError(f"LM head: hidden={hidden} and vocab={vocab} must be x8")
+        self.hidden, self.vocab = hidden, vocab
+        self.device = torch.device(device)
+        self.W = (weight if weight is not None else
+                  torch.empty(vocab, hidden, dtype=torch.bfloat16, device=self.device))
+        self.WT = torch.empty(hidden, vocab, dtype=torch.bfloat16, device=self.device)
+        self._bufs: dict = {}
+
+    def refresh_transpose(self) -> None:
+        self.WT.copy_(self.W.t())
+
+    def _buffers(self, T: int) -> dict:
+        b = self._bufs
+        if not b or b["logits"].shape[0] < T:
+            dev = self.device
+            b.update(logits=torch.empty(T, self.vocab, dtype=torch.bfloat16, device=dev),
+                     dlogits=torch.empty(T, self.vocab, dtype=torch.bfloat16, device=dev),
+                     loss_rows=torch.zeros(T, dtype=torch.float32, device=dev),
+                     loss=torch.zeros(1, dtype=torch.float32, device=dev),
+                     counter=torch.zeros(1, dtype=torch.int32, device=dev))
+        return b
+
+    def forward_backward(self, X: torch.Tensor, labels: torch.Tensor, dX: torch.Tensor,
+                         n_valid: int | None = None) -> torch.Tensor:
+        """Mean CE of the rows of X [T, h] against labels [T] (int32, < 0 ignored) and its
+        gradient w.r.t. X into dX [T, h].  Returns the device loss (fp32 [1]); all on the current
+        stream, nothing read back."""
+        T = labels.shape[0]
+        if X.shape[0] < T or X.shape[1] != self.hidden or dX.shape[0] < T:
+            raise ConfigurationError(f"LM head: X {tuple(X.shape)} / dX {tuple(dX.shape)} vs T={T}")
+        if T == 0:
+            raise ConfigurationError("LM head: no training rows")
+        b = self._buffers(T)
+        n = T if n_valid is None else n_valid
+        ops.gemm_lora(X, self.W, b["logits"], M=T)
+        ops.cross_entropy(b["logits"], labels, self.vocab, loss_rows=b["loss_rows"],
+                          loss_mean=b["loss"], counter=b["counter"], dlogits=b["dlogits"],
+                          grad_scale=1.0 / max(n, 1))
+        ops.gemm_lora(b["dlogits"], self.WT, dX, M=T)
+        return b["loss"]

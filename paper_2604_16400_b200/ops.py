@@ -39,9 +39,11 @@ def only(*kinds: str):
 
 
 def enabled(kind: str) -> bool:
-    """'lora' stands for both rank-space kinds ('shrink' = K1, 'reduce' = K5 + apply)."""
+    """'lora' stands for both rank-space kinds ('shrink' = K1, 'reduce' = K5 + apply); 'head' (K7
+    cross-entropy) rides with 'gemm' (the LM-head GEMMs)."""
     k = _filter.kinds
-    return k is None or kind in k or (kind in ("shrink", "reduce") and "lora" in k)
+    return (k is None or kind in k or (kind in ("shrink", "reduce") and "lora" in k)
+            or (kind == "head" and "gemm" in k))
 
 
 def launch_count() -> int:
@@ -215,3 +217,24 @@ def lora_apply(groups: list, mode: int, *, adamw: torch.Tensor | None = None) ->
         return
     arr = (_lib.ReduceGroup * len(groups))(*groups)
     _lib.call("collm_lora_apply", arr, len(groups), mode, _p(adamw), _stream())
+
+
+def cross_entropy(logits: torch.Tensor, labels: torch.Tensor, V: int, *,
+                  loss_rows: torch.Tensor, loss_mean: torch.Tensor | None = None,
+                  counter: torch.Tensor | None = None, dlogits: torch.Tensor | None = None,
+                  grad_scale: float = 1.0) -> None:
+    """K7: per-row softmax cross-entropy of bf16 logits [T, >=V] against int32 labels (< 0 =
+    ignored), the row-ordered mean over valid rows, and dlogits = grad_scale*(softmax - onehot)."""
+    _need(logits, torch.bfloat16, "logits")
+    _need(labels, torch.int32, "labels")
+    _need(loss_rows, torch.float32, "loss_rows")
+    T = labels.shape[0]
+    if logits.shape[0] < T or loss_rows.shape[0] < T:
+        raise ValueError(f"cross_entropy: logits {tuple(logits.shape)} / loss_rows vs T={T}")
+    if dlogits is not None:
+        _need(dlogits, torch.bfloat16, "dlogits")
+    if not _launch("head"):
+        return
+    _lib.call("collm_cross_entropy", logits.data_ptr(), logits.stride(0), T, V, labels.data_ptr(),
+              loss_rows.data_ptr(), _p(loss_mean), _p(counter), _p(dlogits),
+              dlogits.stride(0) if dlogits is not None else 0, float(grad_scale), _stream())

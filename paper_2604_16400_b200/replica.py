@@ -26,7 +26,7 @@ import torch
 from . import _lib, ops
 from .configs import LayerConfig
 from .domain import ConfigurationError, InferenceItem, MixedBatch, TrainItem
-from .layer import AdamWConfig, LoraProjection, OptimizerState
+from .layer import AdamWConfig, LMHead, LoraProjection, OptimizerState
 from .segments import DevicePlan, HostPlan, build_mixed_batch, plan_segments, uniform_plan
 
 ENTRY = ("qkv", "q", "k", "v", "gate_up", "gate", "up")
@@ -51,7 +51,7 @@ class StepPlan:
 
 class ReplicaStack:
     def __init__(self, cfg: LayerConfig, device: torch.device | str = "cuda", seed: int = 0,
-                 optimizer: AdamWConfig | None = None, init: bool = True):
+                 optimizer: AdamWConfig | None = None, init: bool = True, lm_head: bool = False):
         self.cfg = cfg
         self.device = torch.device(device)
         self.specs = cfg.projections
@@ -59,6 +59,10 @@ class ReplicaStack:
         self.layers: list[list[LoraProjection]] = [
             [LoraProjection(spec, cfg.n_adapters, self.device) for spec in self.specs]
             for _ in range(L)]
+        # lm_head: the training rows' real next-token CE (K7) drives the backward from the top
+        # (dY_top = its dX) and gives the step's training loss; without it dY_top is synthetic
+        self.head = LMHead(cfg.model.hidden, cfg.model.vocab, self.device) if lm_head else None
+        self._loss: torch.Tensor | None = None
         self.opt = OptimizerState(optimizer, self.device)
         self.seed = seed
         if init:
@@ -103,6 +107,9 @@ class ReplicaStack:
                     proj.B[:, bnd[s]:bnd[s + 1], :r] = b.to(torch.bfloat16)
                 proj.scale.fill_(sp.alpha / r)
                 proj.make_trainable(self.cfg.train_adapter)
+        if self.head is not None:
+            self.head.W.normal_(0.0, 0.02, generator=g)
+            self.head.refresh_transpose()
 
     def projections(self):
         for layer in self.layers:
@@ -202,6 +209,10 @@ class ReplicaStack:
                    for s in self.specs} if Ttr else {},
         }
         acts["X"][0].copy_(rnd(T, h))
+        if self.head is not None and Ttr:
+            # next-token targets of the training rows (synthetic token ids; no dataset offline)
+            acts["labels"] = torch.randint(0, self.cfg.model.vocab, (Ttr,), device=dev,
+                                           generator=g, dtype=torch.int32)
         self._acts = acts
         self._plan = plan
         return acts
@@ -282,6 +293,9 @@ class ReplicaStack:
                 caches[l][name] = box["c"]
                 proj.forward_gemm(box["c"], plan.device, Y, wait=sig)
                 prev = after(main)
+        if Ttr and backward and self.head is not None:
+            # K2 logits -> K7 softmax-CE fwd+bwd -> K3 dX: the real dY entering the top layer
+            self._loss = self.head.forward_backward(a["X"][L][:Ttr], a["labels"], a["dY_top"])
         if Ttr and backward:
             opt = self.opt if optimizer_step else None
             mode = _lib.MODE_ADAMW if opt is not None else _lib.MODE_STORE_GRAD
@@ -325,6 +339,12 @@ class ReplicaStack:
         if overlap:
             main.wait_stream(side)
         return a["X"][L]
+
+    def last_loss(self) -> float:
+        """Training loss of the last step that ran the LM head (reads the device scalar back)."""
+        if self._loss is None:
+            raise ConfigurationError("no step with the LM head has run (lm_head=True, training rows)")
+        return float(self._loss.item())
 
     # ------------------------------------------------------------------ step generation
     def advance_step(self, optimizer_step: bool = True) -> None:

@@ -125,11 +125,33 @@ def make_lora(seed: int, out: dict):
     out[p + "dB"] = B_t.grad.numpy()   # [N, r_pad]
 
 
+def make_ce(out: dict):
+    """3. ce_autograd.npz — torch float64 F.cross_entropy (mean over non-ignored rows,
+    ignore_index=-100) and its autograd gradient w.r.t. the logits: an independent formulation
+    pinning oracle.cross_entropy (the reference has no loss arithmetic, perf.py:92-126)."""
+    import torch
+    g = np.random.default_rng(7)
+    for T, V in ((6, 40), (33, 512)):
+        z = (g.standard_normal((T, V)) * 3).astype(np.float32)
+        y = g.integers(0, V, T).astype(np.int64)
+        y[1] = -100  # an ignored row
+        zt = torch.tensor(z, dtype=torch.float64, requires_grad=True)
+        loss = torch.nn.functional.cross_entropy(zt, torch.tensor(y), ignore_index=-100)
+        loss.backward()
+        out[f"ce_{T}x{V}_logits"] = z
+        out[f"ce_{T}x{V}_labels"] = y
+        out[f"ce_{T}x{V}_loss"] = np.float64(loss.item())
+        out[f"ce_{T}x{V}_dlogits"] = zt.grad.numpy()
+
+
 if __name__ == "__main__":
+    ce = {}
+    make_ce(ce)
+    np.savez_compressed(os.path.join(HERE, "ce_autograd.npz"), **ce)
     make_fedavg()
     lo = {}
     for seed in (0, 1):
         make_lora(seed, lo)
     np.savez_compressed(os.path.join(HERE, "lora_autograd.npz"), **lo)
-    for f in ("fedavg_ref.npz", "lora_autograd.npz"):
+    for f in ("fedavg_ref.npz", "lora_autograd.npz", "ce_autograd.npz"):
         print(f, os.path.getsize(os.path.join(HERE, f)), "bytes")

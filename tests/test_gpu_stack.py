@@ -107,6 +107,40 @@ def test_measured_latency_backend():
     assert be.true_infer_latency(None, cfg) == t_inf  # cached per (B, b)
 
 
+def test_real_training_backend_train_step():
+    """backend.RealTrainingBackend.train_step replaces the reference's convergence stand-in
+    (perf.train_step, perf.py:111-126) with real steps: the returned state (a dataclass shaped
+    like the reference's TrainState) carries the measured CE loss, the first step anchors
+    initial_loss, later steps report the real decrement, and training on fixed synthetic targets
+    lowers the loss."""
+    import dataclasses
+
+    from paper_2604_16400_b200.backend import RealTrainingBackend
+    from paper_2604_16400_b200.configs import CONFIGS
+
+    @dataclasses.dataclass(frozen=True)
+    class State:  # the fields of coserve.perf.TrainState the engine reads (perf.py:92-109)
+        loss: float = 2.0
+        initial_loss: float = 2.0
+        asymptote_loss: float = 0.5
+        steps: int = 0
+        last_decrement: float = 0.0
+
+    from paper_2604_16400_b200.layer import AdamWConfig
+    be = RealTrainingBackend(CONFIGS["tiny"], optimizer=AdamWConfig(lr=1e-2))
+    s0 = State()
+    s1 = be.train_step(s0, 2)
+    assert s1.steps == 1 and s1.initial_loss == s1.loss and s1.last_decrement == 0.0
+    assert 0.0 < s1.loss < 50.0
+    s = s1
+    for _ in range(5):
+        prev = s
+        s = be.train_step(s, 2)
+        assert abs(s.last_decrement - (prev.loss - s.loss)) < 1e-12
+    assert s.steps == 6
+    assert s.loss < s1.loss  # AdamW on the LoRA adapter fits the fixed targets
+
+
 def test_stack_backward_matches_oracle():
     """The stack's training-row backward through the overlapped step — dH shrinks, dX GEMMs and
     the per-layer batched K5 launch (STORE_GRAD mode) — against the oracle on the stack's own
@@ -160,3 +194,28 @@ def test_flag_overlap_mode_bitwise(cfg_key):
     torch.cuda.synchronize()
     for a, b in zip(want, _state(fl)):
         assert torch.equal(a, b)
+
+
+def test_lm_head_loss_and_top_gradient():
+    """The LM head on the training rows (K2 logits, K7 CE, K3 dX): the step's loss equals the
+    oracle CE of the bf16 logits of the stack's final hidden rows, and dY_top = dlogits . W."""
+    import numpy as np
+
+    import oracle
+    from paper_2604_16400_b200.replica import ReplicaStack
+    cfg = _config("tiny")
+    st = ReplicaStack(cfg, "cuda", seed=3, lm_head=True)
+    plan = st.plan(*cfg.batch(0))
+    a = st.allocate(plan, distinct_synthetic=True)
+    st.run_step(plan, optimizer_step=False)
+    torch.cuda.synchronize()
+    Ttr, L = plan.n_train, cfg.model.layers
+    Xtop = a["X"][L][:Ttr].float().cpu().numpy()
+    Wh = st.head.W.float().cpu().numpy()
+    logits = oracle.bf16_round(Xtop @ Wh.T)
+    rows, mean, dz = oracle.cross_entropy(logits, a["labels"].cpu().numpy())
+    assert abs(st.last_loss() - mean) <= 1e-3 * abs(mean)
+    dX_ref = oracle.bf16_round(dz) @ Wh
+    got = a["dY_top"].float().cpu().numpy()
+    err = np.abs(got - dX_ref).max()
+    assert err <= 1e-2 * np.abs(dX_ref).max() + 1e-6, err

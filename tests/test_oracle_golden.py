@@ -105,3 +105,15 @@ def test_adamw_matches_torch():
         tp.grad = torch.from_numpy(gr)
         opt.step()
     assert np.allclose(p, tp.detach().numpy(), rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("shape", ["6x40", "33x512"])
+def test_cross_entropy_oracle_vs_autograd(shape):
+    """oracle.cross_entropy (K7's restatement) against torch float64 F.cross_entropy + autograd
+    (tests/golden/make_golden.py, ignore_index rows included)."""
+    d = np.load(os.path.join(GOLD, "ce_autograd.npz"))
+    z, y = d[f"ce_{shape}_logits"], d[f"ce_{shape}_labels"]
+    loss_rows, mean, dz = oracle.cross_entropy(z, y)
+    assert abs(mean - float(d[f"ce_{shape}_loss"])) < 1e-12
+    np.testing.assert_allclose(dz, d[f"ce_{shape}_dlogits"], rtol=0, atol=1e-14)
+    assert loss_rows[1] == 0.0 and np.all(dz[1] == 0.0)  # the ignored row
