@@ -17,3 +17,7 @@ ncu --set full --clock-control none --import-source on -k regex:"gemm_lora" -s $
 ncu --set full --clock-control none --import-source on -k regex:"gemm_lora" -s $((NG + NG / 2)) -c 1 -o $OUT/full_gemm_dx_down python tools/profile_step.py --config $CFG 2>&1 | tail -1
 ncu --set full --clock-control none --import-source on -k regex:"lora_shrink" -s $NS -c 1 -o $OUT/full_shrink_fwd_qkv python tools/profile_step.py --config $CFG 2>&1 | tail -1
 ncu --set full --clock-control none --import-source on -k regex:"lora_reduce" -s $NR -c 1 -o $OUT/full_reduce_layer python tools/profile_step.py --config $CFG 2>&1 | tail -1
+# a split-2 dX GEMM in 4-CTA clusters (o of the top layer: the third dX GEMM of the backward) and
+# the LM-head cross-entropy kernel (K7) at the 7B head shape
+ncu --set full --clock-control none --import-source on -k regex:"gemm_lora" -s $((NG + NG / 2 + 2)) -c 1 -o $OUT/full_gemm_dx_o_split2 python tools/profile_step.py --config $CFG 2>&1 | tail -1
+ncu --set full --clock-control none --import-source on -k regex:"cross_entropy" -s 3 -c 1 -o $OUT/full_ce_head python tools/ce_bench.py 512 32000 2>&1 | tail -1
