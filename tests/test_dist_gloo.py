@@ -69,3 +69,55 @@ def test_single_process_is_identity():
     before = t.clone()
     assert sync.allreduce_grads(t) is t and torch.equal(t, before)
     assert sync.fedavg_params(t) is t
+
+
+class _FakeProj:
+    def __init__(self):
+        self.refreshed = 0
+
+    def refresh_from_master(self):
+        self.refreshed += 1
+
+
+class _FakeStack:
+    """The two members broadcast_adapter uses: the flat fp32 masters and the projections."""
+
+    def __init__(self, flat):
+        self.flat_master = flat
+        self._p = [_FakeProj(), _FakeProj()]
+
+    def projections(self):
+        return iter(self._p)
+
+
+def _bcast_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_16400_b200.registry import broadcast_adapter
+        st = _FakeStack(torch.full((7,), float(rank + 1)))
+        broadcast_adapter(st, src=1)
+        q.put((rank, st.flat_master.numpy().copy(), [p.refreshed for p in st._p]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_global_adapter_broadcast():
+    """The aggregated adapter is pushed from the server replica to every replica (one broadcast
+    of the flat fp32 masters, then each replica rewrites its bf16 copies) — the step the
+    reference's round protocol omits (engine.py:468-480)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=100) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=30)
+        assert p.exitcode == 0
+    for rank, flat, refreshed in res:
+        assert np.all(flat == 2.0), (rank, flat)  # rank 1's masters everywhere
+        assert refreshed == [1, 1]

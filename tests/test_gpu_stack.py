@@ -219,3 +219,57 @@ def test_lm_head_loss_and_top_gradient():
     got = a["dY_top"].float().cpu().numpy()
     err = np.abs(got - dX_ref).max()
     assert err <= 1e-2 * np.abs(dX_ref).max() + 1e-6, err
+
+
+def test_adapter_pager_paging_is_exact():
+    """registry.AdapterPager: adapters stored in pinned host memory and paged into device slots
+    by async copies give bitwise the same forward as adapters set in place; LRU eviction never
+    touches the pinned (trainable) slot nor a slot the current request needs; save/load
+    round-trips the reference layout exactly."""
+    import os
+    import tempfile
+
+    from paper_2604_16400_b200.registry import AdapterPager
+    ref, plan = _stack(False, "tiny", seed=5)
+    n = ref.cfg.n_adapters
+    ref.run_step(plan, backward=False)
+    torch.cuda.synchronize()
+    want = ref._acts["X"][-1].clone()
+    # a second stack whose inference adapters come from the pager's host store
+    st, plan2 = _stack(False, "tiny", seed=6)
+    for p_ref, p in zip(ref.projections(), st.projections()):
+        p.W.copy_(p_ref.W)
+        p.refresh_transpose()
+    pager = AdapterPager(st)
+    projs = list(ref.projections())
+    for a in range(n):
+        pager.register(f"tenant{a}", [p.get_adapter(a) for p in projs])
+    t = ref.cfg.train_adapter
+    for p_ref, p in zip(projs, st.projections()):  # the pinned trainable slot: set in place
+        p.A[t].copy_(p_ref.A[t])
+        p.B[t].copy_(p_ref.B[t])
+        p.scale[t:t + 1].copy_(p_ref.scale[t:t + 1])
+    slots = pager.ensure([f"tenant{a}" for a in range(n) if a != t])
+    assert slots == {f"tenant{a}": a for a in range(n) if a != t}
+    st._acts["X"][0].copy_(ref._acts["X"][0])
+    st.run_step(plan2, backward=False)
+    pager.mark_used(range(n))
+    torch.cuda.synchronize()
+    assert torch.equal(st._acts["X"][-1], want)
+    # eviction: a new adapter takes the least recently used pageable slot
+    pager.register("new", [p.get_adapter((t + 1) % n) for p in projs])
+    order = [f"tenant{a}" for a in range(n) if a != t]
+    pager.ensure(order[1:])                 # touch all but the first -> it is the LRU
+    got = pager.ensure(["new"])["new"]
+    assert got == int(order[0][len("tenant"):]) and got != t
+    assert f"tenant{got}" not in pager.slot_of
+    torch.cuda.synchronize()
+    for p_src, p in zip(projs, st.projections()):
+        assert torch.equal(p.A[got], p_src.A[(t + 1) % n]) and torch.equal(p.B[got], p_src.B[(t + 1) % n])
+        assert torch.equal(p.A[t], p_src.A[t])
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "a.pt")
+        pager.save("tenant1", path)
+        pager.load("copy", path)
+    for (A0, B0, s0), (A1, B1, s1) in zip(pager.host["tenant1"], pager.host["copy"]):
+        assert torch.equal(A0, A1) and torch.equal(B0, B1) and torch.equal(s0, s1)
