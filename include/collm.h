@@ -166,6 +166,24 @@ int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int
 int collm_lora_apply(const collm_reduce_group* groups, int n_groups, int mode,
                      const float* adamw, void* stream);
 
+/* ---- K8: attention of the mixed batch over a paged KV cache (forward) -------------------------
+ * Every query row t (decode, prefill or training token) attends causally to tokens
+ * [0, row_pos[t]] of its sequence row_seq[t], whose K/V already sit in the paged cache:
+ *   out[t, h] = sum_j softmax_j(scale * q[t, h] . K[j, h/G]) V[j, h/G],  G = n_heads / n_kv_heads
+ * q [T, ldq] / out [T, ldo] bf16 (head h at columns h*head_dim); k_cache, v_cache bf16
+ * [n_pages, n_kv_heads, page_size, head_dim] (head-major pages); block_table [n_seq, bt_stride]
+ * int32 page ids;
+ * max_ctx >= every row_pos + 1.  head_dim 128, G <= 8, page_size a power of two.  fp32 softmax,
+ * deterministic (split partials combined in split order by the last CTA; workspace counters
+ * zeroed once and restored).  Replaces: nothing in the reference (which has no attention); the
+ * step either side of the LoRA projections. */
+size_t collm_attention_workspace_bytes(int T, int n_heads, int n_kv_heads, int max_ctx);
+int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_heads,
+                          int head_dim, const void* k_cache, const void* v_cache, int page_size,
+                          const int32_t* block_table, int bt_stride, const int32_t* row_seq,
+                          const int32_t* row_pos, int max_ctx, float scale, void* out, int ldo,
+                          void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- K7: softmax cross-entropy forward + backward over LM-head logits ------------------------
  * For each row t of logits [T, ld] (bf16, V used columns, V and ld multiples of 8):
  *   loss_rows[t] = logsumexp(z_t) - z_t[labels[t]]  (0 when labels[t] < 0 or >= V: ignored)

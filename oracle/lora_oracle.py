@@ -23,7 +23,7 @@ import numpy as np
 __all__ = [
     "bf16_round", "bf16_to_bits", "bits_to_f32", "build_rows", "expand_segments", "tile_slots",
     "slot_of_row", "shrink_tiles", "lora_forward", "lora_backward", "adamw_step", "AdamWState",
-    "fedavg", "AggregationError", "projection_flops", "cross_entropy",
+    "fedavg", "AggregationError", "projection_flops", "cross_entropy", "paged_attention",
 ]
 
 
@@ -237,6 +237,33 @@ def cross_entropy(logits, labels, grad_scale=None):
     d *= g
     d[~valid] = 0.0
     return loss_rows, mean, d
+
+
+# --------------------------------------------------------------------------- attention (K8)
+def paged_attention(q, k_cache, v_cache, block_table, row_seq, row_pos, n_heads, n_kv_heads,
+                    scale=None):
+    """Causal attention of each query row over tokens [0, pos] of its sequence's paged KV cache
+    (the step either side of the LoRA projections; the reference has no
+    attention).  q [T, n_heads*D]; caches [n_pages, n_kv_heads, page, D]; block_table
+    [n_seq, max_pages].  float64, returns [T, n_heads*D]."""
+    q = np.asarray(q, np.float64)
+    kc = np.asarray(k_cache, np.float64)
+    vc = np.asarray(v_cache, np.float64)
+    page, D = kc.shape[2], kc.shape[3]
+    G = n_heads // n_kv_heads
+    sc = D ** -0.5 if scale is None else scale
+    out = np.zeros((q.shape[0], n_heads * D))
+    for t in range(q.shape[0]):
+        n = int(row_pos[t]) + 1
+        j = np.arange(n)
+        pages = np.asarray(block_table)[int(row_seq[t])][j // page]
+        K = kc[pages, :, j % page]  # [n, n_kv_heads, D]
+        V = vc[pages, :, j % page]
+        for h in range(n_heads):
+            s = K[:, h // G] @ q[t, h * D:(h + 1) * D] * sc
+            p = np.exp(s - s.max())
+            out[t, h * D:(h + 1) * D] = (p / p.sum()) @ V[:, h // G]
+    return out
 
 
 # --------------------------------------------------------------------------- FedAvg

@@ -49,6 +49,9 @@ SIGNATURES: dict[str, tuple] = {
     "collm_lora_shrink": (_I, [_P, _I, _P, _LL, _I, _P, _I, _P, _IP, _I, _P, _P, _I, _P, _P,
                                _P, _P, _P, _P]),
     "collm_cross_entropy": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _F, _P]),
+    "collm_attention_workspace_bytes": (_SZ, [_I, _I, _I, _I]),
+    "collm_paged_attention": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _I, _P, _I, _P, _P, _I, _F,
+                                   _P, _I, _P, _SZ, _P]),
     "collm_gemm_workspace_bytes": (_SZ, [_I]),
     "collm_set_gemm_lean": (_I, [_I]),
     "collm_gemm_lora": (_I, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _P,

@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "gemm_lora.cuh"
 #include "reduce_adamw.cuh"
+#include "attn.cuh"
 #include "ce.cuh"
 #include "segments.cuh"
 #include "shrink.cuh"
@@ -653,6 +654,7 @@ int collm_preload(void) {
   COLLM_PRELOAD(lora_reduce_kernel<48>);
   COLLM_PRELOAD(lora_apply_kernel);
   COLLM_PRELOAD((cross_entropy_kernel<8, 512>));
+  COLLM_PRELOAD(paged_attention_kernel);
   COLLM_PRELOAD((cross_entropy_kernel<0, 256>));
 #undef COLLM_PRELOAD
   return COLLM_OK;
@@ -847,6 +849,60 @@ int collm_lora_apply(const collm_reduce_group* groups, int n_groups, int mode,
   for (int g = 0; g < n_groups; ++g) total += (long long)p.groups[g].P * p.groups[g].Q;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 4LL * num_sms_cached());
   lora_apply_kernel<<<std::max(blocks, 1), 256, 0, (cudaStream_t)stream>>>(p, total);
+  CUDA_TRY(cudaGetLastError());
+  return COLLM_OK;
+}
+
+// ------------------------------------------------------------------------------------ K8
+size_t collm_attention_workspace_bytes(int T, int n_heads, int n_kv_heads, int max_ctx) {
+  if (T <= 0 || n_kv_heads <= 0 || n_heads <= 0 || max_ctx <= 0) return 0;
+  const size_t splits = (size_t)(max_ctx + kAttnSplit - 1) / kAttnSplit;
+  const size_t counters = ((size_t)T * n_kv_heads * 4 + 255) & ~(size_t)255;
+  return counters + (size_t)T * n_heads * splits * (kAttnD + 2) * 4;
+}
+
+int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_heads,
+                          int head_dim, const void* k_cache, const void* v_cache, int page_size,
+                          const int32_t* block_table, int bt_stride, const int32_t* row_seq,
+                          const int32_t* row_pos, int max_ctx, float scale, void* out, int ldo,
+                          void* workspace, size_t ws_bytes, void* stream) {
+  CHECK_ARG(q && k_cache && v_cache && block_table && row_seq && row_pos && out, "null input");
+  CHECK_ARG(T >= 0, "T=%d", T);
+  if (T == 0) return COLLM_OK;
+  CHECK_ARG(head_dim == kAttnD, "head_dim=%d (supported: %d)", head_dim, kAttnD);
+  CHECK_ARG(n_kv_heads >= 1 && n_heads % n_kv_heads == 0 && n_heads / n_kv_heads <= kAttnMaxG,
+            "n_heads=%d / n_kv_heads=%d (GQA group <= %d)", n_heads, n_kv_heads, kAttnMaxG);
+  CHECK_ARG(page_size >= 1 && (page_size & (page_size - 1)) == 0, "page_size=%d must be 2^k",
+            page_size);
+  CHECK_ARG(max_ctx >= 1 && bt_stride * page_size >= max_ctx, "max_ctx=%d exceeds the block table",
+            max_ctx);
+  CHECK_ARG(ldq >= n_heads * head_dim && ldo >= n_heads * head_dim, "ldq/ldo too small");
+  CHECK_ARG(aligned16(k_cache) && aligned16(v_cache), "KV caches must be 16-byte aligned");
+  const size_t need = collm_attention_workspace_bytes(T, n_heads, n_kv_heads, max_ctx);
+  CHECK_ARG(workspace && ws_bytes >= need, "attention workspace too small: %zu < %zu", ws_bytes,
+            need);
+  AttnParams p{};
+  p.q = (const bf16*)q;
+  p.ldq = ldq;
+  p.k_cache = (const bf16*)k_cache;
+  p.v_cache = (const bf16*)v_cache;
+  int shift = 0;
+  while ((1 << shift) < page_size) ++shift;
+  p.page_shift = shift;
+  p.n_heads = n_heads;
+  p.n_kv_heads = n_kv_heads;
+  p.block_table = block_table;
+  p.bt_stride = bt_stride;
+  p.row_seq = row_seq;
+  p.row_pos = row_pos;
+  p.out = (bf16*)out;
+  p.ldo = ldo;
+  p.scale = scale;
+  p.max_splits = (max_ctx + kAttnSplit - 1) / kAttnSplit;
+  p.counters = (int32_t*)workspace;
+  p.part = (float*)((char*)workspace + (((size_t)T * n_kv_heads * 4 + 255) & ~(size_t)255));
+  paged_attention_kernel<<<dim3(T, n_kv_heads, p.max_splits), kAttnThreads, 0,
+                           (cudaStream_t)stream>>>(p);
   CUDA_TRY(cudaGetLastError());
   return COLLM_OK;
 }

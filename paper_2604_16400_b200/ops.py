@@ -238,3 +238,32 @@ def cross_entropy(logits: torch.Tensor, labels: torch.Tensor, V: int, *,
     _lib.call("collm_cross_entropy", logits.data_ptr(), logits.stride(0), T, V, labels.data_ptr(),
               loss_rows.data_ptr(), _p(loss_mean), _p(counter), _p(dlogits),
               dlogits.stride(0) if dlogits is not None else 0, float(grad_scale), _stream())
+
+
+_attn_ws = Workspace()
+
+
+def paged_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
+                    block_table: torch.Tensor, row_seq: torch.Tensor, row_pos: torch.Tensor,
+                    out: torch.Tensor, *, n_heads: int, n_kv_heads: int, max_ctx: int,
+                    scale: float | None = None) -> None:
+    """K8: out[t, h] = causal attention of query row t over tokens [0, row_pos[t]] of its
+    sequence's paged KV cache (see collm.h).  q / out [T, n_heads*128] bf16, caches
+    [n_pages, n_kv_heads, page, 128] bf16 (head-major pages), block_table [n_seq, max_pages] int32."""
+    for t, n in ((q, "q"), (k_cache, "k_cache"), (v_cache, "v_cache"), (out, "out")):
+        _need(t, torch.bfloat16, n)
+    for t, n in ((block_table, "block_table"), (row_seq, "row_seq"), (row_pos, "row_pos")):
+        _need(t, torch.int32, n)
+    T = row_pos.shape[0]
+    D = k_cache.shape[-1]
+    if k_cache.shape != v_cache.shape or k_cache.shape[1] != n_kv_heads:
+        raise ValueError(f"paged_attention: caches {tuple(k_cache.shape)} / {tuple(v_cache.shape)}")
+    if not _launch("attention"):
+        return
+    ws_bytes = _lib.load().collm_attention_workspace_bytes(T, n_heads, n_kv_heads, max_ctx)
+    ws = _attn_ws.get(ws_bytes, q.device)
+    _lib.call("collm_paged_attention", q.data_ptr(), q.stride(0), T, n_heads, n_kv_heads, D,
+              k_cache.data_ptr(), v_cache.data_ptr(), k_cache.shape[2], block_table.data_ptr(),
+              block_table.stride(0), row_seq.data_ptr(), row_pos.data_ptr(), max_ctx,
+              float(scale if scale is not None else D ** -0.5), out.data_ptr(), out.stride(0),
+              _p(ws), 0 if ws is None else ws.numel(), _stream())

@@ -226,3 +226,48 @@ def test_cross_entropy_vs_oracle(T, V):
     torch.cuda.synchronize()
     for a, b in zip(first, (loss_rows, mean, dz)):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n_heads,n_kv", [(4, 4), (8, 2)])
+def test_paged_attention_vs_oracle(n_heads, n_kv):
+    """K8 over a shuffled paged KV cache: decode rows with contexts 1..700 (multi-split, split
+    boundary 256/257), a prefill segment (causal, positions 0..n-1) and GQA — against the float64
+    oracle (bf16 output tolerance); two launches bitwise identical (split combine order fixed,
+    counters restored)."""
+    import numpy as np
+
+    import oracle
+    from paper_2604_16400_b200 import ops
+    g = torch.Generator().manual_seed(n_heads * 10 + n_kv)
+    D, page = 128, 16
+    ctxs = [1, 37, 256, 257, 700]          # decode sequences (context length incl. the new token)
+    prefill = 23                           # one prefill sequence: rows at positions 0..22
+    seq_lens = ctxs + [prefill]
+    pages_per = [(n + page - 1) // page for n in seq_lens]
+    n_pages = sum(pages_per) + 5
+    perm = torch.randperm(n_pages, generator=g)
+    bt = torch.zeros(len(seq_lens), max(pages_per), dtype=torch.int32)
+    o = 0
+    for s, npg in enumerate(pages_per):
+        bt[s, :npg] = perm[o:o + npg].to(torch.int32)
+        o += npg
+    kc = (torch.randn(n_pages, n_kv, page, D, generator=g)).to(torch.bfloat16)
+    vc = (torch.randn(n_pages, n_kv, page, D, generator=g)).to(torch.bfloat16)
+    row_seq = [s for s in range(len(ctxs))] + [len(ctxs)] * prefill
+    row_pos = [n - 1 for n in ctxs] + list(range(prefill))
+    T = len(row_seq)
+    q = (torch.randn(T, n_heads * D, generator=g) * 2).to(torch.bfloat16)
+    out = torch.empty(T, n_heads * D, dtype=torch.bfloat16, device="cuda")
+    args = dict(n_heads=n_heads, n_kv_heads=n_kv, max_ctx=max(seq_lens))
+    rs = torch.tensor(row_seq, dtype=torch.int32).cuda()
+    rp = torch.tensor(row_pos, dtype=torch.int32).cuda()
+    ops.paged_attention(q.cuda(), kc.cuda(), vc.cuda(), bt.cuda(), rs, rp, out, **args)
+    torch.cuda.synchronize()
+    ref = oracle.paged_attention(q.float().numpy(), kc.float().numpy(), vc.float().numpy(),
+                                 bt.numpy(), row_seq, row_pos, n_heads, n_kv)
+    _close_bf16(out, torch.from_numpy(ref).float().cuda())
+    out2 = torch.empty_like(out)
+    ops.paged_attention(q.cuda(), kc.cuda(), vc.cuda(), bt.cuda(), rs, rp, out2, **args)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
+    assert np.isfinite(out.float().cpu().numpy()).all()

@@ -117,3 +117,45 @@ def test_cross_entropy_oracle_vs_autograd(shape):
     assert abs(mean - float(d[f"ce_{shape}_loss"])) < 1e-12
     np.testing.assert_allclose(dz, d[f"ce_{shape}_dlogits"], rtol=0, atol=1e-14)
     assert loss_rows[1] == 0.0 and np.all(dz[1] == 0.0)  # the ignored row
+
+
+def test_paged_attention_oracle_vs_torch_sdpa():
+    """oracle.paged_attention (K8's restatement) against torch float64 scaled_dot_product_attention
+    on the same sequences laid out contiguously: a causal prefill sequence and decode rows with
+    GQA (torch's reference attention, an independent formulation; the reference has none)."""
+    import torch
+    import torch.nn.functional as F
+    g = np.random.default_rng(3)
+    H, KV, D, page = 4, 2, 128, 8
+    lens = [5, 19]  # sequence 0: decode row at position 4; sequence 1: prefill rows 0..18
+    npg = [(n + page - 1) // page for n in lens]
+    n_pages = sum(npg) + 2
+    perm = g.permutation(n_pages)
+    bt = np.zeros((2, max(npg)), np.int32)
+    bt[0, :npg[0]] = perm[:npg[0]]
+    bt[1, :npg[1]] = perm[npg[0]:npg[0] + npg[1]]
+    kc = g.standard_normal((n_pages, KV, page, D))
+    vc = g.standard_normal((n_pages, KV, page, D))
+    row_seq = [0] + [1] * lens[1]
+    row_pos = [lens[0] - 1] + list(range(lens[1]))
+    q = g.standard_normal((len(row_seq), H * D))
+    got = oracle.paged_attention(q, kc, vc, bt, row_seq, row_pos, H, KV)
+
+    def contiguous(s):
+        j = np.arange(lens[s])
+        return (torch.tensor(kc[bt[s][j // page], :, j % page]),
+                torch.tensor(vc[bt[s][j // page], :, j % page]))
+    # decode row: attends to all 5 tokens of sequence 0
+    K0, V0 = contiguous(0)
+    qd = torch.tensor(q[0]).view(H, 1, D)
+    ref0 = F.scaled_dot_product_attention(qd, K0.permute(1, 0, 2).repeat_interleave(H // KV, 0),
+                                          V0.permute(1, 0, 2).repeat_interleave(H // KV, 0))
+    np.testing.assert_allclose(got[0], ref0.reshape(-1).numpy(), rtol=1e-10, atol=1e-10)
+    # prefill rows: causal over sequence 1
+    K1, V1 = contiguous(1)
+    qp = torch.tensor(q[1:]).view(lens[1], H, D).permute(1, 0, 2)
+    ref1 = F.scaled_dot_product_attention(qp, K1.permute(1, 0, 2).repeat_interleave(H // KV, 0),
+                                          V1.permute(1, 0, 2).repeat_interleave(H // KV, 0),
+                                          is_causal=True)
+    np.testing.assert_allclose(got[1:], ref1.permute(1, 0, 2).reshape(lens[1], -1).numpy(),
+                               rtol=1e-10, atol=1e-10)
