@@ -7,10 +7,7 @@
 //
 // GQA: G = n_heads / n_kv_heads query heads share one KV head; one CTA handles (row, KV head,
 // split of <= kAttnSplit tokens) for all G heads, so each K/V byte of the split is read once.
-// Three phases per CTA: scores (one thread per token: 16-byte loads of its K row, G dot products
-// against the row's queries staged in shared memory), max / sum of exp over the split (block
-// reduction), then P.V (each warp a quarter of the tokens, a lane 4 of the 128 dims: a warp reads
-// one whole 256-byte V row per token).  Splits of one (row, KV head) combine in split order in the CTA that finishes
+// Each CTA streams its split as 8 half-warp flash-decoding streams (below).  Splits of one (row, KV head) combine in split order in the CTA that finishes
 // last (arrival counter, restored): (m, l, acc) rescaled exactly like flash-decoding —
 // deterministic, no float atomics.  fp32 softmax / accumulation, bf16 in and out, D = 128.
 //
@@ -45,147 +42,141 @@ struct AttnParams {
   int max_splits;
 };
 
+// Half-warp streams: lanes 0-15 of a warp walk one token, lanes 16-31 the next, each lane owning 8
+// of the 128 dims (16-byte loads: a half-warp reads a whole K row, then the same token's V row).
+// Per stream an online softmax (m, l, acc[8] per head) — no block-wide phases; the 8 streams of
+// the CTA merge through shared memory at the end (fixed order).
+template <int G>
 __global__ void __launch_bounds__(kAttnThreads) paged_attention_kernel(const AttnParams p) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  constexpr int kStreams = 2 * kAttnThreads / 32;  // 8 half-warps
   const int t = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
-  const int G = p.n_heads / p.n_kv_heads;
   const int pos = p.row_pos[t];
   const int n_tok = pos + 1;
   const int n_splits = (n_tok + kAttnSplit - 1) / kAttnSplit;
   if (split >= n_splits) return;  // this row's context is shorter
   const int seq = p.row_seq[t];
   const int j0 = split * kAttnSplit, j1 = min(n_tok, j0 + kAttnSplit);
-  const int n = j1 - j0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int hl = lane & 15, stream = warp * 2 + (lane >> 4);
   const int psz = 1 << p.page_shift;
   const int32_t* bt = p.block_table + (size_t)seq * p.bt_stride;
+  const int h0 = kvh * G;
 
-  __shared__ float sq[kAttnMaxG][kAttnD];
-  __shared__ float ss[kAttnMaxG][kAttnSplit];
-  __shared__ float red[kAttnMaxG][kAttnThreads / 32];
-  __shared__ float s_m[kAttnMaxG], s_l[kAttnMaxG];
-  __shared__ bool s_last;
-
-  // queries of the G heads of this KV head (pre-scaled)
-  for (int e = tid; e < G * kAttnD; e += kAttnThreads) {
-    const int g = e / kAttnD, d = e % kAttnD;
-    sq[g][d] = p.scale * __bfloat162float(p.q[(size_t)t * p.ldq + (kvh * G + g) * kAttnD + d]);
-  }
-  __syncthreads();
-
-  // phase 1: scores, one thread per token
-  auto kv_row = [&](const bf16* cache, int j) {
-    const int pg = bt[j >> p.page_shift];
-    return cache + (((size_t)pg * p.n_kv_heads + kvh) * psz + (j & (psz - 1))) * kAttnD;
-  };
-  for (int i = tid; i < n; i += kAttnThreads) {
-    const bf16* kr = kv_row(p.k_cache, j0 + i);
-    float acc[kAttnMaxG];
+  // this lane's 8 query dims of each head, pre-scaled by scale * log2(e) (exp2 softmax)
+  float qf[G][8];
 #pragma unroll
-    for (int g = 0; g < kAttnMaxG; ++g) acc[g] = 0.f;
-#pragma unroll 4
-    for (int v8 = 0; v8 < kAttnD / 8; ++v8) {
-      const uint4 u = ld_global_nc_v4(kr + 8 * v8);
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  for (int g = 0; g < G; ++g) {
+    const uint4 u = ld_global_nc_v4(p.q + (size_t)t * p.ldq + (h0 + g) * kAttnD + 8 * hl);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      qf[g][2 * k] = __uint_as_float(w[k] << 16) * p.scale * kLog2e;
+      qf[g][2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u) * p.scale * kLog2e;
+    }
+  }
+  float m[G], l[G], acc[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) acc[g][d] = 0.f;
+  }
+  auto row_of = [&](const bf16* cache, int j) {
+    const int pg = bt[j >> p.page_shift];
+    return cache + (((size_t)pg * p.n_kv_heads + kvh) * psz + (j & (psz - 1))) * kAttnD + 8 * hl;
+  };
+  constexpr int kU = G >= 4 ? 1 : 2;  // tokens per stream in flight (registers: G x 8 accumulators)
+  // warp-uniform trip count (the half-warp shuffles need both halves): a half whose token is
+  // past the split end computes on zeros and skips its state update
+  for (int jw = j0 + warp * 2; jw < j1; jw += kStreams * kU) {
+    uint4 kr[kU], vr[kU];
+    bool ok[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = jw + (lane >> 4) + u * kStreams;
+      ok[u] = j < j1;
+      kr[u] = ok[u] ? ld_global_nc_v4(row_of(p.k_cache, j)) : make_uint4(0, 0, 0, 0);
+      vr[u] = ok[u] ? ld_global_nc_v4(row_of(p.v_cache, j)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      float kf[8], vf[8];
+      const uint32_t kw[4] = {kr[u].x, kr[u].y, kr[u].z, kr[u].w};
+      const uint32_t vw[4] = {vr[u].x, vr[u].y, vr[u].z, vr[u].w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float a = __uint_as_float(w[k] << 16), b = __uint_as_float(w[k] & 0xffff0000u);
+        kf[2 * k] = __uint_as_float(kw[k] << 16);
+        kf[2 * k + 1] = __uint_as_float(kw[k] & 0xffff0000u);
+        vf[2 * k] = __uint_as_float(vw[k] << 16);
+        vf[2 * k + 1] = __uint_as_float(vw[k] & 0xffff0000u);
+      }
 #pragma unroll
-        for (int g = 0; g < kAttnMaxG; ++g)
-          if (g < G) acc[g] += a * sq[g][8 * v8 + 2 * k] + b * sq[g][8 * v8 + 2 * k + 1];
+      for (int g = 0; g < G; ++g) {
+        float sdot = 0.f;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) sdot = fmaf(qf[g][d], kf[d], sdot);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+        if (!ok[u]) continue;
+        // online softmax in base 2 (scores already carry log2 e)
+        const float mn = fmaxf(m[g], sdot);
+        const float corr = exp2f(m[g] - mn);  // m = -inf at first: exp2(-inf) = 0
+        const float pr = exp2f(sdot - mn);
+        l[g] = l[g] * corr + pr;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) acc[g][d] = fmaf(acc[g][d], corr, pr * vf[d]);
+        m[g] = mn;
       }
     }
-#pragma unroll
-    for (int g = 0; g < kAttnMaxG; ++g)
-      if (g < G) ss[g][i] = acc[g];
   }
-  __syncthreads();
 
-  // phase 2: per head max and sum of exp over the split
-  for (int g = 0; g < G; ++g) {
-    float m = -INFINITY;
-    for (int i = tid; i < n; i += kAttnThreads) m = fmaxf(m, ss[g][i]);
+  // merge the 8 streams (fixed order) through shared memory: (m, l) per stream and head, acc
+  __shared__ float sml[kStreams][G][2];
+  __shared__ __align__(16) float sacc[kStreams][G][kAttnD];
+  __shared__ bool s_last;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) red[g][warp] = m;
-  }
-  __syncthreads();
-  if (tid < G) {
-    float m = red[tid][0];
-    for (int w = 1; w < kAttnThreads / 32; ++w) m = fmaxf(m, red[tid][w]);
-    s_m[tid] = m;
-  }
-  __syncthreads();
   for (int g = 0; g < G; ++g) {
-    const float m = s_m[g];
-    float l = 0.f;
-    for (int i = tid; i < n; i += kAttnThreads) {
-      const float e = __expf(ss[g][i] - m);
-      ss[g][i] = e;
-      l += e;
+    if (hl == 0) {
+      sml[stream][g][0] = m[g];
+      sml[stream][g][1] = l[g];
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane == 0) red[g][warp] = l;
+    *reinterpret_cast<float4*>(&sacc[stream][g][8 * hl]) = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+    *reinterpret_cast<float4*>(&sacc[stream][g][8 * hl + 4]) = make_float4(acc[g][4], acc[g][5], acc[g][6], acc[g][7]);
   }
   __syncthreads();
-  if (tid < G) {
-    float l = 0.f;
-    for (int w = 0; w < kAttnThreads / 32; ++w) l += red[tid][w];
-    s_l[tid] = l;
+  float M[G], L[G], A[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    M[g] = -INFINITY;
+    for (int s2 = 0; s2 < kStreams; ++s2) M[g] = fmaxf(M[g], sml[s2][g][0]);
+    L[g] = 0.f;
+    A[g] = 0.f;
+    for (int s2 = 0; s2 < kStreams; ++s2) {
+      const float ms = sml[s2][g][0];
+      const float f = ms == -INFINITY ? 0.f : exp2f(ms - M[g]);
+      L[g] += f * sml[s2][g][1];
+      A[g] += f * sacc[s2][g][tid];
+    }
   }
-  __syncthreads();
-
-  // phase 3: P.V — warp w takes the tokens i = w (mod 4), lane the 4 dims [4 lane, 4 lane + 4)
-  // (8-byte loads, a warp reads a whole 256-byte V row); the 4 warp partials meet in smem
-  float pacc[kAttnMaxG][4];
+  if (n_splits == 1) {
 #pragma unroll
-  for (int g = 0; g < kAttnMaxG; ++g) pacc[g][0] = pacc[g][1] = pacc[g][2] = pacc[g][3] = 0.f;
-#pragma unroll 4
-  for (int i = warp; i < n; i += kAttnThreads / 32) {
-    const uint2 u = __ldg(reinterpret_cast<const uint2*>(kv_row(p.v_cache, j0 + i) + 4 * lane));
-    const float v0 = __uint_as_float(u.x << 16), v1 = __uint_as_float(u.x & 0xffff0000u);
-    const float v2 = __uint_as_float(u.y << 16), v3 = __uint_as_float(u.y & 0xffff0000u);
-#pragma unroll
-    for (int g = 0; g < kAttnMaxG; ++g)
-      if (g < G) {
-        const float pr = ss[g][i];
-        pacc[g][0] += pr * v0;
-        pacc[g][1] += pr * v1;
-        pacc[g][2] += pr * v2;
-        pacc[g][3] += pr * v3;
-      }
-  }
-  __shared__ __align__(16) float wacc[kAttnThreads / 32][kAttnMaxG][kAttnD];
-#pragma unroll
-  for (int g = 0; g < kAttnMaxG; ++g)
-    if (g < G)
-      *reinterpret_cast<float4*>(&wacc[warp][g][4 * lane]) =
-          make_float4(pacc[g][0], pacc[g][1], pacc[g][2], pacc[g][3]);
-  __syncthreads();
-  float acc[kAttnMaxG];
-#pragma unroll
-  for (int g = 0; g < kAttnMaxG; ++g)
-    acc[g] = g < G ? (wacc[0][g][tid] + wacc[1][g][tid]) + (wacc[2][g][tid] + wacc[3][g][tid]) : 0.f;
-
-  const int h0 = kvh * G;
-  if (n_splits == 1) {  // whole context in one split: normalise and store
-#pragma unroll
-    for (int g = 0; g < kAttnMaxG; ++g)
-      if (g < G) p.out[(size_t)t * p.ldo + (h0 + g) * kAttnD + tid] = __float2bfloat16_rn(acc[g] / s_l[g]);
+    for (int g = 0; g < G; ++g)
+      p.out[(size_t)t * p.ldo + (h0 + g) * kAttnD + tid] = __float2bfloat16_rn(A[g] / L[g]);
     return;
   }
-  // split partial: (m, l, acc) -> workspace; the last split CTA combines in split order
+  // split partial (m in base 2, l, acc) -> workspace; the last split CTA combines in split order
   const size_t stride_g = kAttnD + 2;
   float* mine = p.part + (((size_t)t * p.n_kv_heads + kvh) * p.max_splits + split) * G * stride_g;
 #pragma unroll
-  for (int g = 0; g < kAttnMaxG; ++g)
-    if (g < G) {
-      mine[g * stride_g + 2 + tid] = acc[g];
-      if (tid == 0) {
-        mine[g * stride_g] = s_m[g];
-        mine[g * stride_g + 1] = s_l[g];
-      }
+  for (int g = 0; g < G; ++g) {
+    mine[g * stride_g + 2 + tid] = A[g];
+    if (tid == 0) {
+      mine[g * stride_g] = M[g];
+      mine[g * stride_g + 1] = L[g];
     }
+  }
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -197,17 +188,18 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attention_kernel(const Att
   if (!s_last) return;
   __threadfence();
   const float* base = p.part + ((size_t)t * p.n_kv_heads + kvh) * p.max_splits * G * stride_g;
+#pragma unroll
   for (int g = 0; g < G; ++g) {
-    float M = -INFINITY;
-    for (int s = 0; s < n_splits; ++s) M = fmaxf(M, __ldcg(base + ((size_t)s * G + g) * stride_g));
-    float L = 0.f, A = 0.f;
-    for (int s = 0; s < n_splits; ++s) {
-      const float* b = base + ((size_t)s * G + g) * stride_g;
-      const float f = __expf(__ldcg(b) - M);
-      L += f * __ldcg(b + 1);
-      A += f * __ldcg(b + 2 + tid);
+    float Mx = -INFINITY;
+    for (int s2 = 0; s2 < n_splits; ++s2) Mx = fmaxf(Mx, __ldcg(base + ((size_t)s2 * G + g) * stride_g));
+    float Ls = 0.f, As = 0.f;
+    for (int s2 = 0; s2 < n_splits; ++s2) {
+      const float* b = base + ((size_t)s2 * G + g) * stride_g;
+      const float f = exp2f(__ldcg(b) - Mx);
+      Ls += f * __ldcg(b + 1);
+      As += f * __ldcg(b + 2 + tid);
     }
-    p.out[(size_t)t * p.ldo + (h0 + g) * kAttnD + tid] = __float2bfloat16_rn(A / L);
+    p.out[(size_t)t * p.ldo + (h0 + g) * kAttnD + tid] = __float2bfloat16_rn(As / Ls);
   }
 }
 

@@ -654,7 +654,10 @@ int collm_preload(void) {
   COLLM_PRELOAD(lora_reduce_kernel<48>);
   COLLM_PRELOAD(lora_apply_kernel);
   COLLM_PRELOAD((cross_entropy_kernel<8, 512>));
-  COLLM_PRELOAD(paged_attention_kernel);
+  COLLM_PRELOAD(paged_attention_kernel<1>);
+  COLLM_PRELOAD(paged_attention_kernel<2>);
+  COLLM_PRELOAD(paged_attention_kernel<4>);
+  COLLM_PRELOAD(paged_attention_kernel<8>);
   COLLM_PRELOAD((cross_entropy_kernel<0, 256>));
 #undef COLLM_PRELOAD
   return COLLM_OK;
@@ -901,8 +904,15 @@ int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_h
   p.max_splits = (max_ctx + kAttnSplit - 1) / kAttnSplit;
   p.counters = (int32_t*)workspace;
   p.part = (float*)((char*)workspace + (((size_t)T * n_kv_heads * 4 + 255) & ~(size_t)255));
-  paged_attention_kernel<<<dim3(T, n_kv_heads, p.max_splits), kAttnThreads, 0,
-                           (cudaStream_t)stream>>>(p);
+  const dim3 grid(T, n_kv_heads, p.max_splits);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (n_heads / n_kv_heads) {
+    case 1: paged_attention_kernel<1><<<grid, kAttnThreads, 0, st>>>(p); break;
+    case 2: paged_attention_kernel<2><<<grid, kAttnThreads, 0, st>>>(p); break;
+    case 4: paged_attention_kernel<4><<<grid, kAttnThreads, 0, st>>>(p); break;
+    case 8: paged_attention_kernel<8><<<grid, kAttnThreads, 0, st>>>(p); break;
+    default: return fail(COLLM_EINVAL, "GQA group %d not in {1, 2, 4, 8}", n_heads / n_kv_heads);
+  }
   CUDA_TRY(cudaGetLastError());
   return COLLM_OK;
 }
