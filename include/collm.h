@@ -123,9 +123,12 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
                     const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
                     const int32_t* lora_flag, const int32_t* gen, int lora_pdl, void* stream);
 
-/* Select the GEMM pipeline depth: lean != 0 -> ~128 KB shared memory per CTA so one CTA of the
- * LoRA kernels can run on the same SM concurrently (graph branch / second stream); 0 -> deepest
- * pipeline (default).  Process-wide setting. */
+/* Co-residence mode of the kernels (process-wide): 0 (default) -> deepest GEMM pipelines, default
+ * carveouts; 1 -> lean GEMM pipelines (~181 KB shared memory per CTA) and the rank-space kernels
+ * (shrink, K5) configured to fit next to a GEMM CTA (max-shared carveout, shallower K5 ring) — for
+ * a shrink running concurrently on a second stream next to GEMM CTAs that wait for it; 2 -> only
+ * the rank-space half of 1 (the programmatic-dependent-launch overlap: every shrink CTA is
+ * resident before its GEMM starts, so the GEMM keeps its deeper pipeline). */
 int collm_set_gemm_lean(int lean);
 
 /* ---- K5: LoRA weight-gradient reductions with fused AdamW ------------------------------------

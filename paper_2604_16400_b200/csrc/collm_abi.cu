@@ -359,8 +359,8 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (g_gemm_lean) {
-    // next to a lean GEMM ask for the max-shared carveout: an SM this kernel reaches first must
+  if (g_reduce_lean) {
+    // next to a GEMM ask for the max-shared carveout: an SM this kernel reaches first must
     // still fit a GEMM CTA; alone, keep the default (more L1)
     attr[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
     attr[na].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
@@ -664,7 +664,7 @@ int collm_preload(void) {
 }
 
 int collm_set_gemm_lean(int lean) {
-  g_gemm_lean = lean != 0;
+  g_gemm_lean = (lean & 1) != 0;  // 1: lean GEMM pipelines too; 2: rank-space kernels only
   g_reduce_lean = lean != 0;
   return COLLM_OK;
 }
