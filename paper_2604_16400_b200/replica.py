@@ -246,10 +246,13 @@ class ReplicaStack:
             self.advance_step(optimizer_step and backward and Ttr > 0)
         main = torch.cuda.current_stream(self.device)
         side = self._side_stream() if overlap else main
-        # pdl: every shrink CTA is resident before its GEMM launches, so the GEMM keeps its deep
-        # pipeline (2 = only the rank-space kernels fit themselves next to GEMM CTAs); flag: the
-        # side-stream shrink may need room next to GEMM CTAs spinning on its flag (1 = lean GEMMs)
-        _lib.load().collm_set_gemm_lean((2 if self.overlap_mode == "pdl" else 1) if overlap else 0)
+        # pdl: every shrink CTA is resident before its GEMM launches and the GEMM waits for nothing
+        # that needs SM room, so all kernels keep their standalone configuration (deep GEMM
+        # pipelines, default carveouts: measured 1.5-2 % faster than fitting a rank-space CTA next
+        # to each GEMM CTA); flag: the side-stream shrink may need room next to GEMM CTAs spinning
+        # on its flag (1 = lean GEMMs + max-shared carveouts)
+        lean = (0 if self.overlap_mode == "pdl" else 1) if overlap else 0
+        _lib.load().collm_set_gemm_lean(int(os.environ.get("COLLM_LEAN_MODE", lean)))
         n_sig = 0
 
         pdl = overlap and self.overlap_mode == "pdl"
