@@ -428,7 +428,8 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
 
   // N tile: 256 unless the sub-projection boundaries (or a narrow N) call for 128; stream-K
   // removes the wave-quantization reason to prefer narrower tiles.
-  const int sms = num_sms_cached();
+  static const int max_sms_env = [] { const char* e = getenv("COLLM_GEMM_MAX_SMS"); return e ? atoi(e) : 0; }();
+  const int sms = max_sms_env > 0 ? std::min(num_sms_cached(), max_sms_env) : num_sms_cached();  // debug cap
   auto aligned_to = [&](int t) {
     if (!lora || !sub_n_start) return true;
     for (int i = 1; i < n_sub; ++i)
