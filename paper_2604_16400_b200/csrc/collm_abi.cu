@@ -134,12 +134,12 @@ int max_gemm_clusters() {
   if (n < 0) {
     if (configure_gemm<BN, STAGES, CG, MC>()) return 0;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(num_sms_cached() / (CG * MC) * (CG * MC));
+    cfg.gridDim = dim3(num_sms_cached() / (CG * (MC == 1 ? 1 : 2)) * (CG * (MC == 1 ? 1 : 2)));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = GemmSmem<BN, STAGES, CG>::kTotal;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG * MC;
+    attr[0].val.clusterDim.x = CG * (MC == 1 ? 1 : 2);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -147,7 +147,7 @@ int max_gemm_clusters() {
     int c = 0;
     if (cudaOccupancyMaxActiveClusters(&c, gemm_lora_kernel<BN, STAGES, CG, MC>, &cfg) != cudaSuccess) {
       cudaGetLastError();
-      c = num_sms_cached() / (CG * MC);
+      c = num_sms_cached() / (CG * (MC == 1 ? 1 : 2));
     }
     n = c;
   }
@@ -162,10 +162,10 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   int rc = configure_gemm<BN, STAGES, CG, MC>();
   if (rc) return rc;
   if (MC > 1) {
-    const int cap = (CG * MC) * max_gemm_clusters<BN, STAGES, CG, MC>();
+    const int cap = (CG * (MC == 1 ? 1 : 2)) * max_gemm_clusters<BN, STAGES, CG, MC>();
     if (grid > cap)
       return fail(COLLM_EINVAL, "GEMM grid %d exceeds co-resident %d-CTA clusters (%d CTAs)", grid,
-                  CG * MC, cap);
+                  CG * (MC == 1 ? 1 : 2), cap);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -174,7 +174,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG * MC;
+  attr[0].val.clusterDim.x = CG * (MC == 1 ? 1 : 2);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   // PDL (opt-in, COLLM_GEMM_PDL=1): the prologue overlaps the previous grid of the stream (the
@@ -458,18 +458,21 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   int force_sched_eff = force_sched;
   for (int attempt = 0; attempt < 2 && best.cg == 0; ++attempt, force_sched_eff = -1)
   for (int cg : {2, 1})
-  for (int mc : {1, 2}) {
+  for (int mc : {1, 2, 3}) {
     if (force_cg && cg != force_cg) continue;
-    if (mc == 2 && cg != 2) continue;
+    if (mc != 1 && cg != 2) continue;
+    if (mc == 3 && force_mc != 3) continue;  // A-multicast clusters: opt-in (COLLM_GEMM_MC=3)
     if (force_mc && mc != force_mc && attempt == 0) continue;  // retry: any, like the schedule
-    const long long units = sms / cg;
+    const long long units = mc == 3 ? max_gemm_clusters<256, 6, 2, 3>() : sms / cg;
     const long long nmu = (M + kGemmBM * cg - 1) / (kGemmBM * cg);
     for (int b : {256, 128}) {
       if (force_bn && b != force_bn) continue;
       if (!aligned_to(b) || (b == 256 && N <= 128 && !force_bn)) continue;
       const double kb = cg == 2 ? (b == 256 ? 0.43 : 0.34) : (b == 256 ? 0.48 : 0.34);
-      const long long tiles = nmu * ((N + b - 1) / b);
+      const long long tiles = nmu * (((N + b - 1) / b + (mc == 3 ? 1 : 0)) / (mc == 3 ? 2 : 1));
+      if (mc == 3 && b != 256) continue;
       for (int sc : {0, 1, 4}) {
+        if (mc == 3 && sc != 0) continue;  // data-parallel only
         if (force_sched_eff >= 0 && (force_sched_eff == 2 ? 1 : force_sched_eff == 3 ? 0 : force_sched_eff) != sc) continue;
         double cost;
         if (sc == 4) {
@@ -518,7 +521,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   for (int i = 0; i < kMaxSub; ++i) p.sub_h_col[i] = 0;
 
   CUtensorMap ta, tb, th, tlb, ty;
-  int rc = make_tmap(&ta, A, K, M, lda, kGemmBK, kGemmBM);
+  int rc = make_tmap(&ta, A, K, M, lda, kGemmBK, mc == 3 ? kGemmBM / 2 : kGemmBM);
   if (rc) return rc;
   rc = make_tmap(&ty, Y, N, M, ldy, 32, 32);  // epilogue TMA stores, [32 x 32] boxes
   if (rc) return rc;
@@ -563,7 +566,9 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   // stream-K range non-empty)
   const long long min_work = (long long)nm * p.num_n_tiles * ((K + kGemmBK - 1) / kGemmBK);
   const int grid = sched == 4 ? cg * 2 * nm * p.num_n_tiles
-                              : cg * (int)std::min<long long>(sms / cg, min_work);
+                   : mc == 3 ? 4 * (int)std::min<long long>(max_gemm_clusters<256, 6, 2, 3>(),
+                                                            (long long)nm * ((p.num_n_tiles + 1) / 2))
+                             : cg * (int)std::min<long long>(sms / cg, min_work);
   p.sched = sched;
   p.lora_flag = lora ? lora_flag : nullptr;
   p.gen = gen;
@@ -596,6 +601,10 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   // LoRA kernels running concurrently on a second stream (collm_set_gemm_lean / COLLM_GEMM_LEAN)
   const char* lean_env = getenv("COLLM_GEMM_LEAN");
   const bool lean = lean_env ? atoi(lean_env) != 0 : g_gemm_lean;
+  if (mc == 3) {
+    if (lean) return launch_gemm<256, 5, 2, 3>(ta, tb, th, tlb, ty, p, grid, st);
+    return launch_gemm<256, 6, 2, 3>(ta, tb, th, tlb, ty, p, grid, st);
+  }
   if (mc == 2) {
     if (lean) {
       if (bn == 256) return launch_gemm<256, 5, 2, 2>(ta, tb, th, tlb, ty, p, grid, st);
@@ -646,6 +655,8 @@ int collm_preload(void) {
   COLLM_PRELOAD((gemm_lora_kernel<128, 8, 2, 2>));
   COLLM_PRELOAD((gemm_lora_kernel<256, 5, 2, 2>));
   COLLM_PRELOAD((gemm_lora_kernel<128, 6, 2, 2>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 6, 2, 3>));
+  COLLM_PRELOAD((gemm_lora_kernel<256, 5, 2, 3>));
   COLLM_PRELOAD((gemm_lora_kernel<256, 4, 1, 1>));
   COLLM_PRELOAD((gemm_lora_kernel<128, 6, 1, 1>));
   COLLM_PRELOAD((gemm_lora_kernel<256, 3, 1, 1>));

@@ -164,6 +164,20 @@ __device__ __forceinline__ void bulk_copy_s2cluster(uint32_t dst_cluster, const 
       : "memory");
 }
 
+// Pair TMA load multicast to the CTAs of `mask` (same smem offset in each); every destination's
+// bytes complete on the mbarrier at `bar`'s offset in the LEADER (even rank) of that destination's
+// pair — `bar` is this CTA's own barrier address with the pair (peer) bit cleared.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* smem_dst, const CUtensorMap* m,
+                                                    const void* bar, uint16_t mask, int32_t c0,
+                                                    int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask), "r"(c0),
+      "r"(c1)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05 / TMEM
 template <uint32_t kCols, int CG = 1>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {

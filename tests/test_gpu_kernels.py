@@ -29,7 +29,7 @@ def lib():
 
 
 GEMM_VARIANTS = [("1", "dp"), ("1", "hybrid"), ("2", "dp"), ("2", "hybrid"), ("2", "split2"),
-                 ("2", "dp", "2"), ("2", "hybrid", "2"), ("2", "split2", "2")]
+                 ("2", "dp", "2"), ("2", "hybrid", "2"), ("2", "split2", "2"), ("2", "dp", "3")]
 
 
 @pytest.fixture(params=GEMM_VARIANTS, ids=lambda v: f"cg{v[0]}-{v[1]}" + (f"-mc{v[2]}" if len(v) > 2 else ""))
@@ -37,7 +37,8 @@ def gemm_variant(request, monkeypatch):
     """Force each kernel variant (CTA or CTA-pair tiles; data-parallel, stream-K, or split-2
     where every tile's K is halved over two CTA pairs that swap half-tile partials — shapes
     with too many tiles for split-2 fall back to the cost model's choice; mc2: 4-CTA clusters of
-    two pairs multicasting their shared A boxes)."""
+    two pairs halving K (split-2 over DSMEM); mc3: 4-CTA clusters of two pairs on adjacent N tiles
+    multicasting their shared A boxes)."""
     monkeypatch.setenv("COLLM_GEMM_CG", request.param[0])
     monkeypatch.setenv("COLLM_GEMM_SCHED", request.param[1])
     monkeypatch.setenv("COLLM_GEMM_MC", request.param[2] if len(request.param) > 2 else "1")
