@@ -275,7 +275,7 @@ def run_ours(args, cfg, workload):
 
     flat_grad = None
     if not fused_opt:
-        flat_grad = stack.flatten_grads()
+        flat_grad = stack.flat_grad  # every projection's grads are views of this one buffer
 
     def sync_and_apply():
         if backend == "nccl":
@@ -293,14 +293,12 @@ def run_ours(args, cfg, workload):
         stack.capture(plan, optimizer_step=fused_opt)
     if not fused_opt:
         stack.opt.advance()
-        for p in stack.projections():
-            p.apply_optimizer(stack.opt)
+        stack.apply_optimizer()
         apply_graph = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(dev)
         s.wait_stream(st_dev)
         with torch.cuda.stream(s), torch.cuda.graph(apply_graph, stream=s):
-            for p in stack.projections():
-                p.apply_optimizer(stack.opt)
+            stack.apply_optimizer()
         st_dev.wait_stream(s)
 
     n0 = ops.launch_count()
@@ -382,7 +380,11 @@ def run_ours(args, cfg, workload):
         lora_ms = timed(gl.replay, reps, st_dev)
         n_gemm = sum(2 if Ttr else 1 for _ in stack.projections())
         achieved = step_flops / (gemm_ms / 1e3) / 1e12
-        peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+        # the GEMM-only graph is a short isolated burst (well under a second): the burst peak
+        # (cuBLAS 8192^3 best-of-10) is its comparator; the sustained (power-capped) peak is
+        # reported beside it
+        peak = peaks.get("bf16_tflops", peaks.get("bf16_tflops_sustained"))
+        peak_sus = peaks.get("bf16_tflops_sustained", peak)
         traffic = None
         tf = ROOT / "profiles" / "gemm_traffic.json"
         if tf.exists():
@@ -393,7 +395,8 @@ def run_ours(args, cfg, workload):
         out["roofline"] = {
             "bound": "tensor", "kernel": "gemm_lora_kernel (tcgen05, K2 fwd + K3 dX)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_source": f"{peaks_src} bf16_tflops_sustained",
+            "traffic": traffic, "peak_source": f"{peaks_src} bf16_tflops (burst)",
+            "peak_sustained": peak_sus, "frac_sustained": achieved / peak_sus,
             "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": n_gemm,
             "share_of_step": gemm_ms / ms_max}
         lb = stack.lora_bytes(plan)

@@ -78,7 +78,9 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
  * H[t, g.rank_off + j] = scale[a] * sum_{k in [g.k_lo, g.k_hi)} X[t,k] * A[a][g.rank_off + j, k]
  * for each shrink tile (rows of one adapter a; a = -1 -> no LoRA, zeros) and each rank group g
  * (groups: n_groups x 4 ints rank_off, n_ranks (multiple of 8, <= 64), k_lo, k_hi).  Outputs
- * (each optional): H32 fp32 [T, ldh]; H16 bf16 [T, ldh]; Hslots bf16 [n_slots*256, ldh] — the
+ * (each optional): H32 fp32 [T, ldh]; H16 bf16 [T, ldh]; H16lo bf16 [T, ldh] = bf16(h - H16), so
+ * H16 + H16lo carries the fp32 result to ~2^-16 relative (the backward's dH feeding the dA
+ * reduction: collm_reduce_group.V2); Hslots bf16 [n_slots*256, ldh] — the
  * GEMM's LoRA slot blocks, written completely: row t's value at row slot_of_row[t]*256 + t%256 and
  * zeros in the other slots of its 256-row slot tile (tile_slot_ptr).  One CTA per (tile, group) covers
  * the whole K range; the reduction is in-CTA and fixed-order (deterministic, no workspace).
@@ -90,7 +92,7 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
  * Replaces: the inference half of perf.true_infer_latency (perf.py:62-74). */
 int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
                       const int32_t* tiles, int n_tiles, const float* scale, const int32_t* groups,
-                      int n_groups, float* H32, void* H16, int ldh, void* Hslots,
+                      int n_groups, float* H32, void* H16, void* H16lo, int ldh, void* Hslots,
                       const int32_t* slot_of_row, const int32_t* tile_slot_ptr, int32_t* signal,
                       const int32_t* gen, void* stream);
 
@@ -137,7 +139,7 @@ int collm_set_gemm_lean(int lean);
  * (c_row_off+p)*ldc + c_col_off+q of grad / master / m / v and of out_same (bf16), and at
  * (t_row_off+q)*ld_trans + t_col_off+p of out_trans (bf16).  One launch serves up to 16 groups
  * — all projections of a layer (per projection: dB per sub-projection, U = dY, V = H16; dA^T in
- * <= 64-rank chunks, U = X_tr, V = dH16); all groups share T.
+ * <= 64-rank chunks, U = X_tr, V = dH16, V2 = dH16lo); all groups share T.
  * Replaces: AdapterParams.perturbed (launcher.py:43-47) and perf.train_step (perf.py:111-126). */
 typedef struct {
   const void* U;     /* bf16 [T, ldu] */
@@ -152,6 +154,7 @@ typedef struct {
   int u_off, P, v_off, Q;
   int ldc, ld_trans;
   int c_row_off, c_col_off, t_row_off, t_col_off;
+  const void* V2;    /* optional bf16 [T, ldv]: C = U^T (V + V2) (the lo half of a hi+lo pair) */
 } collm_reduce_group;
 
 /* mode STORE_GRAD: grad = C*grad_scale (+grad if accum_in).  mode ADAMW: the same gradient drives

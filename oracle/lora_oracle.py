@@ -1,9 +1,13 @@
 """numpy restatement of the unified PEFT layer — TEST INFRASTRUCTURE ONLY (see __init__.py).
 
-Every function restates one step of the algorithm the device path implements, with the same
-bf16 rounding points (inputs, the rank-space intermediates H = s.X.A^T and dH = s.dY.B, and the
-bf16 working copies of the adapter) and exact (float64) arithmetic everywhere else, so the device
-result must agree up to fp32 summation order and one rounding of the outputs.
+Every function restates one step of the algorithm the device path implements, with exact
+(float64) arithmetic apart from the rounding points that DEFINE the computed function: the bf16
+inputs, the forward's rank-space activation H16 = bf16(s.X.A^T) (the forward really multiplies
+B by the rounded H, so Y and dB = dY^T.H16 are exact derivatives of that function) and the bf16
+working copies of the adapter.  The backward's dH = s.dY.B_t is NOT rounded by default
+(``dh_mode="exact"``): the device carries it as a bf16 hi+lo pair into the dA reduction, so dA
+must match exact math to SURVEY §8(c)'s 1e-3; ``dh_mode="bf16"`` restates the single-rounding
+variant (round 1's device algorithm) for comparison.
 
 Reference anchors (/root/reference):
   * adapter layout  b_mat (d, r), a_mat (r, l), update = b_mat @ a_mat ... pkg/src/coserve/launcher.py:28-47
@@ -22,7 +26,7 @@ import numpy as np
 
 __all__ = [
     "bf16_round", "bf16_to_bits", "bits_to_f32", "build_rows", "expand_segments", "tile_slots",
-    "slot_of_row", "shrink_tiles", "lora_forward", "lora_backward", "adamw_step", "AdamWState",
+    "slot_of_row", "shrink_tiles", "lora_shrink", "lora_forward", "lora_backward", "adamw_step", "AdamWState",
     "fedavg", "AggregationError", "projection_flops", "cross_entropy", "paged_attention",
 ]
 
@@ -129,6 +133,25 @@ def _sub_bounds(sub_sizes):
     return b
 
 
+def lora_shrink(X, A, scale, row_adapter, chunk=4096):
+    """K1's restatement: H16[t] = bf16(scale[a] * X[t] . A[a]^T) for a = row_adapter[t] >= 0 (0
+    for base-only rows).  X [T, K], A [n_ad, R, K], float32 holding bf16 values; rows of one
+    adapter are processed in chunks (float64 products).  Returns float32 [T, R]."""
+    T = X.shape[0]
+    R = A.shape[1]
+    H16 = np.zeros((T, R), np.float32)
+    for a in np.unique(row_adapter):
+        if a < 0:
+            continue
+        rows = np.nonzero(row_adapter == a)[0]
+        Aa = A[a].astype(np.float64).T
+        for c in range(0, len(rows), chunk):
+            rr = rows[c:c + chunk]
+            H = float(scale[a]) * (X[rr].astype(np.float64) @ Aa)
+            H16[rr] = bf16_round(H.astype(np.float32))
+    return H16
+
+
 def lora_forward(X, W, A, B, scale, row_adapter, sub_sizes, r_pad):
     """Forward of one (possibly fused) LoRA projection over the mixed rows.
 
@@ -136,20 +159,17 @@ def lora_forward(X, W, A, B, scale, row_adapter, sub_sizes, r_pad):
     at s*r_pad), B [n_ad, N, r_pad], scale [n_ad]; all float32 holding bf16 values.
       H16[t]     = bf16(scale[a] * X[t] . A[a]^T)                       (a = row_adapter[t] >= 0)
       Y[t, n_s]  = X[t] . W[n_s]^T + H16[t, s*r_pad:(s+1)*r_pad] . B[a][n_s]^T
+    Rows are independent: pass X[rows], row_adapter[rows] to evaluate a subset of rows.
     Returns Y (float64, before the output rounding) and H16 (float32 bf16 values; 0 for a < 0).
     """
     X64 = X.astype(np.float64)
-    T = X.shape[0]
     bounds = _sub_bounds(sub_sizes)
-    R = len(sub_sizes) * r_pad
     Y = X64 @ W.astype(np.float64).T
-    H16 = np.zeros((T, R), np.float32)
+    H16 = lora_shrink(X, A, scale, row_adapter)
     for a in np.unique(row_adapter):
         if a < 0:
             continue
         rows = np.nonzero(row_adapter == a)[0]
-        H = float(scale[a]) * (X64[rows] @ A[a].astype(np.float64).T)
-        H16[rows] = bf16_round(H.astype(np.float32))
         for s in range(len(sub_sizes)):
             cols = slice(bounds[s], bounds[s + 1])
             Y[np.ix_(rows, np.arange(bounds[s], bounds[s + 1]))] += (
@@ -158,30 +178,43 @@ def lora_forward(X, W, A, B, scale, row_adapter, sub_sizes, r_pad):
     return Y, H16
 
 
-def lora_backward(dY, X_tr, H16_tr, W, A_t, B_t, s, sub_sizes, r_pad):
+def lora_backward(dY, X_tr, H16_tr, W, A_t, B_t, s, sub_sizes, r_pad, dh_mode="exact",
+                  dx_rows=None, chunk=2048):
     """Backward of the training rows (all on adapter t, scale s) through one projection.
 
-      dH16[:, sub s] = bf16(s * dY[:, n_s] . B_t[n_s])
-      dX             = dY . W + dH16 . A_t
+      dH[:, sub s]   = s * dY[:, n_s] . B_t[n_s]                  (dh_mode "bf16": rounded)
+      dX             = dY . W + dH . A_t
       dB[n_s]        = dY[:, n_s]^T . H16_tr[:, sub s]            ([N, r_pad], B_t's layout)
-      dA^T           = X_tr^T . dH16                              ([K, R], A_t^T's layout)
-    (d/dW of the frozen base is not formed.)  Returns float64 dX, dB, dAT and float32 dH16.
+      dA^T           = X_tr^T . dH                                ([K, R], A_t^T's layout)
+    (d/dW of the frozen base is not formed; the forward's H16 rounding is straight-through.)
+    The T reductions run over row chunks (float64 partial products); ``dx_rows`` restricts dX to
+    those rows (the dense dY.W term dominates the cost at BASELINE shapes).
+    Returns float64 dX ([len(dx_rows) or T, K]), dB, dAT and dH (float64; float32 bf16 values
+    in "bf16" mode).
     """
+    if dh_mode not in ("exact", "bf16"):
+        raise ValueError(f"dh_mode {dh_mode!r}")
     bounds = _sub_bounds(sub_sizes)
-    dY64 = dY.astype(np.float64)
     T = dY.shape[0]
     R = len(sub_sizes) * r_pad
-    dH16 = np.zeros((T, R), np.float32)
+    K = X_tr.shape[1]
+    dH = np.zeros((T, R), np.float64)
     dB = np.zeros((bounds[-1], r_pad))
-    for si in range(len(sub_sizes)):
-        ns = slice(bounds[si], bounds[si + 1])
-        rs = slice(si * r_pad, (si + 1) * r_pad)
-        dH = s * (dY64[:, ns] @ B_t[ns].astype(np.float64))
-        dH16[:, rs] = bf16_round(dH.astype(np.float32))
-        dB[ns] = dY64[:, ns].T @ H16_tr[:, rs].astype(np.float64)
-    dX = dY64 @ W.astype(np.float64) + dH16.astype(np.float64) @ A_t.astype(np.float64)
-    dAT = X_tr.astype(np.float64).T @ dH16.astype(np.float64)
-    return dX, dB, dAT, dH16
+    dAT = np.zeros((K, R))
+    Bt64 = B_t.astype(np.float64)
+    for c in range(0, T, chunk):
+        rr = slice(c, min(T, c + chunk))
+        dY64 = dY[rr].astype(np.float64)
+        for si in range(len(sub_sizes)):
+            ns = slice(bounds[si], bounds[si + 1])
+            rs = slice(si * r_pad, (si + 1) * r_pad)
+            d = s * (dY64[:, ns] @ Bt64[ns])
+            dH[rr, rs] = bf16_round(d.astype(np.float32)) if dh_mode == "bf16" else d
+            dB[ns] += dY64[:, ns].T @ H16_tr[rr, rs].astype(np.float64)
+        dAT += X_tr[rr].astype(np.float64).T @ dH[rr]
+    rows = np.arange(T) if dx_rows is None else np.asarray(dx_rows)
+    dX = dY[rows].astype(np.float64) @ W.astype(np.float64) + dH[rows] @ A_t.astype(np.float64)
+    return dX, dB, dAT, (dH.astype(np.float32) if dh_mode == "bf16" else dH)
 
 
 def projection_flops(T, T_tr, K, N):

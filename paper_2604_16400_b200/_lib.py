@@ -33,7 +33,8 @@ class ReduceGroup(C.Structure):
     _fields_ = [("U", _P), ("V", _P), ("grad", _P), ("master", _P), ("m", _P), ("v", _P),
                 ("out_same", _P), ("out_trans", _P), ("ldu", _I), ("ldv", _I), ("u_off", _I),
                 ("P", _I), ("v_off", _I), ("Q", _I), ("ldc", _I), ("ld_trans", _I),
-                ("c_row_off", _I), ("c_col_off", _I), ("t_row_off", _I), ("t_col_off", _I)]
+                ("c_row_off", _I), ("c_col_off", _I), ("t_row_off", _I), ("t_col_off", _I),
+                ("V2", _P)]
 
 
 _RGP = C.POINTER(ReduceGroup)
@@ -46,7 +47,7 @@ SIGNATURES: dict[str, tuple] = {
     "collm_preload": (_I, []),
     "collm_plan_segments": (_I, [_IP, _IP, _I, _I, _IP, _IP, _I, _IP, _IP, _I, _IP]),
     "collm_expand_segments": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P]),
-    "collm_lora_shrink": (_I, [_P, _I, _P, _LL, _I, _P, _I, _P, _IP, _I, _P, _P, _I, _P, _P,
+    "collm_lora_shrink": (_I, [_P, _I, _P, _LL, _I, _P, _I, _P, _IP, _I, _P, _P, _P, _I, _P, _P,
                                _P, _P, _P, _P]),
     "collm_cross_entropy": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _F, _P]),
     "collm_attention_workspace_bytes": (_SZ, [_I, _I, _I, _I]),

@@ -52,7 +52,10 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attention_kernel(const Att
   constexpr int kStreams = 2 * kAttnThreads / 32;  // 8 half-warps
   const int t = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
   const int pos = p.row_pos[t];
-  const int n_tok = pos + 1;
+  // a row_pos beyond max_ctx (host cannot check device positions) is clamped to the launched
+  // split count: the last split's combine always runs and restores its arrival counter, so one
+  // bad row never corrupts the shared workspace of later launches
+  const int n_tok = min(pos + 1, p.max_splits * kAttnSplit);
   const int n_splits = (n_tok + kAttnSplit - 1) / kAttnSplit;
   if (split >= n_splits) return;  // this row's context is shorter
   const int seq = p.row_seq[t];

@@ -288,10 +288,11 @@ static bool g_reduce_lean = false;
 
 int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride, int lda,
                       const int32_t* tiles, int n_tiles, const float* scale, const int32_t* groups,
-                      int n_groups, float* H32, void* H16, int ldh, void* Hslots,
+                      int n_groups, float* H32, void* H16, void* H16lo, int ldh, void* Hslots,
                       const int32_t* slot_of_row, const int32_t* tile_slot_ptr, int32_t* signal,
                       const int32_t* gen, void* stream) {
   CHECK_ARG(X && A && tiles && scale && groups, "null input");
+  CHECK_ARG(!H16lo || H16, "H16lo needs H16");
   CHECK_ARG(!signal == !gen, "signal and gen go together");
   CHECK_ARG(n_tiles >= 0, "n_tiles < 0");
   if (n_tiles == 0) return COLLM_OK;
@@ -325,6 +326,7 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
   }
   p.H32 = H32;
   p.H16 = (bf16*)H16;
+  p.H16lo = (bf16*)H16lo;
   p.ldh = ldh;
   p.Hslots = (bf16*)Hslots;
   p.slot_of_row = slot_of_row;
@@ -725,6 +727,7 @@ static int build_reduce_params(ReduceParams& p, const collm_reduce_group* abi_gr
     ReduceGroup gr;
     gr.U = (const bf16*)s.U;
     gr.V = (const bf16*)s.V;
+    gr.V2 = (const bf16*)s.V2;
     gr.grad = s.grad;
     gr.master = s.master;
     gr.m = s.m;
@@ -747,7 +750,7 @@ static int build_reduce_params(ReduceParams& p, const collm_reduce_group* abi_gr
     if (need_uv) {
       CHECK_ARG(gr.U && gr.V, "group %d: null U/V", g);
       CHECK_ARG(gr.u_off % 8 == 0 && gr.v_off % 8 == 0 && gr.ldu % 8 == 0 && gr.ldv % 8 == 0 &&
-                    aligned16(gr.U) && aligned16(gr.V),
+                    aligned16(gr.U) && aligned16(gr.V) && (!gr.V2 || aligned16(gr.V2)),
                 "group %d: U/V must be 16-byte aligned with x8 offsets/leading dimensions", g);
     }
     CHECK_ARG(gr.ldc >= gr.c_col_off + gr.Q, "group %d: ldc=%d too small", g, gr.ldc);

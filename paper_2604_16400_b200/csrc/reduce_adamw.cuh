@@ -4,7 +4,12 @@
 //   C[p, q] = sum_t U[t, u_off + p] * V[t, v_off + q]        (fp32 accumulation)
 //
 //   dB_s   = dY[:, n-range of sub s]^T . H16[:, s*r : (s+1)*r]     (P = N_s, Q = r)
-//   dA^T   = X^T . dH16                                            (P = K,   Q = R)
+//   dA^T   = X^T . (dH16 + dH16lo)                                 (P = K,   Q = R)
+//
+// A group may carry a second V operand V2 (same layout) reduced into the same accumulator:
+// C = U^T (V + V2).  The dA^T groups use it for the bf16 hi+lo pair of dH (the shrink writes
+// dH16 = bf16(dH) and dH16lo = bf16(dH - dH16)), so the gradient sees dH to ~2^-16 relative
+// instead of one bf16 rounding (LoRA grads within 1e-3 of the exact math).
 //
 // The trainable adapter's fp32 master copies live in these C layouts (B: [N, r], A^T: [K, R]),
 // so the optimizer is elementwise on the reduced tile; the bf16 working copies the forward and
@@ -43,6 +48,7 @@ enum ReduceMode : int {
 struct ReduceGroup {
   const bf16* U;
   const bf16* V;
+  const bf16* V2;  // optional second V operand (same ldv / v_off): C = U^T (V + V2)
   float* grad;
   float* master;
   float* m;
@@ -221,7 +227,7 @@ struct ReduceSmem {
   static constexpr size_t kTBytes = (size_t)QT * (kReducePT + 8) * 2;
   static constexpr size_t kEpi = kCBytes + kTBytes;
   static size_t total(int stages) {
-    const size_t pipe = (size_t)stages * (kUStage + kVStage);
+    const size_t pipe = (size_t)stages * (kUStage + 2 * kVStage);  // V and V2 rings
     return (pipe > kEpi ? pipe : kEpi) + 16;
   }
 };
@@ -234,6 +240,8 @@ __global__ void __launch_bounds__(kReduceThreads, 4) lora_reduce_kernel(const Re
   extern __shared__ __align__(16) uint8_t smem[];
   bf16 (*Us)[TC][S::kUP] = reinterpret_cast<bf16 (*)[TC][S::kUP]>(smem);
   bf16 (*Vs)[TC][S::kVP] = reinterpret_cast<bf16 (*)[TC][S::kVP]>(smem + ST * S::kUStage);
+  bf16 (*Vs2)[TC][S::kVP] =
+      reinterpret_cast<bf16 (*)[TC][S::kVP]>(smem + ST * (S::kUStage + S::kVStage));
   float (*Cs)[QT + 1] = reinterpret_cast<float (*)[QT + 1]>(smem);
   bf16 (*Ct)[PT + 8] = reinterpret_cast<bf16 (*)[PT + 8]>(smem + S::kCBytes);
   __shared__ int s_last;
@@ -253,6 +261,8 @@ __global__ void __launch_bounds__(kReduceThreads, 4) lora_reduce_kernel(const Re
   // per thread), V chunk = TC x QT (<= 1 vector per thread)
   const bf16* u_base = gr.U + gr.u_off + p0;
   const bf16* v_base = gr.V + gr.v_off;
+  const bool has_v2 = gr.V2 != nullptr;  // CTA-uniform
+  const bf16* v2_base = has_v2 ? gr.V2 + gr.v_off : gr.V;
   const size_t ldu = gr.ldu, ldv = gr.ldv;
   const int T = p.T;
   static_assert(TC * (PT / 8) == 2 * kReduceThreads, "U chunk: two vectors per thread");
@@ -274,6 +284,8 @@ __global__ void __launch_bounds__(kReduceThreads, 4) lora_reduce_kernel(const Re
       const int t = t0 + v_r;
       const bool ok = t < T && v_col_ok;
       cp_async_16(&Vs[stage][v_r][v_c], ok ? v_base + (size_t)t * ldv + v_c : gr.V, ok);
+      if (has_v2)
+        cp_async_16(&Vs2[stage][v_r][v_c], ok ? v2_base + (size_t)t * ldv + v_c : gr.V, ok);
     }
   };
 
@@ -306,10 +318,20 @@ __global__ void __launch_bounds__(kReduceThreads, 4) lora_reduce_kernel(const Re
                         &Vs[stage][kk + rr + ((mat & 1) ? 8 : 0)][(j + ((mat & 2) ? 1 : 0)) * 8]);
           mma_m16n8k16_bf16(d[j], a0, a1, a2, a3, b0, b1);
           mma_m16n8k16_bf16(d[j + 1], a0, a1, a2, a3, b2, b3);
+          if (has_v2) {
+            ldsm_x4_trans(b0, b1, b2, b3,
+                          &Vs2[stage][kk + rr + ((mat & 1) ? 8 : 0)][(j + ((mat & 2) ? 1 : 0)) * 8]);
+            mma_m16n8k16_bf16(d[j], a0, a1, a2, a3, b0, b1);
+            mma_m16n8k16_bf16(d[j + 1], a0, a1, a2, a3, b2, b3);
+          }
         } else {
           const int rr = lane & 7, mat = (lane >> 3) & 1;
           ldsm_x2_trans(b0, b1, &Vs[stage][kk + rr + mat * 8][j * 8]);
           mma_m16n8k16_bf16(d[j], a0, a1, a2, a3, b0, b1);
+          if (has_v2) {
+            ldsm_x2_trans(b0, b1, &Vs2[stage][kk + rr + mat * 8][j * 8]);
+            mma_m16n8k16_bf16(d[j], a0, a1, a2, a3, b0, b1);
+          }
         }
       }
     }

@@ -51,6 +51,7 @@ struct ShrinkParams {
   // outputs (any may be null)
   float* H32;
   bf16* H16;
+  bf16* H16lo;  // residual v - bf16(v) (with H16: a bf16 hi+lo pair carrying ~16 mantissa bits)
   int ldh;
   bf16* Hslots;  // [n_slots*256, ldh] — row (slot*256 + t%256)
   const int32_t* slot_of_row;
@@ -113,6 +114,7 @@ __device__ __forceinline__ void shrink_store(const ShrinkParams& p, const RowSlo
   if (has_adapter) {
     if (p.H32) p.H32[(size_t)t * p.ldh + col] = v;
     if (p.H16) p.H16[(size_t)t * p.ldh + col] = vb;
+    if (p.H16lo) p.H16lo[(size_t)t * p.ldh + col] = __float2bfloat16_rn(v - __bfloat162float(vb));
   }
   if (p.Hslots) {
     const bf16 zero = __float2bfloat16_rn(0.f);

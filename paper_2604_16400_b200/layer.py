@@ -146,6 +146,7 @@ class LoraProjection:
         self._H16: torch.Tensor | None = None
         self._Hslots: torch.Tensor | None = None
         self._dH16: torch.Tensor | None = None
+        self._dH16lo: torch.Tensor | None = None
 
     # ------------------------------------------------------------------ weights / registry
     def refresh_transpose(self) -> None:
@@ -211,9 +212,16 @@ class LoraProjection:
         return self._H16, self._Hslots
 
     def _dh_buffer(self, T: int) -> torch.Tensor:
+        """dH = s.dY.B_t as a bf16 hi+lo pair: ``_dH16`` (hi, the dX GEMM's LoRA operand) and
+        ``_dH16lo`` = bf16(dH - hi) (the dA reduction adds it: X^T (hi + lo))."""
         if self._dH16 is None or self._dH16.shape[0] < T:
             self._dH16 = torch.zeros(T, self.spec.R, dtype=torch.bfloat16, device=self.device)
+            self._dH16lo = torch.zeros(T, self.spec.R, dtype=torch.bfloat16, device=self.device)
         return self._dH16[:T]
+
+    def _dh_lo(self, T: int) -> torch.Tensor:
+        self._dh_buffer(T)
+        return self._dH16lo[:T]
 
     # ------------------------------------------------------------------ hot path
     def forward(self, X: torch.Tensor, plan: DevicePlan, Y: torch.Tensor | None = None,
@@ -221,6 +229,14 @@ class LoraProjection:
         """K1 + K2 over all rows of the pass: Y = X.W^T + per-row s_a.(X.A_a^T).B_a^T."""
         cache = self.forward_lora(X, plan, n_train)
         return self.forward_gemm(cache, plan, Y), cache
+
+    def _check_plan(self, plan: DevicePlan) -> None:
+        # the kernels index A / B / scale by adapter id: an unknown tenant must be a
+        # ConfigurationError, not an out-of-bounds read
+        if plan.max_adapter >= self.n_adapters:
+            raise ConfigurationError(
+                f"{self.spec.name}: adapter {plan.max_adapter} is not a registered slot "
+                f"(n_adapters={self.n_adapters})")
 
     def forward_lora(self, X: torch.Tensor, plan: DevicePlan, n_train: int = 0,
                      signal: tuple | None = None) -> ForwardCache:
@@ -231,6 +247,7 @@ class LoraProjection:
         T = plan.n_rows
         if X.shape[0] < T or X.shape[1] != spec.in_features:
             raise ConfigurationError(f"{spec.name}: X {tuple(X.shape)} vs T={T}, K={spec.in_features}")
+        self._check_plan(plan)
         H16, Hslots = self._buffers(T, plan.n_slots)
         R, K = spec.R, spec.in_features
         if plan.n_slots:
@@ -256,6 +273,7 @@ class LoraProjection:
         if Y is None:
             Y = torch.empty(T, spec.out_features, dtype=torch.bfloat16, device=self.device)
         rp = spec.r_pad
+        self._check_plan(plan)
         if plan.n_slots:
             Hs = self._Hslots[: plan.n_slots * TILE_M]
             bnd = spec.sub_bounds
@@ -271,9 +289,11 @@ class LoraProjection:
             ops.gemm_lora(X, self.W, Y, M=T)
         return Y
 
-    def _grad_groups(self, dY=None, X_tr=None, H_tr=None, dH16=None, *, targets: str):
+    def _grad_groups(self, dY=None, X_tr=None, H_tr=None, dH16=None, dH16lo=None, *,
+                     targets: str):
         """The K5 group table of this projection: dB per sub-projection (U = dY, V = H16) and
-        dA^T in <=64-wide rank chunks (U = X_tr, V = dH16), with their optimizer targets."""
+        dA^T in <=64-wide rank chunks (U = X_tr, V = dH16 hi, V2 = dH16lo), with their optimizer
+        targets."""
         st = self.train_state
         spec = self.spec
         K, N, R, rp = spec.in_features, spec.out_features, spec.R, spec.r_pad
@@ -290,7 +310,7 @@ class LoraProjection:
                 t_col_off=bnd[s]))
         for q in range(0, R, 64):
             groups.append(ops.reduce_group(
-                X_tr, dH16, u_off=0, P=K, v_off=q, Q=min(64, R - q), ldc=R, c_col_off=q,
+                X_tr, dH16, V2=dH16lo, u_off=0, P=K, v_off=q, Q=min(64, R - q), ldc=R, c_col_off=q,
                 grad=st.grad_AT, master=st.master_AT if full else None,
                 m=st.m_AT if full else None, v=st.v_AT if full else None,
                 out_same=st.AT16 if full else None, out_trans=self.A[st.adapter] if full else None,
@@ -323,7 +343,8 @@ class LoraProjection:
 
     def backward_dh(self, dY: torch.Tensor, cache: ForwardCache, train_plan: DevicePlan,
                     signal: tuple | None = None) -> torch.Tensor:
-        """K1: dH = s * dY . B_t, one rank group per sub-projection (its own N range)."""
+        """K1: dH = s * dY . B_t (bf16 hi + lo), one rank group per sub-projection (its own N
+        range)."""
         st = self._require_train()
         spec = self.spec
         Ttr = cache.n_train
@@ -333,7 +354,7 @@ class LoraProjection:
         groups = [(s * rp + g, min(64, rp - g), bnd[s], bnd[s + 1])
                   for s in range(len(spec.subs)) for g in range(0, rp, 64)]
         ops.lora_shrink(dY, st.BT16, train_plan.shrink_tiles, train_plan.n_shrink_tiles,
-                        self.scale, groups, R, a_stride=0, H16=dH16,
+                        self.scale, groups, R, a_stride=0, H16=dH16, H16lo=self._dh_lo(Ttr),
                         signal=signal[0] if signal else None, gen=signal[1] if signal else None)
         return dH16
 
@@ -362,13 +383,14 @@ class LoraProjection:
         self._require_train()
         Ttr = cache.n_train
         dH16 = self._dh_buffer(Ttr)
-        return self._grad_groups(dY, cache.X[:Ttr], cache.H16[:Ttr], dH16,
+        return self._grad_groups(dY, cache.X[:Ttr], cache.H16[:Ttr], dH16, self._dh_lo(Ttr),
                                  targets="full" if optimizer is not None else "grad")
 
     def backward_grads(self, dY: torch.Tensor, cache: ForwardCache, *,
                        optimizer: OptimizerState | None = None, accumulate: bool = False,
                        grad_scale: float = 1.0) -> None:
-        """K5: dB = dY^T . H16 (per sub), dA^T = X^T . dH16 — one launch, fused AdamW or store."""
+        """K5: dB = dY^T . H16 (per sub), dA^T = X^T . (dH16 + dH16lo) — one launch, fused AdamW
+        or store."""
         rg = self.grad_groups(dY, cache, optimizer=optimizer)
         mode = _lib.MODE_ADAMW if optimizer is not None else _lib.MODE_STORE_GRAD
         ops.lora_reduce(cache.n_train, rg, mode, accum_in=accumulate, grad_scale=grad_scale,
@@ -419,16 +441,21 @@ class LMHead:
 
     def forward_backward(self, X: torch.Tensor, labels: torch.Tensor, dX: torch.Tensor,
                          n_valid: int | None = None) -> torch.Tensor:
-        """Mean CE of the rows of X [T, h] against labels [T] (int32, < 0 ignored) and its
-        gradient w.r.t. X into dX [T, h].  Returns the device loss (fp32 [1]); all on the current
-        stream, nothing read back."""
+        """Mean CE of the rows of X [T, h] against labels [T] (int32, < 0 or >= V ignored) and
+        its gradient w.r.t. X into dX [T, h].  Returns the device loss (fp32 [1]).  The gradient is
+        that of the reported mean, so it is scaled by 1 / n_valid (the count of non-ignored
+        labels); pass ``n_valid`` when the caller knows it (the step path does) — otherwise it is
+        counted here from the device labels, which reads one scalar back (a host sync)."""
         T = labels.shape[0]
         if X.shape[0] < T or X.shape[1] != self.hidden or dX.shape[0] < T:
             raise ConfigurationError(f"LM head: X {tuple(X.shape)} / dX {tuple(dX.shape)} vs T={T}")
         if T == 0:
             raise ConfigurationError("LM head: no training rows")
         b = self._buffers(T)
-        n = T if n_valid is None else n_valid
+        if n_valid is None:
+            n = int(((labels >= 0) & (labels < self.vocab)).sum().item())
+        else:
+            n = n_valid
         ops.gemm_lora(X, self.W, b["logits"], M=T)
         ops.cross_entropy(b["logits"], labels, self.vocab, loss_rows=b["loss_rows"],
                           loss_mean=b["loss"], counter=b["counter"], dlogits=b["dlogits"],

@@ -116,11 +116,13 @@ _gemm_ws = Workspace()
 def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: int,
                 scale: torch.Tensor, groups: list[tuple[int, int, int, int]], ldh: int, *,
                 a_stride: int | None = None, H32: torch.Tensor | None = None,
-                H16: torch.Tensor | None = None, Hslots: torch.Tensor | None = None,
+                H16: torch.Tensor | None = None, H16lo: torch.Tensor | None = None,
+                Hslots: torch.Tensor | None = None,
                 slot_of_row: torch.Tensor | None = None,
                 tile_slot_ptr: torch.Tensor | None = None, signal: torch.Tensor | None = None,
                 gen: torch.Tensor | None = None) -> None:
     """K1: H[t, ranks of g] = scale[a] * X[t, K-range of g] . A_a[ranks of g]^T (see collm.h).
+    ``H16lo``: also write bf16(h - H16), the lo half of a bf16 hi+lo pair.
     ``signal``/``gen``: publish completion for a GEMM consuming the output on another stream."""
     _need(X, torch.bfloat16, "X")
     _need(A, torch.bfloat16, "A")
@@ -132,7 +134,7 @@ def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: 
     flat = [v for g in groups for v in g]
     _lib.call("collm_lora_shrink", X.data_ptr(), X.stride(0), A.data_ptr(), int(a_stride), lda,
               tiles.data_ptr(), n_tiles, scale.data_ptr(), _lib.int_array(flat), len(groups),
-              _p(H32), _p(H16), ldh, _p(Hslots), _p(slot_of_row), _p(tile_slot_ptr), _p(signal),
+              _p(H32), _p(H16), _p(H16lo), ldh, _p(Hslots), _p(slot_of_row), _p(tile_slot_ptr), _p(signal),
               _p(gen), _stream())
 
 
@@ -187,12 +189,15 @@ def reduce_tsplit(T: int, n_tiles: int, device: torch.device) -> int:
 
 def reduce_group(U=None, V=None, *, u_off=0, P, v_off=0, Q, ldc, c_row_off=0, c_col_off=0,
                  grad=None, master=None, m=None, v=None, out_same=None, out_trans=None,
-                 ld_trans=0, t_row_off=0, t_col_off=0) -> _lib.ReduceGroup:
-    """One ``collm_reduce_group``: C[p,q] = sum_t U[t,u_off+p] V[t,v_off+q] and its targets."""
+                 ld_trans=0, t_row_off=0, t_col_off=0, V2=None) -> _lib.ReduceGroup:
+    """One ``collm_reduce_group``: C[p,q] = sum_t U[t,u_off+p] (V + V2)[t,v_off+q] and its
+    targets (``V2`` optional, same layout as V: the lo half of a bf16 hi+lo pair)."""
+    if V2 is not None and (V is None or V2.stride(0) != V.stride(0)):
+        raise ValueError("V2 must have V's layout")
     return _lib.ReduceGroup(
         _p(U), _p(V), _p(grad), _p(master), _p(m), _p(v), _p(out_same), _p(out_trans),
         U.stride(0) if U is not None else 0, V.stride(0) if V is not None else 0,
-        u_off, P, v_off, Q, ldc, ld_trans, c_row_off, c_col_off, t_row_off, t_col_off)
+        u_off, P, v_off, Q, ldc, ld_trans, c_row_off, c_col_off, t_row_off, t_col_off, _p(V2))
 
 
 def lora_reduce(T: int, groups: list, mode: int, *, accum_in: bool = False,

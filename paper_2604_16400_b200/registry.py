@@ -32,8 +32,9 @@ class AdapterPager:
         self.stack = stack
         self.projs: list[LoraProjection] = list(stack.projections())
         self.n_slots = stack.cfg.n_adapters
-        # the trainable adapter's slot is never evicted (its masters / optimizer state live there)
-        self.pinned = set(pinned_slots if pinned_slots is not None else (stack.cfg.train_adapter,))
+        # trainable adapters' slots are never evicted (their masters / optimizer state live there)
+        self.pinned = set(pinned_slots if pinned_slots is not None
+                          else (t.slot for t in stack.trainers.values()))
         self.host: dict[object, list[tuple[torch.Tensor, torch.Tensor, torch.Tensor]]] = {}
         self.slot_of: collections.OrderedDict = collections.OrderedDict()  # adapter id -> slot, LRU
         self.held: list[object | None] = [None] * self.n_slots
@@ -160,8 +161,7 @@ def broadcast_adapter(stack, src: int = 0, group=None) -> None:
     bf16 copies (collm_lora_apply COPY_ONLY).  The reference stores the aggregate but never pushes
     it back (engine.py:468-480); this closes that loop."""
     import torch.distributed as dist
-    flat = stack.flat_master if getattr(stack, "flat_master", None) is not None else stack.flatten_masters()
+    flat = stack.flat_master  # built once with the trainer (never re-homed behind a graph)
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.broadcast(flat, src=src, group=group)
-    for p in stack.projections():
-        p.refresh_from_master()
+    stack.refresh_from_master()

@@ -26,10 +26,25 @@ import torch
 from . import _lib, ops
 from .configs import LayerConfig
 from .domain import ConfigurationError, InferenceItem, MixedBatch, TrainItem
-from .layer import AdamWConfig, LMHead, LoraProjection, OptimizerState
+from .layer import AdamWConfig, LMHead, LoraProjection, OptimizerState, TrainState
 from .segments import DevicePlan, HostPlan, build_mixed_batch, plan_segments, uniform_plan
 
 ENTRY = ("qkv", "q", "k", "v", "gate_up", "gate", "up")
+
+
+@dataclass
+class Trainer:
+    """One trainable adapter of the replica (the reference's per-replica ``adapter``,
+    engine.py:92, trained by that replica's FL client): its device slot, the per-projection fp32
+    masters / AdamW moments / gradients (re-homed at creation into ONE flat master buffer and ONE
+    flat gradient buffer, so a cross-replica sync is a single collective) and its optimizer step."""
+
+    key: object
+    slot: int
+    states: list[TrainState]
+    opt: OptimizerState
+    flat_master: torch.Tensor
+    flat_grad: torch.Tensor
 
 
 @dataclass
@@ -63,12 +78,14 @@ class ReplicaStack:
         # (dY_top = its dX) and gives the step's training loss; without it dY_top is synthetic
         self.head = LMHead(cfg.model.hidden, cfg.model.vocab, self.device) if lm_head else None
         self._loss: torch.Tensor | None = None
-        self.opt = OptimizerState(optimizer, self.device)
+        self.optimizer_cfg = optimizer
+        self.trainers: dict[object, Trainer] = {}
+        self.active: Trainer | None = None
         self.seed = seed
+        self._graph: torch.cuda.CUDAGraph | None = None
         if init:
             self.init_synthetic(seed)
         self._acts: dict | None = None
-        self._graph: torch.cuda.CUDAGraph | None = None
         self._side: torch.cuda.Stream | None = None
         self.overlap = False
         # how a projection's shrink overlaps its GEMM: "pdl" (default) = same stream, the GEMM
@@ -106,68 +123,129 @@ class ReplicaStack:
                     b.normal_(0.0, 0.02, generator=g)
                     proj.B[:, bnd[s]:bnd[s + 1], :r] = b.to(torch.bfloat16)
                 proj.scale.fill_(sp.alpha / r)
-                proj.make_trainable(self.cfg.train_adapter)
         if self.head is not None:
             self.head.W.normal_(0.0, 0.02, generator=g)
             self.head.refresh_transpose()
+        self.trainers.clear()
+        self.add_trainer("default", self.cfg.train_adapter)
+
+    # ------------------------------------------------------------------ trainable adapters
+    @property
+    def opt(self) -> OptimizerState:
+        return self._require_trainer().opt
+
+    @property
+    def train_slot(self) -> int:
+        return self._require_trainer().slot
+
+    def _require_trainer(self) -> Trainer:
+        if self.active is None:
+            raise ConfigurationError("no trainable adapter (add_trainer)")
+        return self.active
+
+    def add_trainer(self, key, slot: int, copy_from: int | None = None) -> Trainer:
+        """Start fine-tuning device slot ``slot`` as trainer ``key``: fp32 masters from the slot's
+        bf16 weights (after copying adapter ``copy_from``'s weights into it, when given), fresh
+        AdamW state, and the flat master / gradient buffers — built here, once, so nothing later
+        re-homes tensors a captured graph points at.  The new trainer becomes the active one."""
+        if not 0 <= slot < self.cfg.n_adapters:
+            raise ConfigurationError(f"trainer slot {slot} outside [0, {self.cfg.n_adapters})")
+        if any(t.slot == slot and k != key for k, t in self.trainers.items()):
+            raise ConfigurationError(f"slot {slot} is already trained by another trainer")
+        if self._graph is not None:
+            raise ConfigurationError("add trainers before capturing a graph")
+        states = []
+        with torch.no_grad():
+            for p in self.projections():
+                if copy_from is not None and copy_from != slot:
+                    p.A[slot].copy_(p.A[copy_from])
+                    p.B[slot].copy_(p.B[copy_from])
+                    p.scale[slot:slot + 1].copy_(p.scale[copy_from:copy_from + 1])
+                states.append(p.make_trainable(slot))
+        flat_m = self._flatten(states, ("master_B", "master_AT"), copy=True)
+        flat_g = self._flatten(states, ("grad_B", "grad_AT"), copy=False)
+        tr = Trainer(key, slot, states, OptimizerState(self.optimizer_cfg, self.device), flat_m,
+                     flat_g)
+        self.trainers[key] = tr
+        self.use_trainer(key)
+        return tr
+
+    def use_trainer(self, key) -> Trainer:
+        """Make trainer ``key`` the one the next steps train (eager steps; a captured graph is
+        bound to the trainer active at capture)."""
+        tr = self.trainers.get(key)
+        if tr is None:
+            raise ConfigurationError(f"unknown trainer {key!r}")
+        for p, st in zip(self.projections(), tr.states):
+            p.train_state = st
+        self.active = tr
+        return tr
+
+    def _flatten(self, states, names, copy: bool) -> torch.Tensor:
+        total = sum(getattr(st, n).numel() for st in states for n in names)
+        flat = torch.zeros(total, dtype=torch.float32, device=self.device)
+        off = 0
+        for st in states:
+            for n in names:
+                t = getattr(st, n)
+                view = flat[off:off + t.numel()].view(t.shape)
+                if copy:
+                    view.copy_(t)
+                setattr(st, n, view)
+                off += t.numel()
+        return flat
 
     def projections(self):
         for layer in self.layers:
             yield from layer
 
     def trainable_tensors(self, which: str = "master") -> list[torch.Tensor]:
-        """The trainable adapter's fp32 tensors across the stack (for cross-replica sync):
+        """The active trainer's fp32 tensors across the stack (for cross-replica sync):
         'master' = parameters (fedavg mode), 'grad' = gradients (grad-sync mode)."""
         out = []
-        for p in self.projections():
-            st = p.train_state
-            if which == "master":
-                out += [st.master_B, st.master_AT]
-            else:
-                out += [st.grad_B, st.grad_AT]
+        for st in self._require_trainer().states:
+            out += [st.master_B, st.master_AT] if which == "master" else [st.grad_B, st.grad_AT]
         return out
 
-    def flatten_grads(self) -> torch.Tensor:
-        """Re-home every projection's gradient buffers as views of ONE flat fp32 tensor, so the
-        cross-replica sync is a single NCCL allreduce (call before capturing a graph)."""
-        states = [p.train_state for p in self.projections()]
-        total = sum(st.grad_B.numel() + st.grad_AT.numel() for st in states)
-        flat = torch.zeros(total, dtype=torch.float32, device=self.device)
-        off = 0
-        for st in states:
-            for name in ("grad_B", "grad_AT"):
-                t = getattr(st, name)
-                setattr(st, name, flat[off:off + t.numel()].view(t.shape))
-                off += t.numel()
-        self.flat_grad = flat
-        return flat
+    @property
+    def flat_grad(self) -> torch.Tensor:
+        """The active trainer's gradients as ONE flat fp32 buffer (every projection's grad_B /
+        grad_AT are views of it): the cross-replica sync is a single NCCL allreduce."""
+        return self._require_trainer().flat_grad
 
-    def flatten_masters(self) -> torch.Tensor:
-        """Same for the fp32 master parameters (fedavg parameter-averaging mode)."""
-        states = [p.train_state for p in self.projections()]
-        total = sum(st.master_B.numel() + st.master_AT.numel() for st in states)
-        flat = torch.empty(total, dtype=torch.float32, device=self.device)
-        off = 0
-        for st in states:
-            for name in ("master_B", "master_AT"):
-                t = getattr(st, name)
-                flat[off:off + t.numel()].copy_(t.reshape(-1))
-                setattr(st, name, flat[off:off + t.numel()].view(t.shape))
-                off += t.numel()
-        self.flat_master = flat
-        return flat
+    @property
+    def flat_master(self) -> torch.Tensor:
+        """The active trainer's fp32 master parameters as ONE flat buffer (fedavg mode)."""
+        return self._require_trainer().flat_master
+
+    def refresh_from_master(self) -> None:
+        """Rewrite every bf16 copy of the active trainer's adapter from its fp32 masters (after
+        an average / broadcast of ``flat_master``)."""
+        for p in self.projections():
+            p.refresh_from_master()
+
+    def apply_optimizer(self) -> None:
+        """AdamW of the active trainer from its (e.g. allreduced) gradient buffers, on the
+        current stream, using the step ``opt.advance()`` already set."""
+        for p in self.projections():
+            p.apply_optimizer(self.opt)
 
     # ------------------------------------------------------------------ plans
     def plan(self, train: TrainItem | None, items: list[InferenceItem]) -> StepPlan:
+        for it in items:
+            if it.adapter >= self.cfg.n_adapters:
+                raise ConfigurationError(
+                    f"request {it.request_id}: adapter {it.adapter} is not a registered slot "
+                    f"(n_adapters={self.cfg.n_adapters})")
         mb = build_mixed_batch(train, items)
         hp = plan_segments(mb.seg_start, mb.seg_adapter)
         dp = DevicePlan(hp, self.device, expand=False)
         th = td = None
         if mb.n_train_rows:
-            if mb.train_adapter != self.cfg.train_adapter:
+            if mb.train_adapter != self.train_slot:
                 raise ConfigurationError(
                     f"training rows use adapter {mb.train_adapter}, the replica trains "
-                    f"{self.cfg.train_adapter}")
+                    f"{self.train_slot}")
             th = uniform_plan(mb.n_train_rows, mb.train_adapter)
             td = DevicePlan(th, self.device)
         return StepPlan(mb, hp, dp, th, td)
@@ -213,6 +291,7 @@ class ReplicaStack:
             # next-token targets of the training rows (synthetic token ids; no dataset offline)
             acts["labels"] = torch.randint(0, self.cfg.model.vocab, (Ttr,), device=dev,
                                            generator=g, dtype=torch.int32)
+            acts["n_valid"] = Ttr  # every synthetic target is a real token id
         self._acts = acts
         self._plan = plan
         return acts
@@ -301,7 +380,8 @@ class ReplicaStack:
                 prev = after(main)
         if Ttr and backward and self.head is not None:
             # K2 logits -> K7 softmax-CE fwd+bwd -> K3 dX: the real dY entering the top layer
-            self._loss = self.head.forward_backward(a["X"][L][:Ttr], a["labels"], a["dY_top"])
+            self._loss = self.head.forward_backward(a["X"][L][:Ttr], a["labels"], a["dY_top"],
+                                                    n_valid=a.get("n_valid"))
         if Ttr and backward:
             opt = self.opt if optimizer_step else None
             mode = _lib.MODE_ADAMW if opt is not None else _lib.MODE_STORE_GRAD

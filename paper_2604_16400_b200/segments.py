@@ -145,6 +145,7 @@ class DevicePlan:
         self.slot_adapter = buf[offs[3]:offs[4]]
         self.shrink_tiles = buf[offs[4]:offs[5]]
         self.n_slots = host.n_slots
+        self.max_adapter = int(host.seg_adapter.max()) if host.seg_adapter.size else -1
         self.n_shrink_tiles = int(host.shrink_tiles.shape[0])
         self.row_adapter = torch.empty(self.n_rows, dtype=torch.int32, device=dev)
         self.slot_of_row = torch.empty(self.n_rows, dtype=torch.int32, device=dev)

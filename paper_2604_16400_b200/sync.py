@@ -4,7 +4,7 @@ Each GPU is an independent replica (one process per GPU, ``torch.distributed`` w
 NVLink/NVSwitch).  Replicas fine-tuning the same adapter exchange it in one of two ways:
 
 * ``grad`` mode (north star): every optimizer step, the flat fp32 LoRA-gradient buffer of the
-  trainable adapter (all layers, all projections — :meth:`ReplicaStack.flatten_grads`) is
+  trainable adapter (all layers, all projections — :attr:`ReplicaStack.flat_grad`) is
   averaged with ONE ``all_reduce(AVG)``; then the AdamW apply kernel runs on every replica, so
   all replicas keep identical adapters.
 * ``fedavg`` mode (reference semantics, /root/reference/pkg/src/coserve/launcher.py:68-80 called

@@ -80,7 +80,7 @@ class _FakeProj:
 
 
 class _FakeStack:
-    """The two members broadcast_adapter uses: the flat fp32 masters and the projections."""
+    """The members broadcast_adapter uses: the flat fp32 masters and the bf16-copy refresh."""
 
     def __init__(self, flat):
         self.flat_master = flat
@@ -88,6 +88,10 @@ class _FakeStack:
 
     def projections(self):
         return iter(self._p)
+
+    def refresh_from_master(self):
+        for p in self._p:
+            p.refresh_from_master()
 
 
 def _bcast_worker(rank, world, port, q):

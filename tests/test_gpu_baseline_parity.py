@@ -1,0 +1,161 @@
+"""GPU parity at the BASELINE shapes: one full layer of each BASELINE config (Llama-2-7B r=16 x 32
+adapters, Llama-3-8B r=32 x 64 adapters prefill-heavy, Llama-2-13B r=64 training-heavy) through
+the real step (``ReplicaStack.run_step``: every projection, forward of all rows, dH + dX + the
+per-layer K5 reduction) against the float64 oracle on the same bf16 inputs — the slot plans
+(16 slots per 256-row tile at 7B, 64 adapters at 8B), the GEMM schedules chosen at those shapes
+(split-2 / stream-K / data-parallel) and 13B's rank groups (R = 192) and <=48-wide K5 chunks are
+exactly the ones the bench measures.
+
+Tolerances (stated here):
+  * H16 (forward rank space, all rows): rel. Frobenius <= 4e-3 (one bf16 rounding);
+  * Y, dX (bf16 out, fp32 accumulation) on sampled rows covering every segment boundary, every
+    256-row slot tile and random interior rows: |err|_inf <= 1e-2 |ref|_inf + 1e-3 and
+    rel. Frobenius <= 4e-3;
+  * dB, dA^T (fp32, all training rows) vs EXACT math (the oracle's dH is not rounded):
+    rel. Frobenius <= 1e-3;  dH hi+lo vs exact dH: <= 1e-4;
+  * fused AdamW (a second replica, same seed, mode ADAMW): masters within 1e-6 + 1e-5|w| of the
+    oracle's AdamW step on the device gradient.
+The oracle sees every row of the reductions; only the dense Y / dX rows are sampled (their
+cost is ~T x K x N per projection in float64).
+"""
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = ["llama2-7b", "llama3-8b", "llama2-13b"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    from paper_2604_16400_b200 import _lib, build
+    build.build()
+    _lib.load()
+
+
+def _one_layer(key):
+    from paper_2604_16400_b200.configs import CONFIGS as C
+    cfg = C[key]
+    return dataclasses.replace(cfg, model=dataclasses.replace(cfg.model, layers=1))
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _check_bf16_out(out, ref, what):
+    out = np.asarray(out, np.float64)
+    err = np.abs(out - ref).max()
+    tol = 1e-2 * np.abs(ref).max() + 1e-3
+    assert err <= tol, f"{what}: |err|_inf {err} > {tol}"
+    assert _rel(out, ref) <= 4e-3, f"{what}: rel {_rel(out, ref)}"
+
+
+def _sample_rows(seg_start, T, n_tr, g, n_rand=192):
+    rows = {0, T - 1}
+    for s in seg_start[1:-1]:
+        rows.update((s - 1, s))
+    for m in range(0, T, 256):
+        rows.update((m, min(T - 1, m + 255)))
+    rows.update(g.integers(0, T, n_rand).tolist())
+    rows.update(g.integers(0, max(1, n_tr), 32).tolist())
+    return np.array(sorted(r for r in rows if 0 <= r < T))
+
+
+def _f(t):
+    return t.float().cpu().numpy()
+
+
+def _stack_inputs(st, plan, l=0):
+    a = st._acts
+    L = st.cfg.model.layers
+    out = {}
+    for proj in st.layers[l]:
+        name = proj.spec.name
+        X = a["X"][l] if name in ("qkv", "q", "k", "v", "gate_up", "gate", "up") else \
+            (a["Xo"][l] if name == "o" else a["Xd"][l])
+        Y = a["X"][l + 1] if name == "down" else a["Y"][name]
+        dY = (a["dY_top"] if l == L - 1 else a["dX_first"][l + 1]) if name == "down" \
+            else a["dY"][l][name]
+        dX = a["dX_first"][l] if proj is st.layers[l][0] else a["dX"][name]
+        out[name] = (X, Y, dY, dX)
+    return out
+
+
+@pytest.mark.parametrize("key", CONFIGS)
+def test_baseline_layer_matches_oracle(key):
+    from paper_2604_16400_b200.replica import ReplicaStack
+    cfg = _one_layer(key)
+    train, items = cfg.batch(0)
+    st = ReplicaStack(cfg, "cuda", seed=0)
+    st.overlap = True
+    plan = st.plan(train, items)
+    st.allocate(plan, distinct_synthetic=True)
+    st.run_step(plan, optimizer_step=False)  # STORE_GRAD: the raw LoRA gradients
+    torch.cuda.synchronize()
+
+    # K0 from the oracle's own row builder (independent of the package's planner)
+    ob = oracle.build_rows((train.adapter, train.rows),
+                           [(it.request_id, it.adapter, it.n_rows, int(it.role)) for it in items])
+    seg_start, seg_ad = ob[0], ob[1]
+    T, Ttr = seg_start[-1], train.rows
+    assert T == plan.n_rows and Ttr == plan.n_train
+    row_ad = oracle.expand_segments(seg_start, seg_ad)
+    assert np.array_equal(plan.device.row_adapter.cpu().numpy(), row_ad)
+    g = np.random.default_rng(0)
+    rows = _sample_rows(seg_start, T, Ttr, g)
+    dx_rows = rows[rows < Ttr]
+
+    grads = {}
+    for proj in st.layers[0]:
+        sp = proj.spec
+        name = sp.name
+        X, Y, dY, dX = _stack_inputs(st, plan)[name]
+        Xh = _f(X[:T])
+        W, A, B, sc = _f(proj.W), _f(proj.A), _f(proj.B), proj.scale.cpu().numpy()
+        # forward: H16 on every row, Y on the sampled rows
+        H16_ref = oracle.lora_shrink(Xh, A, sc, row_ad)
+        assert _rel(_f(proj._H16[:T]), H16_ref) <= 4e-3, f"{key} {name} H16"
+        Y_ref, _ = oracle.lora_forward(Xh[rows], W, A, B, sc, row_ad[rows], sp.subs, sp.r_pad)
+        _check_bf16_out(_f(Y[rows]), Y_ref, f"{key} {name} Y")
+        # backward of the training rows vs exact math
+        t = proj.train_state.adapter
+        dX_ref, dB_ref, dAT_ref, dH_ref = oracle.lora_backward(
+            _f(dY[:Ttr]), Xh[:Ttr], H16_ref[:Ttr], W, A[t], B[t], float(sc[t]), sp.subs,
+            sp.r_pad, dx_rows=dx_rows)
+        _check_bf16_out(_f(dX[dx_rows]), dX_ref, f"{key} {name} dX")
+        pair = _f(proj._dH16[:Ttr]).astype(np.float64) + _f(proj._dH16lo[:Ttr])
+        assert _rel(pair, dH_ref) <= 1e-4, f"{key} {name} dH hi+lo {_rel(pair, dH_ref)}"
+        gB = proj.train_state.grad_B.cpu().numpy()
+        gAT = proj.train_state.grad_AT.cpu().numpy()
+        assert _rel(gB, dB_ref) <= 1e-3, f"{key} {name} dB rel {_rel(gB, dB_ref)}"
+        assert _rel(gAT, dAT_ref) <= 1e-3, f"{key} {name} dA^T rel {_rel(gAT, dAT_ref)}"
+        grads[name] = (gB, gAT, proj.train_state.master_B.cpu().numpy().copy(),
+                       proj.train_state.master_AT.cpu().numpy().copy())
+    del st
+    torch.cuda.empty_cache()
+
+    # the fused AdamW path of the same step (fresh replica, same seed -> bitwise the same grads)
+    from paper_2604_16400_b200.layer import AdamWConfig
+    opt = AdamWConfig(lr=1e-3, weight_decay=0.01)
+    st2 = ReplicaStack(cfg, "cuda", seed=0, optimizer=opt)
+    st2.overlap = True
+    plan2 = st2.plan(train, items)
+    st2.allocate(plan2, distinct_synthetic=True)
+    st2.run_step(plan2, optimizer_step=True)
+    torch.cuda.synchronize()
+    for proj in st2.layers[0]:
+        gB, gAT, mB0, mAT0 = grads[proj.spec.name]
+        for m0, gr, dev, what in ((mB0, gB, proj.train_state.master_B, "B"),
+                                  (mAT0, gAT, proj.train_state.master_AT, "A^T")):
+            ost = oracle.AdamWState(np.zeros_like(m0), np.zeros_like(m0))
+            ref = oracle.adamw_step(m0, gr, ost, lr=opt.lr, wd=opt.weight_decay)
+            got = dev.cpu().numpy()
+            bad = np.abs(got - ref) > 1e-6 + 1e-5 * np.abs(ref)
+            assert not bad.any(), f"{key} {proj.spec.name} AdamW {what}: {int(bad.sum())} elems"

@@ -41,7 +41,7 @@ def test_reduce_group_struct_matches_header():
     fields = re.findall(r"(\w+)\s*[,;]", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
     names = [f[0] for f in _lib.ReduceGroup._fields_]
     assert fields == names
-    assert C.sizeof(_lib.ReduceGroup) == 8 * 8 + 12 * 4
+    assert C.sizeof(_lib.ReduceGroup) == 9 * 8 + 12 * 4
 
 
 def test_status_mapping(lib):

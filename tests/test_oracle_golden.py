@@ -2,9 +2,10 @@
 
 * fedavg / adapter layout: bit-exact against outputs of the reference's own launcher.fedavg and
   AdapterParams.zeros (/root/reference/pkg/src/coserve/launcher.py:28-80).
-* LoRA forward/backward: against an independent torch-float64-autograd formulation.  Y and dB
-  share the oracle's rounding points exactly (rel 1e-12); dX and dA differ by the bf16 rounding of
-  dH that the device algorithm applies and autograd does not (rel <= 1e-2).
+* LoRA forward/backward: against an independent torch-float64-autograd formulation.  Y, dB, dX
+  and dA share the oracle's rounding points exactly (rel 1e-12; the backward's dH is exact, as
+  the device's bf16 hi+lo pair carries it); the single-rounding variant (dh_mode="bf16") is
+  shown to miss SURVEY §8(c)'s 1e-3 on dA, which is why the device does not use it.
 * the reference's own FedAvg property tests (tests/test_launcher.py:41-82) re-run on the oracle.
 """
 
@@ -87,8 +88,13 @@ def test_lora_oracle_vs_autograd(seed):
     dX, dB, dAT, _ = oracle.lora_backward(dY, X[:T_tr], H16[:T_tr], W, A[ta], B[ta],
                                           float(scale[ta]), subs, r_pad)
     assert _rel(dB, d[p + "dB"]) < 1e-12
-    assert _rel(dAT.T, d[p + "dA"]) < 1e-2
-    assert _rel(dX, d[p + "dX"]) < 1e-2
+    assert _rel(dAT.T, d[p + "dA"]) < 1e-12
+    assert _rel(dX, d[p + "dX"]) < 1e-12
+    # the single-rounding variant stays within bf16 output tolerance on dX, not 1e-3 on dA
+    dX1, _, dAT1, _ = oracle.lora_backward(dY, X[:T_tr], H16[:T_tr], W, A[ta], B[ta],
+                                           float(scale[ta]), subs, r_pad, dh_mode="bf16")
+    assert _rel(dX1, d[p + "dX"]) < 4e-3
+    assert 1e-4 < _rel(dAT1.T, d[p + "dA"]) < 1e-2
 
 
 def test_adamw_matches_torch():
