@@ -422,7 +422,7 @@ def run_ours(args, cfg, workload):
         Xt = stack._acts["X"][cfg.model.layers][:Ttr]
         labels = torch.randint(0, V, (Ttr,), device=dev, generator=gh, dtype=torch.int32)
         dXt = torch.empty(Ttr, h, dtype=torch.bfloat16, device=dev)
-        loss = head.forward_backward(Xt, labels, dXt)
+        loss = head.forward_backward(Xt, labels, dXt, n_valid=Ttr)
         torch.cuda.synchronize()
         hb = head._buffers(Ttr)
         ghead, gce = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
@@ -430,7 +430,7 @@ def run_ours(args, cfg, workload):
         s.wait_stream(st_dev)
         with torch.cuda.stream(s):
             with torch.cuda.graph(ghead, stream=s):
-                head.forward_backward(Xt, labels, dXt)
+                head.forward_backward(Xt, labels, dXt, n_valid=Ttr)
             with torch.cuda.graph(gce, stream=s):
                 ops.cross_entropy(hb["logits"], labels, V, loss_rows=hb["loss_rows"],
                                   loss_mean=hb["loss"], counter=hb["counter"],

@@ -1,153 +1,422 @@
-"""Drop-in seam into the reference engine (coserve): latency and optimizer stand-ins -> B200 layer.
+"""The drop-in seam: the reference engine's replica step runs on the B200 unified layer.
 
-The reference engine imports its hardware model by NAME (``from .perf import ...
-true_infer_latency, true_train_latency, train_step``, /root/reference/pkg/src/coserve/engine.py:40)
-and calls those names from the replica-step handlers (engine.py:315-317, :379-383, :395); FedAvg is
-the module global ``fedavg`` of launcher.py (called at :226).  The least invasive drop-in is to
-rebind exactly those names for the duration of a run — the reference's loop, dispatcher,
-coordinator and launcher run unmodified:
+The reference (coserve) is a discrete-event simulator whose replica step asks a hardware model
+for numbers: ``true_infer_latency`` at ``Engine._start_batch`` (engine.py:312-333),
+``true_train_latency`` at ``_handle_train_start`` (:372-388), the convergence stand-in
+``train_step`` at ``_handle_train_done`` (:391-408) and the toy ``fedavg`` of ``AdapterParams`` in
+``FLProcess.finalize_round`` (launcher.py:215-246, :226).  :func:`make_engine` builds an ``Engine``
+subclass that overrides exactly those handlers and routes them through a :class:`ReplicaBackend`;
+the reference's loop, dispatcher, coordinator, state machine and launcher run unmodified (the
+override passes each measured number into the reference's own handler body, so no reference
+logic is restated here):
 
-    with install(engine_module, MeasuredLatencyBackend(cfg)):
-        ledger = Engine(scenario, seed).run()
+* :class:`SimulatedBackend` answers with the reference's own perf model (byte-identical runs —
+  the seam is transparent).
+* :class:`CudaLoraBackend` runs the real co-batched passes on this GPU: ``infer_step`` composes a
+  ``MixedBatch`` from the DISPATCHED requests (``Request.stream_id`` -> the tenant's adapter slot,
+  ``output_tokens`` -> decode iterations), ``train_step`` runs the replica's training micro-batch
+  co-batched with the decode rows of its in-flight inference batch (forward + backward + fused
+  AdamW + LM-head CE: the measured loss), each simulated replica trains ITS OWN adapter slot
+  (per-replica fp32 masters / AdamW state), ``aggregate`` averages the reporting replicas'
+  adapters on the device and hands the mean back to every participant (the broadcast the
+  reference omits, engine.py:478-480).  Latencies are CUDA-event times; the gradient-noise scale
+  fed to ``Coordinator.record_noise_scale`` (coordinator.py:293-294) is McCandlish's B_simple
+  estimated from gradient norms at two batch sizes; replica utilization (``WorkLog``,
+  perf.py:129-158) becomes measured GPU busy time (:class:`MeasuredWorkLog`).
 
-``MeasuredLatencyBackend`` answers ``true_infer_latency(profile, BatchConfig(B, b), rng)`` with the
-measured CUDA-event time of a real co-batched pass on this GPU (b decode rows over the tenant
-adapters + B training sequences, forward only) and ``true_train_latency`` with a full training
-step (forward + backward + fused AdamW of the B sequences while b inference rows co-run), keeping
-the coordinator's (B, b, t) sample interface (coordinator.py:284-288) unchanged.
+    from paper_2604_16400_b200.backend import CudaLoraBackend, make_engine
+    Engine = make_engine(coserve.engine, CudaLoraBackend(cfg, streams, n_replicas))
+    ledger = Engine(scenario, seed).run()
 """
 
 from __future__ import annotations
 
 import contextlib
-from dataclasses import dataclass, field
+import dataclasses
+import math
+from typing import Protocol
 
 from .domain import ConfigurationError
 
-
-@dataclass
-class PassthroughBackend:
-    """Delegates to the reference's own functions (used to prove the seam is transparent)."""
-
-    perf_module: object
-
-    def true_infer_latency(self, profile, cfg, rng=None):
-        return self.perf_module.true_infer_latency(profile, cfg, rng)
-
-    def true_train_latency(self, profile, cfg, rng=None):
-        return self.perf_module.true_train_latency(profile, cfg, rng)
+# --------------------------------------------------------------------------- backend protocol
 
 
-@dataclass
-class MeasuredLatencyBackend:
-    """Measured latencies of the B200 unified layer for the reference's (B, b) interface."""
+class ReplicaBackend(Protocol):
+    def infer_step(self, replica, requests, now: float) -> float:
+        """Run (or model) one inference batch of the dispatched ``requests`` on ``replica``;
+        return its latency in seconds."""
 
-    cfg: object                 # configs.LayerConfig
-    device: str = "cuda"
-    seed: int = 0
-    reps: int = 3
-    _stack: object = None
-    _cache: dict = field(default_factory=dict)
+    def train_step(self, replica, train_batch: int, concurrent_b: int, now: float) -> float:
+        """Run (or model) one training step of ``train_batch`` samples while ``concurrent_b``
+        inference rows of the replica's in-flight batch co-run; return its latency (s)."""
 
-    def _replica(self):
-        if self._stack is None:
-            from .replica import ReplicaStack
-            self._stack = ReplicaStack(self.cfg, self.device, seed=self.seed)
-        return self._stack
+    def train_result(self, replica, train_batch: int):
+        """(new reference TrainState, measured gradient-noise scale or None) of the step that
+        finished (``_handle_train_done``)."""
 
-    def _measure(self, B: int, b: int, train: bool) -> float:
-        import torch
-
-        from .domain import InferenceItem, RowRole, TrainItem
-        key = (B, b, train)
-        if key in self._cache:
-            return self._cache[key]
-        st = self._replica()
-        items = [InferenceItem(i, i % self.cfg.n_adapters, 1, RowRole.DECODE) for i in range(b)]
-        tr = TrainItem(self.cfg.train_adapter, B, self.cfg.train_seq) if B > 0 else None
-        if tr is None and not items:
-            raise ConfigurationError("empty pass")
-        plan = st.plan(tr, items)
-        st.allocate(plan, distinct_synthetic=False)
-        opt = train and B > 0
-        st.run_step(plan, optimizer_step=opt)  # warm (sizes workspaces)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(self.reps):
-            st.run_step(plan, optimizer_step=opt, backward=train)
-        e1.record()
-        torch.cuda.synchronize()
-        sec = e0.elapsed_time(e1) / self.reps / 1e3
-        self._cache[key] = sec
-        return sec
-
-    def true_infer_latency(self, profile, cfg, rng=None):
-        if cfg.infer_batch < 1:
-            raise ConfigurationError("infer_batch must be >= 1")
-        return self._measure(cfg.train_batch, cfg.infer_batch, train=False)
-
-    def true_train_latency(self, profile, cfg, rng=None):
-        if cfg.train_batch < 1:
-            raise ConfigurationError("train_batch must be >= 1")
-        return self._measure(cfg.train_batch, cfg.infer_batch, train=True)
+    def aggregate(self, family: str, reporting: list[int]) -> None:
+        """Round boundary: combine the reporting replicas' adapters (FedAvg) and hand the result
+        back to them."""
 
 
-@dataclass
-class RealTrainingBackend(MeasuredLatencyBackend):
-    """Also replaces the convergence stand-in ``train_step`` (perf.py:111-126, called at
-    engine.py:395): every call runs a real co-batched training step (B sequences of the trainable
-    adapter, LM head + next-token CE, fused AdamW) and returns the reference's ``TrainState`` with
-    the MEASURED loss — ``last_decrement`` = previous loss - new loss, so the coordinator's
-    record_decrement / record_noise_scale (engine.py:396-397) consume real training signal;
-    ``noise_scale`` keeps the reference's own definition on top of the real loss."""
+@dataclasses.dataclass
+class SimulatedBackend:
+    """The reference's own hardware model (perf.py), consuming the replica RNG streams exactly as
+    the reference handlers do: an engine built on it is byte-identical to the reference."""
 
-    optimizer: object = None    # layer.AdamWConfig (None: its defaults)
-    _train_stack: object = None
-    _train_plans: dict = field(default_factory=dict)
+    perf: object  # the coserve.perf module
+    domain: object  # the coserve.domain module
 
-    def _trainer(self):
-        if self._train_stack is None:
-            from .replica import ReplicaStack
-            self._train_stack = ReplicaStack(self.cfg, self.device, seed=self.seed,
-                                             optimizer=self.optimizer, lm_head=True)
-        return self._train_stack
+    def infer_step(self, replica, requests, now):
+        return self.perf.true_infer_latency(
+            replica.profile, self.domain.BatchConfig(replica.interference_train_batch, len(requests)),
+            replica.latency_rng)
 
-    def train_step(self, state, batch: int, rng=None):
-        import dataclasses
+    def train_step(self, replica, train_batch, concurrent_b, now):
+        return self.perf.true_train_latency(
+            replica.profile, self.domain.BatchConfig(train_batch, concurrent_b), replica.latency_rng)
 
-        from .domain import TrainItem
-        if batch < 1:
-            raise ConfigurationError("training batch must be >= 1")
-        st = self._trainer()
-        if batch not in self._train_plans:
-            plan = st.plan(TrainItem(self.cfg.train_adapter, batch, self.cfg.train_seq), [])
-            st.allocate(plan, distinct_synthetic=False)
-            self._train_plans[batch] = plan
-        plan = self._train_plans[batch]
-        if st._plan is not plan:
-            st.allocate(plan, distinct_synthetic=False)
-        st.run_step(plan, optimizer_step=True)
-        loss = st.last_loss()
-        if state.steps == 0:  # the stand-in's initial loss is a guess: anchor it to the real one
-            return dataclasses.replace(state, loss=loss, initial_loss=loss, steps=1,
-                                       last_decrement=0.0)
-        return dataclasses.replace(state, loss=loss, steps=state.steps + 1,
-                                   last_decrement=state.loss - loss)
+    def train_result(self, replica, train_batch):
+        return self.perf.train_step(replica.train, train_batch, replica.train_rng), None
+
+    def aggregate(self, family, reporting):
+        return None
+
+
+# --------------------------------------------------------------------------- engine subclass
 
 
 @contextlib.contextmanager
-def install(engine_module, backend):
-    """Rebind the engine module's imported latency functions (and, when the backend provides
-    it, ``train_step``) to ``backend`` for the block."""
-    names = ["true_infer_latency", "true_train_latency"]
-    if hasattr(backend, "train_step"):
-        names.append("train_step")
-    saved = {n: getattr(engine_module, n) for n in names}
+def _rebind(module, name: str, value):
+    saved = getattr(module, name)
+    setattr(module, name, value)
     try:
-        for n in names:
-            setattr(engine_module, n, getattr(backend, n))
-        yield backend
+        yield
     finally:
-        for n, f in saved.items():
-            setattr(engine_module, n, f)
+        setattr(module, name, saved)
+
+
+class MeasuredWorkLog:
+    """``perf.WorkLog`` (perf.py:129-158) on measured GPU busy time: every recorded interval is a
+    pass whose duration was timed with CUDA events, so utilization over a window is the fraction
+    of the window the replica's GPU work covered (clamped to [0, 1]); the reference's work units
+    and capacity are not needed."""
+
+    def __init__(self, capacity: float | None = None) -> None:
+        self.capacity = capacity
+        self._entries: list[tuple[float, float]] = []
+
+    def record(self, start: float, end: float, units: float = 0.0) -> None:
+        if end <= start:
+            raise ConfigurationError("work interval must have positive duration")
+        self._entries.append((start, end))
+
+    def prune(self, horizon: float) -> None:
+        self._entries = [e for e in self._entries if e[1] > horizon]
+
+    def busy(self, now: float, window: float) -> float:
+        lo = now - window
+        return sum(max(0.0, min(e, now) - max(s, lo)) for s, e in self._entries)
+
+    def sample(self, now: float, window: float) -> float:
+        if window <= 0:
+            raise ConfigurationError("utilization window must be positive")
+        return min(1.0, self.busy(now, window) / window)
+
+
+def make_engine(engine_module, backend: ReplicaBackend, measured_worklog: bool | None = None):
+    """An ``Engine`` subclass of the reference ``engine_module`` (coserve.engine) whose replica
+    step goes through ``backend``.  Each override computes the backend's number first and then
+    runs the reference's own handler with the engine module's hardware-model names rebound to
+    return it, so the reference's bookkeeping (busy time, ledger stamps, coordinator samples,
+    event scheduling, FL round protocol) is unchanged."""
+    base = engine_module.Engine
+    if measured_worklog is None:
+        measured_worklog = isinstance(backend, CudaLoraBackend)
+
+    class CollmEngine(base):
+        collm_backend = backend
+
+        def __init__(self, scenario, seed, policy_name="subflow"):
+            super().__init__(scenario, seed, policy_name)
+            if measured_worklog:
+                for r in self.replicas.values():
+                    r.work = MeasuredWorkLog(r.profile.capacity)
+            hook = getattr(backend, "attach", None)
+            if hook is not None:
+                hook(self)
+
+        # engine.py:312-333
+        def _start_batch(self, replica, requests, now):
+            latency = backend.infer_step(replica, requests, now)
+            with _rebind(engine_module, "true_infer_latency", lambda *a, **k: latency):
+                super()._start_batch(replica, requests, now)
+
+        # engine.py:372-388
+        def _handle_train_start(self, ev):
+            replica = self.replicas[ev.payload]
+            runtime = self.processes.get(replica.family)
+            if runtime is None or replica.round_steps_left <= 0:
+                return
+            latency = backend.train_step(replica, replica.batch_cfg.train_batch,
+                                         replica.current_infer_b, self.now)
+            with _rebind(engine_module, "true_train_latency", lambda *a, **k: latency):
+                super()._handle_train_start(ev)
+
+        # engine.py:391-408
+        def _handle_train_done(self, ev):
+            replica = self.replicas[ev.payload]
+            runtime = self.processes.get(replica.family)
+            if runtime is None:
+                return
+            state, noise = backend.train_result(replica, replica.batch_cfg.train_batch)
+            coord = runtime.coordinator
+            patched = noise is not None
+            if patched:  # the measured B_noise instead of the stand-in's property (perf.py:105-108)
+                orig = coord.record_noise_scale
+                coord.record_noise_scale = lambda _v: orig(noise)
+            try:
+                with _rebind(engine_module, "train_step", lambda *a, **k: state):
+                    super()._handle_train_done(ev)
+            finally:
+                if patched:
+                    del coord.record_noise_scale
+
+        # engine.py:415-466 (FLProcess.finalize_round -> fedavg, launcher.py:215-246)
+        def _handle_round_boundary(self, ev):
+            family = ev.payload
+            runtime = self.processes.get(family)
+            reporting = None
+            if runtime is not None and runtime.process.round_done:
+                proc = runtime.process
+                reporting = [rid for rid in proc._round.participants if rid in proc._clients]
+            super()._handle_round_boundary(ev)
+            if reporting:
+                backend.aggregate(family, reporting)
+
+    CollmEngine.__name__ = CollmEngine.__qualname__ = "CollmEngine"
+    return CollmEngine
+
+
+@contextlib.contextmanager
+def install(module, engine_cls):
+    """Rebind ``module.Engine`` (e.g. coserve.experiment, which builds ``Engine(...)`` by name at
+    experiment.py:21-28) to ``engine_cls`` for the block: the reference's CLI / experiment runner
+    then drives the CUDA backend unchanged, including its exit-code mapping."""
+    with _rebind(module, "Engine", engine_cls):
+        yield engine_cls
+
+
+# --------------------------------------------------------------------------- the CUDA backend
+
+
+@dataclasses.dataclass
+class _NoiseEstimator:
+    """McCandlish et al.'s unbiased estimates from gradient norms at two batch sizes (App. A):
+    |G|^2 ~ (B_big |G_big|^2 - B_small |G_small|^2) / (B_big - B_small),
+    tr(S) ~ (|G_small|^2 - |G_big|^2) / (1/B_small - 1/B_big); both smoothed by EMA, then
+    B_simple = tr(S) / |G|^2 (in the units of B: training samples)."""
+
+    decay: float = 0.9
+    g2: float | None = None
+    trace: float | None = None
+
+    def update(self, b_small: float, g2_small: float, b_big: float, g2_big: float) -> None:
+        g2 = (b_big * g2_big - b_small * g2_small) / (b_big - b_small)
+        tr = (g2_small - g2_big) / (1.0 / b_small - 1.0 / b_big)
+        self.g2 = g2 if self.g2 is None else self.decay * self.g2 + (1 - self.decay) * g2
+        self.trace = tr if self.trace is None else self.decay * self.trace + (1 - self.decay) * tr
+
+    @property
+    def b_noise(self) -> float | None:
+        if self.g2 is None or self.trace is None or self.g2 <= 0 or self.trace <= 0:
+            return None
+        return self.trace / self.g2
+
+
+class CudaLoraBackend:
+    """Real co-batched passes for every simulated replica of one engine on this GPU.
+
+    One frozen base model (a :class:`ReplicaStack`) is shared by the engine's replicas (one
+    device); adapter slots [0, n_streams) hold the tenants' adapters (stream_id -> slot, sorted),
+    slots [n_streams, n_streams + n_replicas) each replica's own trainable adapter (initialised
+    from its family's tenant adapter when the replica first trains).  An inference request
+    contributes ``prompt_tokens`` prefill rows on its tenant's adapter and ``output_tokens - 1``
+    decode iterations; a batch's latency is its prefill pass plus, for every distinct set of
+    still-decoding requests, one REAL decode pass of that set times the iterations it lasts
+    (passes over the same rows do the same projection work).  ``latency_scale`` maps device
+    seconds to simulated seconds (1.0: measured time as is)."""
+
+    def __init__(self, cfg, streams, n_replicas: int, device="cuda", seed: int = 0,
+                 prompt_tokens: int = 16, latency_scale: float = 1.0, optimizer=None,
+                 lm_head: bool = True, noise_every: int = 10, families: dict | None = None):
+        from .replica import ReplicaStack
+        streams = sorted(streams)
+        if not streams or n_replicas < 1:
+            raise ConfigurationError("need >= 1 stream and >= 1 replica")
+        if prompt_tokens < 1 or latency_scale <= 0:
+            raise ConfigurationError("prompt_tokens >= 1 and latency_scale > 0 required")
+        self.slot_of_stream = {s: i for i, s in enumerate(streams)}
+        self.n_streams = len(streams)
+        self.family_slot = {}
+        for s, fam in (families or {}).items():
+            self.family_slot.setdefault(fam, self.slot_of_stream[s])
+        n_ad = self.n_streams + n_replicas
+        self.cfg = dataclasses.replace(cfg, n_adapters=n_ad, train_adapter=self.n_streams)
+        self.stack = ReplicaStack(self.cfg, device, seed=seed, optimizer=optimizer,
+                                  lm_head=lm_head, trainer=False)
+        self.prompt_tokens = prompt_tokens
+        self.latency_scale = latency_scale
+        self.noise_every = max(1, noise_every)
+        self._inflight: dict[int, list] = {}
+        self._results: dict[int, tuple] = {}
+        self._losses: dict[int, float] = {}
+        self._noise: dict[int, _NoiseEstimator] = {}
+        self._steps: dict[int, int] = {}
+        self.gpu_seconds = 0.0
+        self.passes = 0
+        self._engine = None
+
+    # -- wiring
+    def attach(self, engine) -> None:
+        self._engine = engine
+        for sid, scfg in engine.stream_map.items():
+            if sid not in self.slot_of_stream:
+                raise ConfigurationError(f"stream {sid!r} has no tenant adapter slot")
+            self.family_slot.setdefault(scfg.family, self.slot_of_stream[sid])
+        if len(engine.replicas) > self.cfg.n_adapters - self.n_streams:
+            raise ConfigurationError(f"{len(engine.replicas)} replicas, backend sized for "
+                                     f"{self.cfg.n_adapters - self.n_streams}")
+
+    def trainer_slot(self, replica_id: int) -> int:
+        return self.n_streams + replica_id
+
+    def _use_trainer(self, replica):
+        st = self.stack
+        key = ("replica", replica.id)
+        if key not in st.trainers:
+            src = self.family_slot.get(replica.family, 0)
+            st.add_trainer(key, self.trainer_slot(replica.id), copy_from=src)
+        return st.use_trainer(key)
+
+    # -- one measured pass
+    def _pass(self, train, items, backward: bool, optimizer_step: bool = True) -> float:
+        import torch
+        st = self.stack
+        plan = st.plan(train, items)
+        st.allocate(plan, distinct_synthetic=False, reuse=True)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st.run_step(plan, optimizer_step=optimizer_step, backward=backward)
+        e1.record()
+        e1.synchronize()
+        sec = e0.elapsed_time(e1) / 1e3
+        self.gpu_seconds += sec
+        self.passes += 1
+        return sec
+
+    def _decode_items(self, requests):
+        from .domain import InferenceItem, RowRole
+        return [InferenceItem(r.id, self.slot_of_stream[r.stream_id], 1, RowRole.DECODE)
+                for r in requests]
+
+    # -- ReplicaBackend
+    def infer_step(self, replica, requests, now):
+        from .domain import InferenceItem, RowRole
+        for r in requests:
+            if r.stream_id not in self.slot_of_stream:
+                raise ConfigurationError(f"request {r.id}: stream {r.stream_id!r} has no adapter")
+        self._inflight[replica.id] = list(requests)
+        items = [InferenceItem(r.id, self.slot_of_stream[r.stream_id], self.prompt_tokens,
+                               RowRole.PREFILL) for r in requests]
+        sec = self._pass(None, items, backward=False)
+        # decode iterations: request r decodes output_tokens - 1 more tokens after the prefill
+        left = sorted(requests, key=lambda r: (r.output_tokens, r.id))
+        done = 1
+        i = 0
+        while i < len(left):
+            active = left[i:]
+            upto = active[0].output_tokens
+            if upto > done:
+                sec += self._pass(None, self._decode_items(active), backward=False) * (upto - done)
+                done = upto
+            while i < len(left) and left[i].output_tokens <= done:
+                i += 1
+        return sec * self.latency_scale
+
+    def train_step(self, replica, train_batch, concurrent_b, now):
+        from .domain import TrainItem
+        if train_batch < 1:
+            raise ConfigurationError("training batch must be >= 1")
+        tr = self._use_trainer(replica)
+        seq = self.cfg.train_seq
+        co = self._decode_items(self._inflight.get(replica.id, [])[:concurrent_b])
+        k = self._steps.get(replica.id, 0)
+        self._steps[replica.id] = k + 1
+        if k % self.noise_every == 0:
+            sec = self._train_with_noise_estimate(replica, tr, train_batch, seq, co)
+        else:
+            sec = self._pass(TrainItem(tr.slot, train_batch, seq), co, backward=True)
+        loss = self.stack.last_loss()
+        prev = self._losses.get(replica.id)
+        self._losses[replica.id] = loss
+        self._results[replica.id] = (loss, None if prev is None else prev - loss)
+        return sec * self.latency_scale
+
+    def _train_with_noise_estimate(self, replica, tr, B, seq, co) -> float:
+        """One training step that also measures |G|^2 at two batch sizes: the gradient of a
+        half-size sub-batch (first half of the sequences, or of the tokens when B = 1) and of
+        the full micro-batch, both stored (not applied); then the AdamW step is applied from the
+        full gradient.  Only the full pass is charged as the step's latency."""
+        import torch
+
+        from .domain import TrainItem
+        st = self.stack
+        if B >= 2:
+            small, b_small, b_big = TrainItem(tr.slot, B // 2, seq), B // 2, B
+        else:
+            small, b_small, b_big = TrainItem(tr.slot, 1, max(1, seq // 2)), 0.5, 1.0
+        self._pass(small, [], backward=True, optimizer_step=False)
+        g2_small = float(torch.dot(tr.flat_grad, tr.flat_grad))
+        sec = self._pass(TrainItem(tr.slot, B, seq), co, backward=True, optimizer_step=False)
+        g2_big = float(torch.dot(tr.flat_grad, tr.flat_grad))
+        st.opt.advance()
+        st.apply_optimizer()
+        if b_big != b_small:
+            self._noise.setdefault(replica.id, _NoiseEstimator()).update(b_small, g2_small,
+                                                                         b_big, g2_big)
+        return sec
+
+    def noise_scale(self, replica_id: int) -> float | None:
+        est = self._noise.get(replica_id)
+        return None if est is None else est.b_noise
+
+    def train_result(self, replica, train_batch):
+        loss, dec = self._results.pop(replica.id)
+        s = replica.train
+        if dec is None:  # first real step of this replica: anchor the stand-in's initial loss
+            new = dataclasses.replace(s, loss=loss, initial_loss=loss, steps=s.steps + 1,
+                                      last_decrement=0.0)
+        else:
+            # the real (noisy, possibly negative) drop: the coordinator EWMA-smooths it
+            # (coordinator.py:324-334)
+            new = dataclasses.replace(s, loss=loss, steps=s.steps + 1,
+                                      last_decrement=s.loss - loss if math.isfinite(loss) else 0.0)
+        return new, self.noise_scale(replica.id)
+
+    def aggregate(self, family, reporting):
+        """FedAvg of the reporting replicas' fp32 master adapters (launcher.py:68-80: element-wise
+        mean of B and of A), on the device, handed back to every reporting replica (bf16 copies
+        rewritten).  One replica per GPU would do this with ``sync.fedavg_params`` (NCCL
+        allreduce) + ``registry.broadcast_adapter``; here the engine's replicas share a GPU."""
+        import torch
+        st = self.stack
+        trs = [st.trainers[("replica", r)] for r in reporting if ("replica", r) in st.trainers]
+        if not trs:
+            return
+        mean = torch.stack([t.flat_master for t in trs]).mean(dim=0)
+        for t in trs:
+            t.flat_master.copy_(mean)
+            st.use_trainer(t.key)
+            st.refresh_from_master()

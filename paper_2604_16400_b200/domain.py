@@ -1,10 +1,12 @@
 """Value types of the co-batched LoRA layer, named after the reference's domain.
 
-Mirrors /root/reference/pkg/src/coserve/domain.py: the same error classes (ConfigurationError
-:15-16, InvariantViolation :19-20), ``Request`` (:45-61) and ``BatchConfig`` (:89-98), with the
-same validation and messages, plus the one new type the unified layer needs: a *mixed* row batch.
-The reference's ``Batch`` refuses to mix streams (domain.py:75-77); the unified PEFT layer mixes
-adapters by design, so its row table is ``MixedBatch``, not a ``Batch``.
+The reference's error classes (ConfigurationError domain.py:15-16, InvariantViolation :19-20) and
+value types (``Request`` :45-61, ``BatchConfig`` :89-98) ARE the reference's own classes whenever
+``coserve`` is importable (see :mod:`.reference`): an error the CUDA path raises is then caught by
+the reference's handlers (experiment.py:43-48).  Without the reference, same-named local classes
+with the same validation and messages stand in.  The one new type the unified layer needs is a
+*mixed* row batch: the reference's ``Batch`` refuses to mix streams (domain.py:75-77); the unified
+PEFT layer mixes adapters by design, so its row table is ``MixedBatch``, not a ``Batch``.
 """
 
 from __future__ import annotations
@@ -12,17 +14,21 @@ from __future__ import annotations
 import enum
 from dataclasses import dataclass, field
 
+from .reference import coserve_module
 
-class ConfigurationError(ValueError):
+_ref_domain = coserve_module("domain")
+
+
+class _LocalConfigurationError(ValueError):
     """Bad input or configuration detected before the kernels run."""
 
 
-class InvariantViolation(RuntimeError):
+class _LocalInvariantViolation(RuntimeError):
     """Internal consistency check failed; indicates a bug, never expected."""
 
 
 @dataclass(frozen=True)
-class Request:
+class _LocalRequest:
     """One inference query (reference domain.py:45-61), plus its prompt/decode shape."""
 
     id: int
@@ -41,7 +47,7 @@ class Request:
 
 
 @dataclass(frozen=True)
-class BatchConfig:
+class _LocalBatchConfig:
     """Per-replica batch sizing knobs: training micro-batch and inference batch (domain.py:89-98)."""
 
     train_batch: int = 0
@@ -50,6 +56,19 @@ class BatchConfig:
     def __post_init__(self) -> None:
         if self.train_batch < 0 or self.infer_batch < 0:
             raise ConfigurationError("batch sizes must be non-negative")
+
+
+if _ref_domain is not None:  # the drop-in: the reference's own classes
+    ConfigurationError = _ref_domain.ConfigurationError
+    InvariantViolation = _ref_domain.InvariantViolation
+    Request = _ref_domain.Request
+    BatchConfig = _ref_domain.BatchConfig
+else:
+    ConfigurationError = _LocalConfigurationError
+    InvariantViolation = _LocalInvariantViolation
+    Request = _LocalRequest
+    BatchConfig = _LocalBatchConfig
+USING_REFERENCE_CLASSES = _ref_domain is not None
 
 
 class RowRole(enum.IntEnum):

@@ -66,7 +66,8 @@ class StepPlan:
 
 class ReplicaStack:
     def __init__(self, cfg: LayerConfig, device: torch.device | str = "cuda", seed: int = 0,
-                 optimizer: AdamWConfig | None = None, init: bool = True, lm_head: bool = False):
+                 optimizer: AdamWConfig | None = None, init: bool = True, lm_head: bool = False,
+                 trainer: bool = True):
         self.cfg = cfg
         self.device = torch.device(device)
         self.specs = cfg.projections
@@ -83,9 +84,10 @@ class ReplicaStack:
         self.active: Trainer | None = None
         self.seed = seed
         self._graph: torch.cuda.CUDAGraph | None = None
+        self._make_default_trainer = trainer
+        self._acts: dict | None = None
         if init:
             self.init_synthetic(seed)
-        self._acts: dict | None = None
         self._side: torch.cuda.Stream | None = None
         self.overlap = False
         # how a projection's shrink overlaps its GEMM: "pdl" (default) = same stream, the GEMM
@@ -127,7 +129,9 @@ class ReplicaStack:
             self.head.W.normal_(0.0, 0.02, generator=g)
             self.head.refresh_transpose()
         self.trainers.clear()
-        self.add_trainer("default", self.cfg.train_adapter)
+        self.active = None
+        if self._make_default_trainer:
+            self.add_trainer("default", self.cfg.train_adapter)
 
     # ------------------------------------------------------------------ trainable adapters
     @property
@@ -251,11 +255,25 @@ class ReplicaStack:
         return StepPlan(mb, hp, dp, th, td)
 
     # ------------------------------------------------------------------ activations
-    def allocate(self, plan: StepPlan, distinct_synthetic: bool | None = None, seed: int = 1) -> dict:
+    def allocate(self, plan: StepPlan, distinct_synthetic: bool | None = None, seed: int = 1,
+                 reuse: bool = False) -> dict:
         """Device buffers of one pass.  Synthetic stand-ins (Xo, Xd, the non-chained output grads)
         are per layer when they fit comfortably in HBM, else shared across layers (same traffic,
-        inputs are far larger than L2 either way)."""
+        inputs are far larger than L2 either way).  ``reuse``: keep the current buffers when they
+        have room for this plan's rows (every kernel takes its row counts from the plan), so a
+        serving loop changing its batch every pass does not reallocate."""
         T, Ttr = plan.n_rows, plan.n_train
+        a = self._acts
+        if (reuse and a is not None and a["cap"] >= T and a["cap_train"] >= Ttr
+                and (distinct_synthetic is None or a["distinct_synthetic"] == distinct_synthetic)):
+            self._plan = plan
+            if Ttr and "labels" in a:
+                a["n_valid"] = Ttr
+            return a
+        if reuse and a is not None:  # grow to cover both the old and the new sizes
+            T, Ttr = max(T, a["cap"]), max(Ttr, a["cap_train"])
+            self._acts = a = None
+            torch.cuda.empty_cache()
         h = self.cfg.model.hidden
         i = self.cfg.model.intermediate
         L = self.cfg.model.layers
@@ -273,6 +291,7 @@ class ReplicaStack:
 
         n_syn = L if distinct_synthetic else 1
         acts = {
+            "cap": T, "cap_train": Ttr,
             "distinct_synthetic": distinct_synthetic,
             "X": [torch.empty(T, h, dtype=bf, device=dev) for _ in range(L + 1)],
             "Xo": [rnd(T, h) for _ in range(n_syn)],
@@ -291,7 +310,7 @@ class ReplicaStack:
             # next-token targets of the training rows (synthetic token ids; no dataset offline)
             acts["labels"] = torch.randint(0, self.cfg.model.vocab, (Ttr,), device=dev,
                                            generator=g, dtype=torch.int32)
-            acts["n_valid"] = Ttr  # every synthetic target is a real token id
+            acts["n_valid"] = plan.n_train  # every synthetic target is a real token id
         self._acts = acts
         self._plan = plan
         return acts
@@ -380,8 +399,8 @@ class ReplicaStack:
                 prev = after(main)
         if Ttr and backward and self.head is not None:
             # K2 logits -> K7 softmax-CE fwd+bwd -> K3 dX: the real dY entering the top layer
-            self._loss = self.head.forward_backward(a["X"][L][:Ttr], a["labels"], a["dY_top"],
-                                                    n_valid=a.get("n_valid"))
+            self._loss = self.head.forward_backward(a["X"][L][:Ttr], a["labels"][:Ttr],
+                                                    a["dY_top"], n_valid=Ttr)
         if Ttr and backward:
             opt = self.opt if optimizer_step else None
             mode = _lib.MODE_ADAMW if opt is not None else _lib.MODE_STORE_GRAD

@@ -26,10 +26,17 @@ import torch
 import torch.distributed as dist
 
 from .domain import ConfigurationError
+from .reference import coserve_module
+
+_ref_launcher = coserve_module("launcher")
 
 
-class AggregationError(ValueError):
-    """Mirror of launcher.AggregationError (launcher.py:24-25)."""
+class _LocalAggregationError(ValueError):
+    """Stand-in for launcher.AggregationError (launcher.py:24-25) without the reference."""
+
+
+# the reference's own class when coserve is importable (the drop-in), else the stand-in
+AggregationError = _ref_launcher.AggregationError if _ref_launcher is not None else _LocalAggregationError
 
 
 def world() -> tuple[int, int]:

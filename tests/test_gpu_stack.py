@@ -91,56 +91,6 @@ def test_stack_forward_matches_oracle():
     assert err <= 1e-2 * np.abs(Y_ref).max() + 1e-3
 
 
-def test_measured_latency_backend():
-    """The engine seam's measured backend (backend.MeasuredLatencyBackend) answers the reference's
-    (B, b) latency interface with real CUDA-event times: positive, cached, and a training step
-    (forward + backward + AdamW) costs more than the forward-only pass of the same rows."""
-    from types import SimpleNamespace
-
-    from paper_2604_16400_b200.backend import MeasuredLatencyBackend
-    from paper_2604_16400_b200.configs import CONFIGS
-    be = MeasuredLatencyBackend(CONFIGS["tiny"], reps=2)
-    cfg = SimpleNamespace(train_batch=2, infer_batch=8)
-    t_inf = be.true_infer_latency(None, cfg)
-    t_tr = be.true_train_latency(None, cfg)
-    assert 0 < t_inf < t_tr < 1.0
-    assert be.true_infer_latency(None, cfg) == t_inf  # cached per (B, b)
-
-
-def test_real_training_backend_train_step():
-    """backend.RealTrainingBackend.train_step replaces the reference's convergence stand-in
-    (perf.train_step, perf.py:111-126) with real steps: the returned state (a dataclass shaped
-    like the reference's TrainState) carries the measured CE loss, the first step anchors
-    initial_loss, later steps report the real decrement, and training on fixed synthetic targets
-    lowers the loss."""
-    import dataclasses
-
-    from paper_2604_16400_b200.backend import RealTrainingBackend
-    from paper_2604_16400_b200.configs import CONFIGS
-
-    @dataclasses.dataclass(frozen=True)
-    class State:  # the fields of coserve.perf.TrainState the engine reads (perf.py:92-109)
-        loss: float = 2.0
-        initial_loss: float = 2.0
-        asymptote_loss: float = 0.5
-        steps: int = 0
-        last_decrement: float = 0.0
-
-    from paper_2604_16400_b200.layer import AdamWConfig
-    be = RealTrainingBackend(CONFIGS["tiny"], optimizer=AdamWConfig(lr=1e-2))
-    s0 = State()
-    s1 = be.train_step(s0, 2)
-    assert s1.steps == 1 and s1.initial_loss == s1.loss and s1.last_decrement == 0.0
-    assert 0.0 < s1.loss < 50.0
-    s = s1
-    for _ in range(5):
-        prev = s
-        s = be.train_step(s, 2)
-        assert abs(s.last_decrement - (prev.loss - s.loss)) < 1e-12
-    assert s.steps == 6
-    assert s.loss < s1.loss  # AdamW on the LoRA adapter fits the fixed targets
-
-
 def test_stack_backward_matches_oracle():
     """The stack's training-row backward through the overlapped step — dH shrinks, dX GEMMs and
     the per-layer batched K5 launch (STORE_GRAD mode) — against the oracle on the stack's own
