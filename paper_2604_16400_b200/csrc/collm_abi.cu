@@ -663,9 +663,12 @@ int collm_preload(void) {
   COLLM_PRELOAD((gemm_lora_kernel<128, 6, 1, 1>));
   COLLM_PRELOAD((gemm_lora_kernel<256, 3, 1, 1>));
   COLLM_PRELOAD((gemm_lora_kernel<128, 4, 1, 1>));
-  COLLM_PRELOAD(lora_reduce_kernel<16>);
-  COLLM_PRELOAD(lora_reduce_kernel<32>);
-  COLLM_PRELOAD(lora_reduce_kernel<48>);
+  COLLM_PRELOAD((lora_reduce_kernel<16, 4>));
+  COLLM_PRELOAD((lora_reduce_kernel<32, 4>));
+  COLLM_PRELOAD((lora_reduce_kernel<48, 4>));
+  COLLM_PRELOAD((lora_reduce_kernel<16, 3>));
+  COLLM_PRELOAD((lora_reduce_kernel<32, 3>));
+  COLLM_PRELOAD((lora_reduce_kernel<48, 3>));
   COLLM_PRELOAD(lora_apply_kernel);
   COLLM_PRELOAD((cross_entropy_kernel<8, 512>));
   COLLM_PRELOAD(paged_attention_kernel<1>);
@@ -788,11 +791,12 @@ size_t collm_reduce_workspace_bytes(const collm_reduce_group* groups, int n_grou
 }  // extern "C"
 
 
-template <int QT>
+template <int QT, int MINB>
 static int launch_reduce(ReduceParams& p, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT, MINB>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ReduceSmem<QT>::total(kReduceMaxStages)));
     configured = true;
   }
@@ -810,7 +814,7 @@ static int launch_reduce(ReduceParams& p, cudaStream_t st) {
   attr[0].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
   cfg.attrs = attr;
   cfg.numAttrs = g_reduce_lean ? 1 : 0;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_reduce_kernel<QT>, p));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_reduce_kernel<QT, MINB>, p));
   return COLLM_OK;
 }
 
@@ -844,9 +848,15 @@ int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int
     p.partials = (float*)((char*)workspace + kCounterBytes);
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (qmax <= 16) return launch_reduce<16>(p, st);
-  if (qmax <= 32) return launch_reduce<32>(p, st);
-  return launch_reduce<48>(p, st);
+  static const int minb = [] { const char* e = getenv("COLLM_K5_MINB"); return e ? atoi(e) : 4; }();
+  if (minb == 3) {
+    if (qmax <= 16) return launch_reduce<16, 3>(p, st);
+    if (qmax <= 32) return launch_reduce<32, 3>(p, st);
+    return launch_reduce<48, 3>(p, st);
+  }
+  if (qmax <= 16) return launch_reduce<16, 4>(p, st);
+  if (qmax <= 32) return launch_reduce<32, 4>(p, st);
+  return launch_reduce<48, 4>(p, st);
 }
 
 int collm_lora_apply(const collm_reduce_group* groups, int n_groups, int mode,

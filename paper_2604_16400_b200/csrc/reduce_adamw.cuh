@@ -232,8 +232,9 @@ struct ReduceSmem {
   }
 };
 
-template <int QT>
-__global__ void __launch_bounds__(kReduceThreads, 4) lora_reduce_kernel(const ReduceParams p) {
+// MINB = resident CTAs per SM the register budget is sized for (4: 64 registers, 3: 80)
+template <int QT, int MINB = 4>
+__global__ void __launch_bounds__(kReduceThreads, MINB) lora_reduce_kernel(const ReduceParams p) {
   using S = ReduceSmem<QT>;
   constexpr int PT = kReducePT, TC = kReduceTC;
   const int ST = p.stages;
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(kReduceThreads, 4) lora_reduce_kernel(const Re
   const bf16* u_base = gr.U + gr.u_off + p0;
   const bf16* v_base = gr.V + gr.v_off;
   const bool has_v2 = gr.V2 != nullptr;  // CTA-uniform
-  const bf16* v2_base = has_v2 ? gr.V2 + gr.v_off : gr.V;
+  const long long v2_delta = has_v2 ? (long long)(gr.V2 - gr.V) : 0;  // V2 = V + delta
   const size_t ldu = gr.ldu, ldv = gr.ldv;
   const int T = p.T;
   static_assert(TC * (PT / 8) == 2 * kReduceThreads, "U chunk: two vectors per thread");
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kReduceThreads, 4) lora_reduce_kernel(const Re
       const bool ok = t < T && v_col_ok;
       cp_async_16(&Vs[stage][v_r][v_c], ok ? v_base + (size_t)t * ldv + v_c : gr.V, ok);
       if (has_v2)
-        cp_async_16(&Vs2[stage][v_r][v_c], ok ? v2_base + (size_t)t * ldv + v_c : gr.V, ok);
+        cp_async_16(&Vs2[stage][v_r][v_c], ok ? v_base + v2_delta + (size_t)t * ldv + v_c : gr.V, ok);
     }
   };
 

@@ -63,7 +63,8 @@ def test_engine_runs_on_the_cuda_backend():
     import coserve.engine as engine
 
     from paper_2604_16400_b200.backend import MeasuredWorkLog, make_engine
-    sc = _scenario(40.0)
+    # the first FL process starts after ~35-55 s of simulated serving (idle detection windows)
+    sc = _scenario(75.0)
     be = _backend(sc, latency_scale=50.0, noise_every=5)
     handed_back = []
     orig = be.aggregate

@@ -40,13 +40,15 @@ for name, K, R, fwd, subs in (("fwd qkv", 4096, 48, True, 1), ("fwd o", 4096, 16
         Xs = [torch.randn(Ttr, K, device="cuda").to(torch.bfloat16) for _ in range(reps)]
         BT = torch.randn(R, K, device="cuda").to(torch.bfloat16)
         H16 = torch.empty(Ttr, R, device="cuda", dtype=torch.bfloat16)
+        H16lo = torch.empty(Ttr, R, device="cuda", dtype=torch.bfloat16) \
+            if os.environ.get("NO_LO") != "1" else None
         n = K // subs
         rp = R // subs
         groups = [(s * rp, rp, s * n, (s + 1) * n) for s in range(subs)]
 
         def run(i):
             ops.lora_shrink(Xs[i % reps], BT, tplan.shrink_tiles, tplan.n_shrink_tiles, scale, groups,
-                            R, a_stride=0, H16=H16)
+                            R, a_stride=0, H16=H16, H16lo=H16lo)
         nbytes = 2 * Ttr * K + 2 * R * K
     for i in range(3):
         run(i)
