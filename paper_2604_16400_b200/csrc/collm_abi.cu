@@ -572,6 +572,13 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
                                                             (long long)nm * ((p.num_n_tiles + 1) / 2))
                              : cg * (int)std::min<long long>(sms / cg, min_work);
   p.sched = sched;
+  {
+    // grouped raster when A does not stay L2-resident across an N column's wave (large M): the
+    // data-parallel tiles go in groups of 8 N columns (measured: see DESIGN.md §GEMM raster)
+    static const int gn_env = [] { const char* e = getenv("COLLM_GEMM_RASTER_GN"); return e ? atoi(e) : -1; }();
+    const double a_bytes = 2.0 * M * K;
+    p.raster_gn = gn_env >= 0 ? gn_env : (a_bytes > 32e6 ? 8 : 1);
+  }
   p.lora_flag = lora ? lora_flag : nullptr;
   p.gen = gen;
   {

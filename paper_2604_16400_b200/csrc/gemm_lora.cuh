@@ -80,6 +80,7 @@ struct GemmLoraParams {
   int debug_no_wait;  // timing experiments only: skip that wait (results undefined)
   int sched;  // 0 = data-parallel (round-robin tiles), 1 = hybrid data-parallel + stream-K,
               // 2 = debug: stream-K split without fix-up (timing experiments only)
+  int raster_gn;  // data-parallel raster: groups of this many N tiles (<= 1: m-fastest columns)
   // ---- stream-K
   float* partials;  // [gridDim.x][BM*BN] fp32 partial tiles
   int32_t* flags;   // [gridDim.x] partial-ready flags (0 on entry; consumers reset them)
@@ -162,11 +163,12 @@ struct StreamK {
   int num_m, sum_s;
   int G;
   int dp_tiles;           // tiles [0, dp_tiles) are data-parallel
+  int gn, full_cols;      // grouped raster over the dp region's first full_cols N columns
   long long W_lo, W;      // stream-K region [W_lo, W_lo + W) of the global stage line
   bool split2;            // sched 4: unit u computes half (u & 1) of tile (u >> 1)
   int n_tiles;
 
-  __device__ void init(const int32_t* pre, int nm, int nn, int grid, int sched) {
+  __device__ void init(const int32_t* pre, int nm, int nn, int grid, int sched, int raster_gn = 1) {
     prefix = pre;
     num_m = nm;
     sum_s = pre[nm];
@@ -178,6 +180,25 @@ struct StreamK {
     dp_tiles = sched == 0 ? tiles : (waves >= 1 ? (waves - 1) * grid : 0);
     W_lo = pos_of_tile(dp_tiles);
     W = (long long)sum_s * nn - W_lo;
+    gn = raster_gn > 1 ? raster_gn : 1;
+    full_cols = dp_tiles / nm;
+  }
+  // Data-parallel tile t -> (m, n).  The dp region is the first dp_tiles tiles of the m-fastest
+  // order (the stream-K tail is the rest of it); inside its first full_cols whole N columns the
+  // tiles are visited in groups of gn columns, n-fastest within a group, so one wave touches
+  // ~sqrt(G) A row-blocks and ~sqrt(G) W column-blocks instead of every A row-block of one
+  // column: at large M (A >> L2) A then streams from DRAM num_n / gn times instead of num_n.
+  __device__ void dp_tile(int t, int& m, int& n) const {
+    if (gn > 1 && t < full_cols * num_m) {
+      const int g = t / (gn * num_m);
+      const int cols = min(gn, full_cols - g * gn);
+      const int local = t - g * gn * num_m;
+      m = local / cols;
+      n = g * gn + local % cols;
+    } else {
+      m = t % num_m;
+      n = t / num_m;
+    }
   }
   __device__ long long pos_of_tile(int t) const {
     return (long long)(t / num_m) * sum_s + prefix[t % num_m];
@@ -233,8 +254,7 @@ struct StreamK {
     }
     for (int t = c; t < dp_tiles; t += G) {
       Segment sg;
-      sg.m_blk = t % num_m;
-      sg.n_blk = t / num_m;
+      dp_tile(t, sg.m_blk, sg.n_blk);
       sg.k0 = 0;
       sg.k1 = stages_of_m(sg.m_blk);
       sg.mode = 0;
@@ -356,7 +376,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
 
   StreamK sk;
   sk.init(s_prefix, p.num_m_tiles, AMC ? (p.num_n_tiles + 1) / 2 : p.num_n_tiles,
-          gridDim.x / (AMC ? CL : CG), p.sched);
+          gridDim.x / (AMC ? CL : CG), p.sched, p.raster_gn);
   const int unit = blockIdx.x / (AMC ? CL : CG);  // CTA pair / CTA (AMC: cluster) in the schedule
 
   if (warp == 0) {
