@@ -52,6 +52,11 @@ def parse_args(argv=None):
     ap.add_argument("--eager", action="store_true", help="no CUDA graph (debug)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="run the LoRA kernels on the GEMM stream (no side-stream overlap)")
+    ap.add_argument("--sync", choices=["grad", "fedavg"], default="grad",
+                    help="cross-replica adapter sync for N > 1 (default: per-step gradient "
+                         "allreduce; fedavg = parameter averaging every --round-steps steps)")
+    ap.add_argument("--round-steps", type=int, default=0,
+                    help="fedavg round length in steps (default: --steps, one round per run)")
     return ap.parse_args(argv)
 
 
@@ -271,54 +276,101 @@ def run_ours(args, cfg, workload):
     plan = stack.plan(train, items)
     stack.allocate(plan)
     T, Ttr = plan.n_rows, plan.n_train
-    fused_opt = world == 1
+    # cross-replica sync of the shared training adapter (the path's only collective):
+    #   grad   (north star): each step's LoRA gradients averaged across the replicas, per-layer
+    #          buckets reduced on a comm stream as soon as the layer's K5 wrote them (overlapping
+    #          the backward of the layers below), each bucket's AdamW applied right after it;
+    #   fedavg (reference semantics, launcher.py:68-80 / :226): local fused-AdamW steps, the fp32
+    #          master adapters averaged every --round-steps steps and the mean handed back.
+    sync_mode = "none" if world == 1 else args.sync
+    fused_opt = sync_mode != "grad"
+    group = None
+    if world > 1:
+        from paper_2604_16400_b200 import sync as _sync
+        group = _sync.new_group(list(range(world)))
+        nccl_v = ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else "-"
+        print(f"[rank {rank}/{world}] {backend} communicator (NCCL {nccl_v}) for the FL process over "
+              f"ranks {list(range(world))} on cuda:{local} ({torch.cuda.get_device_name(dev)}); "
+              f"sync={sync_mode}", file=sys.stderr, flush=True)
 
-    flat_grad = None
-    if not fused_opt:
-        flat_grad = stack.flat_grad  # every projection's grads are views of this one buffer
-
-    def sync_and_apply():
+    def avg_(t):
         if backend == "nccl":
-            dist.all_reduce(flat_grad, op=dist.ReduceOp.AVG)
+            dist.all_reduce(t, op=dist.ReduceOp.AVG, group=group)
         else:  # gloo has no AVG
-            dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM)
-            flat_grad.div_(world)
-        apply_graph.replay()
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            t.div_(world)
 
+    L = cfg.model.layers
+    grad_events = [torch.cuda.Event(external=True) for _ in range(L)] if sync_mode == "grad" else None
     # eager step sizes the workspaces; then capture
-    stack.run_step(plan, optimizer_step=fused_opt)
+    stack.run_step(plan, optimizer_step=fused_opt, grad_events=grad_events)
     torch.cuda.synchronize()
     use_graph = not args.eager
     if use_graph:
-        stack.capture(plan, optimizer_step=fused_opt)
-    if not fused_opt:
-        stack.opt.advance()
-        stack.apply_optimizer()
-        apply_graph = torch.cuda.CUDAGraph()
+        g_step = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(dev)
         s.wait_stream(st_dev)
-        with torch.cuda.stream(s), torch.cuda.graph(apply_graph, stream=s):
-            stack.apply_optimizer()
+        with torch.cuda.stream(s), torch.cuda.graph(g_step, stream=s):
+            stack.run_step(plan, optimizer_step=fused_opt, advance=False, grad_events=grad_events)
         st_dev.wait_stream(s)
+        stack._graph = g_step
+    comm = torch.cuda.Stream(dev) if sync_mode == "grad" else None
+    buckets = stack.grad_buckets() if sync_mode == "grad" else None
+    apply_graphs = []
+    if sync_mode == "grad":
+        stack.opt.advance()
+        for l in range(L):
+            stack.apply_optimizer_layer(l)
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(st_dev)
+        for l in range(L):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+                stack.apply_optimizer_layer(l)
+            apply_graphs.append(g)
+        st_dev.wait_stream(s)
+    refresh_graph = None
+    if sync_mode == "fedavg":
+        refresh_graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(st_dev)
+        with torch.cuda.stream(s), torch.cuda.graph(refresh_graph, stream=s):
+            stack.refresh_from_master()
+        st_dev.wait_stream(s)
+    round_steps = max(1, args.round_steps or args.steps)
 
-    n0 = ops.launch_count()
     if use_graph:
         step = lambda: stack.replay(optimizer_step=fused_opt)  # noqa: E731
     else:
-        step = lambda: stack.run_step(plan, optimizer_step=fused_opt)  # noqa: E731
+        step = lambda: stack.run_step(plan, optimizer_step=fused_opt,  # noqa: E731
+                                      grad_events=grad_events)
     # launches per step (counted on one eager step)
     c0 = ops.launch_count()
-    stack.run_step(plan, optimizer_step=fused_opt)
+    stack.run_step(plan, optimizer_step=fused_opt, grad_events=grad_events)
     launches_per_step = ops.launch_count() - c0 + (2 * sum(1 for _ in stack.projections())
-                                                     if not fused_opt else 0)
-    del n0
+                                                     if sync_mode == "grad" else 0)
+    step_i = 0
+    n_sync = 0
 
     def full_step():
-        if not fused_opt:
+        nonlocal step_i, n_sync
+        if sync_mode == "grad":
             stack.opt.advance()
         step()
-        if not fused_opt:
-            sync_and_apply()
+        if sync_mode == "grad":
+            # layer l's bucket as soon as its K5 (inside the graph) recorded grad_events[l]
+            for l in range(L - 1, -1, -1):
+                comm.wait_event(grad_events[l])
+                with torch.cuda.stream(comm):
+                    avg_(buckets[l])
+                    apply_graphs[l].replay()
+            st_dev.wait_stream(comm)
+            n_sync += 1
+        elif sync_mode == "fedavg" and (step_i + 1) % round_steps == 0:
+            avg_(stack.flat_master)
+            refresh_graph.replay()
+            n_sync += 1
+        step_i += 1
 
     for _ in range(args.warmup):
         full_step()
@@ -331,7 +383,9 @@ def run_ours(args, cfg, workload):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    sync0 = n_sync
     ms = timed(full_step, args.steps, st_dev)
+    n_sync_timed = n_sync - sync0
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -347,13 +401,19 @@ def run_ours(args, cfg, workload):
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights of the named shape; seeded synthetic rows)",
-        "config": dict(workload, sync=("none (1 replica): fused AdamW" if fused_opt else
-                                       f"{backend} allreduce(avg) of the flat LoRA-gradient "
-                                       "buffer each step + AdamW apply kernels"),
+        "config": dict(workload, sync={
+            "none": "none (1 replica): fused AdamW",
+            "grad": f"{backend} allreduce(avg) of the LoRA gradients every step in per-layer "
+                    "buckets on a comm stream (each as soon as its layer's K5 wrote it), "
+                    "per-layer AdamW apply after each bucket",
+            "fedavg": f"local fused-AdamW steps; {backend} allreduce(avg) of the fp32 master "
+                      f"adapter every {round_steps} steps (FedAvg, launcher.py:68-80) + "
+                      "bf16 copies refreshed"}[sync_mode],
                        streams=(f"overlapped ({stack.overlap_mode}): each shrink || its GEMM's "
                                 "main loop, K5 on a side stream" if stack.overlap
                                 else "single stream, serialized")),
         "gpu_launches": launches_per_step * args.steps,
+        "syncs_in_timed_region": n_sync_timed,
         "clocks": clk,
     }
     step_flops = stack.step_flops(plan)

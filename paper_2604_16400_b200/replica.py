@@ -217,6 +217,25 @@ class ReplicaStack:
         grad_AT are views of it): the cross-replica sync is a single NCCL allreduce."""
         return self._require_trainer().flat_grad
 
+    def grad_buckets(self) -> list[torch.Tensor]:
+        """Per-layer views of the active trainer's flat gradient buffer (layer l's projections
+        are contiguous in it): the buckets a grad-mode sync reduces as soon as layer l's K5 has
+        written them, overlapping the backward of the layers below."""
+        tr = self._require_trainer()
+        per_layer = len(self.specs)
+        out, off = [], 0
+        for l in range(self.cfg.model.layers):
+            n = sum(st.grad_B.numel() + st.grad_AT.numel()
+                    for st in tr.states[l * per_layer:(l + 1) * per_layer])
+            out.append(tr.flat_grad[off:off + n])
+            off += n
+        return out
+
+    def apply_optimizer_layer(self, l: int) -> None:
+        """AdamW of layer ``l``'s projections from their grad buffers (current stream)."""
+        for p in self.layers[l]:
+            p.apply_optimizer(self.opt)
+
     @property
     def flat_master(self) -> torch.Tensor:
         """The active trainer's fp32 master parameters as ONE flat buffer (fedavg mode)."""
@@ -318,11 +337,14 @@ class ReplicaStack:
     # ------------------------------------------------------------------ the step
     def run_step(self, plan: StepPlan | None = None, optimizer_step: bool = True,
                  advance: bool = True, overlap: bool | None = None,
-                 backward: bool = True) -> torch.Tensor:
+                 backward: bool = True, grad_events: list | None = None) -> torch.Tensor:
         """Enqueue one full co-batched step on the current stream; returns the final hidden state
         buffer (device).  With ``advance`` the optimizer step counter and the step generation are
         bumped first (keep it False inside CUDA-graph capture; ``replay()`` bumps them).
         ``backward=False``: forward of every row only (an inference-only pass).
+        ``grad_events[l]`` (optional, ``torch.cuda.Event(external=True)`` when capturing): recorded
+        on the stream of layer l's K5 right after it, so a comm stream can reduce that layer's
+        gradient bucket while the backward continues below (grad-mode sync).
 
         Projections run in data-flow order: a projection's shrink (K1) and GEMM (K2/K3) start
         only after the previous projection's GEMM (its input exists only then, as in the real
@@ -404,17 +426,21 @@ class ReplicaStack:
         if Ttr and backward:
             opt = self.opt if optimizer_step else None
             mode = _lib.MODE_ADAMW if opt is not None else _lib.MODE_STORE_GRAD
-            pending = None  # (groups, event) of the last finished layer's K5
+            pending = None  # (layer, groups, event) of the last finished layer's K5
 
             def flush_k5():
                 nonlocal pending
                 if pending is not None:
-                    grp, ev = pending
+                    lk, grp, ev = pending
+
                     # K5 of a whole layer in one launch, after the layer's last dX GEMM: the
                     # fused optimizer rewrites A_t^T, which those GEMMs read
-                    on_side(lambda: ops.lora_reduce(Ttr, grp, mode,
-                                                    adamw=opt.args if opt is not None else None,
-                                                    device=self.device), ev)
+                    def k5():
+                        ops.lora_reduce(Ttr, grp, mode, adamw=opt.args if opt is not None else None,
+                                        device=self.device)
+                        if grad_events is not None:
+                            grad_events[lk].record(torch.cuda.current_stream(self.device))
+                    on_side(k5, ev)
                     pending = None
 
             for l in range(L - 1, -1, -1):
@@ -439,7 +465,7 @@ class ReplicaStack:
                         proj.backward_dx(dY, cache, plan.train_device, dX, wait=sig)
                         prev = after(main)
                     groups += proj.grad_groups(dY, cache, optimizer=opt)
-                pending = (groups, prev)
+                pending = (l, groups, prev)
             flush_k5()
         if overlap:
             main.wait_stream(side)
