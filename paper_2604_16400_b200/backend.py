@@ -229,9 +229,9 @@ class _NoiseEstimator:
 
     @property
     def b_noise(self) -> float | None:
-        if self.g2 is None or self.trace is None or self.g2 <= 0 or self.trace <= 0:
-            return None
-        return self.trace / self.g2
+        if self.g2 is None or self.trace is None or self.g2 <= 0:
+            return None  # noise dominates the signal: B_simple undefined (unbounded)
+        return max(0.0, self.trace) / self.g2  # tr(S) <= 0: no measurable noise
 
 
 class CudaLoraBackend:
@@ -249,7 +249,8 @@ class CudaLoraBackend:
 
     def __init__(self, cfg, streams, n_replicas: int, device="cuda", seed: int = 0,
                  prompt_tokens: int = 16, latency_scale: float = 1.0, optimizer=None,
-                 lm_head: bool = True, noise_every: int = 10, families: dict | None = None):
+                 lm_head: bool = True, noise_every: int = 10, families: dict | None = None,
+                 dataset_seqs: int = 8):
         from .replica import ReplicaStack
         streams = sorted(streams)
         if not streams or n_replicas < 1:
@@ -268,6 +269,9 @@ class CudaLoraBackend:
         self.prompt_tokens = prompt_tokens
         self.latency_scale = latency_scale
         self.noise_every = max(1, noise_every)
+        self.dataset_seqs = max(1, dataset_seqs)
+        self._data = None
+        self._cursor = 0
         self._inflight: dict[int, list] = {}
         self._results: dict[int, tuple] = {}
         self._losses: dict[int, float] = {}
@@ -287,6 +291,42 @@ class CudaLoraBackend:
         if len(engine.replicas) > self.cfg.n_adapters - self.n_streams:
             raise ConfigurationError(f"{len(engine.replicas)} replicas, backend sized for "
                                      f"{self.cfg.n_adapters - self.n_streams}")
+        # every replica starts from its family's adapter: anchor the reference's nominal initial
+        # loss (scenario training.initial_loss) to the MEASURED loss of that adapter on the
+        # training data, so FL rounds (early stop, quality updates, launcher.py:171-246) compare
+        # real losses with real losses
+        from .domain import TrainItem
+        for fam in sorted({r.family for r in engine.replicas.values()}):
+            reps = sorted((r for r in engine.replicas.values() if r.family == fam),
+                          key=lambda r: r.id)
+            tr = self._use_trainer(reps[0])
+            self._pass(TrainItem(tr.slot, 1, self.cfg.train_seq), [], backward=True,
+                       optimizer_step=False)
+            l0 = self.stack.last_loss()
+            for r in reps:
+                r.train = dataclasses.replace(r.train, loss=l0, initial_loss=l0)
+                self._losses[r.id] = l0
+
+    def calibrate(self, target_seconds: float, batch: int = 8, output_tokens: int = 100) -> float:
+        """Set ``latency_scale`` so that an inference batch of ``batch`` requests generating
+        ``output_tokens`` tokens each (on the first tenant) takes ``target_seconds`` simulated —
+        e.g. the reference profile's latency for that batch (``perf.true_infer_latency``), so a
+        reference scenario replays at its own load level on a model much smaller or faster than
+        the one its profile describes.  Returns the scale."""
+        from types import SimpleNamespace
+
+        from .domain import Request
+        if target_seconds <= 0 or batch < 1 or output_tokens < 1:
+            raise ConfigurationError("calibrate: positive target, batch and output_tokens")
+        stream = next(iter(self.slot_of_stream))
+        reqs = [Request(-1 - i, 0.0, 1.0, output_tokens, stream) for i in range(batch)]
+        saved, self.latency_scale = self.latency_scale, 1.0
+        probe = SimpleNamespace(id=-1, family=None)
+        self.infer_step(probe, reqs, 0.0)  # warm (buffers, workspaces)
+        sec = self.infer_step(probe, reqs, 0.0)
+        self._inflight.pop(-1, None)
+        self.latency_scale = target_seconds / sec if sec > 0 else saved
+        return self.latency_scale
 
     def trainer_slot(self, replica_id: int) -> int:
         return self.n_streams + replica_id
@@ -304,7 +344,9 @@ class CudaLoraBackend:
         import torch
         st = self.stack
         plan = st.plan(train, items)
-        st.allocate(plan, distinct_synthetic=False, reuse=True)
+        a = st.allocate(plan, distinct_synthetic=False, reuse=True)
+        if plan.n_train:
+            self._load_training_data(a, plan.n_train)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -315,6 +357,38 @@ class CudaLoraBackend:
         self.gpu_seconds += sec
         self.passes += 1
         return sec
+
+    def _load_training_data(self, acts, n_rows: int) -> None:
+        """The training rows of a pass read a fixed synthetic dataset of ``dataset_seqs``
+        sequences (seeded: the layer-0 hidden states, the path's attention-output / MLP-activation
+        stand-ins that feed o / down (replica.py), and the next-token targets) in epoch order:
+        sequence j of the micro-batch is dataset sequence (cursor + j) mod dataset_seqs, the
+        cursor advancing by the micro-batch size every step — whatever micro-batch size the
+        coordinator picks, every sequence is visited and the loss is measured on the same data
+        (no checkpoints or corpora offline: the 'fine-tuning task' is fitting these targets)."""
+        import torch
+        seq = self.cfg.train_seq
+        if self._data is None:
+            g = torch.Generator(device=self.stack.device)
+            g.manual_seed(7919)
+            n = self.dataset_seqs * seq
+            dev, m = self.stack.device, self.cfg.model
+
+            def rnd(cols):
+                return torch.randn(n, cols, device=dev, generator=g).to(torch.bfloat16)
+            y = torch.randint(0, m.vocab, (n,), device=dev, generator=g, dtype=torch.int32)
+            self._data = {"X0": rnd(m.hidden), "Xo": rnd(m.hidden), "Xd": rnd(m.intermediate),
+                          "labels": y}
+        D = self._data
+        targets = [(acts["X"][0], D["X0"])]
+        targets += [(t, D["Xo"]) for t in acts["Xo"]] + [(t, D["Xd"]) for t in acts["Xd"]]
+        if "labels" in acts:
+            targets.append((acts["labels"], D["labels"]))
+        for j, r0 in enumerate(range(0, n_rows, seq)):
+            d = ((self._cursor + j) % self.dataset_seqs) * seq
+            k = min(seq, n_rows - r0)
+            for dst, src in targets:
+                dst[r0:r0 + k].copy_(src[d:d + k])
 
     def _decode_items(self, requests):
         from .domain import InferenceItem, RowRole
@@ -354,6 +428,7 @@ class CudaLoraBackend:
         co = self._decode_items(self._inflight.get(replica.id, [])[:concurrent_b])
         k = self._steps.get(replica.id, 0)
         self._steps[replica.id] = k + 1
+        self._cursor = (k * train_batch) % self.dataset_seqs
         if k % self.noise_every == 0:
             sec = self._train_with_noise_estimate(replica, tr, train_batch, seq, co)
         else:
@@ -378,15 +453,25 @@ class CudaLoraBackend:
         else:
             small, b_small, b_big = TrainItem(tr.slot, 1, max(1, seq // 2)), 0.5, 1.0
         self._pass(small, [], backward=True, optimizer_step=False)
-        g2_small = float(torch.dot(tr.flat_grad, tr.flat_grad))
+        g2_small = self._loss_grad_norm2(tr)
         sec = self._pass(TrainItem(tr.slot, B, seq), co, backward=True, optimizer_step=False)
-        g2_big = float(torch.dot(tr.flat_grad, tr.flat_grad))
+        g2_big = self._loss_grad_norm2(tr)
         st.opt.advance()
         st.apply_optimizer()
         if b_big != b_small:
             self._noise.setdefault(replica.id, _NoiseEstimator()).update(b_small, g2_small,
                                                                          b_big, g2_big)
         return sec
+
+    def _loss_grad_norm2(self, tr) -> float:
+        """|G|^2 over the parameters whose gradient is the true mean gradient of the training
+        loss: the top layer's last projection (its dY is the LM head's dX, normalised by the
+        number of target tokens).  The other projections' output grads are synthetic stand-ins
+        of the path (replica.py), whose row SUMS would grow with the batch and bias the estimate."""
+        import torch
+        st = tr.states[-1]
+        return float(torch.dot(st.grad_B.reshape(-1), st.grad_B.reshape(-1))
+                     + torch.dot(st.grad_AT.reshape(-1), st.grad_AT.reshape(-1)))
 
     def noise_scale(self, replica_id: int) -> float | None:
         est = self._noise.get(replica_id)

@@ -289,10 +289,11 @@ class ReplicaStack:
             if Ttr and "labels" in a:
                 a["n_valid"] = Ttr
             return a
+        old = None
         if reuse and a is not None:  # grow to cover both the old and the new sizes
             T, Ttr = max(T, a["cap"]), max(Ttr, a["cap_train"])
-            self._acts = a = None
-            torch.cuda.empty_cache()
+            distinct_synthetic = a["distinct_synthetic"]
+            old, self._acts, a = a, None, None
         h = self.cfg.model.hidden
         i = self.cfg.model.intermediate
         L = self.cfg.model.layers
@@ -330,6 +331,24 @@ class ReplicaStack:
             acts["labels"] = torch.randint(0, self.cfg.model.vocab, (Ttr,), device=dev,
                                            generator=g, dtype=torch.int32)
             acts["n_valid"] = plan.n_train  # every synthetic target is a real token id
+        if old is not None:
+            # growth keeps the data already there (the rows a pass sees first keep their inputs
+            # and next-token targets: a replica trains on a stable dataset across regrowth)
+            def keep(new, prev):
+                if new is not None and prev is not None:
+                    n = min(new.shape[0], prev.shape[0])
+                    new[:n].copy_(prev[:n])
+            keep(acts["X"][0], old["X"][0])
+            keep(acts.get("dY_top"), old.get("dY_top"))
+            keep(acts.get("labels"), old.get("labels"))
+            for k in ("Xo", "Xd"):
+                for n_, p_ in zip(acts[k], old[k]):
+                    keep(n_, p_)
+            for dn, dp in zip(acts["dY"], old["dY"]):
+                for name in dn:
+                    keep(dn[name], dp.get(name))
+            del old
+            torch.cuda.empty_cache()
         self._acts = acts
         self._plan = plan
         return acts
