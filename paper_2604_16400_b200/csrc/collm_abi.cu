@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -55,16 +56,31 @@ constexpr size_t kCounterBytes = kCounterCap * sizeof(int32_t);
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Per-device host state.  cudaFuncSetAttribute, SM counts and occupancy are properties of a
+// device, so every cache below is indexed by the calling thread's current device and guarded by
+// one mutex (the ABI functions are reentrant: any thread, any device).
+constexpr int kMaxDevices = 64;
+std::mutex g_state_mu;
+
+int cur_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); d = 0; }
+  return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+
 int num_sms_cached() {
-  static int n = -1;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
-  if (n < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  static int n[kMaxDevices] = {};  // 0: not queried yet
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lk(g_state_mu);
+  if (n[dev] <= 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+      cudaGetLastError();
+      v = 148;
+    }
+    n[dev] = v;
   }
-  return n;
+  return n[dev];
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -110,8 +126,10 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, ui
 template <int BN, int STAGES, int CG, int MC>
 int configure_gemm() {
   using L = GemmSmem<BN, STAGES, CG>;
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[kMaxDevices] = {};
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lk(g_state_mu);
+  if (!configured[dev]) {
     CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG, MC>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
     // the whole unified L1/shared array as shared memory: the SM then has room for a rank-space
@@ -121,7 +139,7 @@ int configure_gemm() {
     CUDA_TRY(cudaFuncSetAttribute(gemm_lora_kernel<BN, STAGES, CG, MC>,
                                   cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
-    configured = true;
+    configured[dev] = true;
   }
   return COLLM_OK;
 }
@@ -130,8 +148,9 @@ int configure_gemm() {
 // flag waits need every CTA resident): 4-CTA clusters must fit inside one GPC.
 template <int BN, int STAGES, int CG, int MC>
 int max_gemm_clusters() {
-  static int n = -1;
-  if (n < 0) {
+  static int n[kMaxDevices] = {};  // 0: not computed yet (a device fits >= 1 cluster)
+  const int dev = cur_device();
+  if (n[dev] <= 0) {
     if (configure_gemm<BN, STAGES, CG, MC>()) return 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(num_sms_cached() / (CG * (MC == 1 ? 1 : 2)) * (CG * (MC == 1 ? 1 : 2)));
@@ -149,9 +168,10 @@ int max_gemm_clusters() {
       cudaGetLastError();
       c = num_sms_cached() / (CG * (MC == 1 ? 1 : 2));
     }
-    n = c;
+    std::lock_guard<std::mutex> lk(g_state_mu);
+    n[dev] = c;
   }
-  return n;
+  return n[dev];
 }
 
 template <int BN, int STAGES, int CG, int MC = 1>
@@ -277,11 +297,12 @@ int collm_expand_segments(const int32_t* seg_start, const int32_t* seg_adapter, 
 
 // Overlap mode (collm_set_gemm_lean): GEMMs run "lean" pipelines and the rank-space kernels are
 // sized and launched to fit next to a GEMM CTA on the same SM.
-static bool g_gemm_lean = false;
+// per device (collm_set_gemm_lean applies to the caller's current device)
+static std::atomic<bool> g_gemm_lean[kMaxDevices];
 static unsigned long long* g_shrink_dbg = nullptr;  // debug only (COLLM_SHRINK_DEBUG)
 // Shared-memory budget of the K5 reduction: lean = next to a GEMM CTA on the same SM (the
 // two-stream overlap, collm_set_gemm_lean), else up to the full ring depth.
-static bool g_reduce_lean = false;
+static std::atomic<bool> g_reduce_lean[kMaxDevices];
 
 // ------------------------------------------------------------------------------------ K1
 
@@ -361,7 +382,7 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (g_reduce_lean) {
+  if (g_reduce_lean[cur_device()]) {
     // next to a GEMM ask for the max-shared carveout: an SM this kernel reaches first must
     // still fit a GEMM CTA; alone, keep the default (more L1)
     attr[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
@@ -609,7 +630,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   // "lean" pipelines (~128 KB smem, <= 128 registers) leave room on every SM for one CTA of the
   // LoRA kernels running concurrently on a second stream (collm_set_gemm_lean / COLLM_GEMM_LEAN)
   const char* lean_env = getenv("COLLM_GEMM_LEAN");
-  const bool lean = lean_env ? atoi(lean_env) != 0 : g_gemm_lean;
+  const bool lean = lean_env ? atoi(lean_env) != 0 : g_gemm_lean[cur_device()].load();
   if (mc == 3) {
     if (lean) return launch_gemm<256, 5, 2, 3>(ta, tb, th, tlb, ty, p, grid, st);
     return launch_gemm<256, 6, 2, 3>(ta, tb, th, tlb, ty, p, grid, st);
@@ -688,8 +709,9 @@ int collm_preload(void) {
 }
 
 int collm_set_gemm_lean(int lean) {
-  g_gemm_lean = (lean & 1) != 0;  // 1: lean GEMM pipelines too; 2: rank-space kernels only
-  g_reduce_lean = lean != 0;
+  const int dev = cur_device();
+  g_gemm_lean[dev] = (lean & 1) != 0;  // 1: lean GEMM pipelines too; 2: rank-space kernels only
+  g_reduce_lean[dev] = lean != 0;
   return COLLM_OK;
 }
 
@@ -800,14 +822,19 @@ size_t collm_reduce_workspace_bytes(const collm_reduce_group* groups, int n_grou
 
 template <int QT, int MINB>
 static int launch_reduce(ReduceParams& p, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT, MINB>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ReduceSmem<QT>::total(kReduceMaxStages)));
-    configured = true;
+  static bool configured[kMaxDevices] = {};
+  const int dev = cur_device();
+  {
+    std::lock_guard<std::mutex> lk(g_state_mu);
+    if (!configured[dev]) {
+      CUDA_TRY(cudaFuncSetAttribute(lora_reduce_kernel<QT, MINB>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ReduceSmem<QT>::total(kReduceMaxStages)));
+      configured[dev] = true;
+    }
   }
-  const size_t budget = g_reduce_lean ? 44u * 1024 : 100u * 1024;
+  const bool reduce_lean = g_reduce_lean[dev];
+  const size_t budget = reduce_lean ? 44u * 1024 : 100u * 1024;
   int stages = kReduceMaxStages;
   while (stages > 2 && ReduceSmem<QT>::total(stages) > budget) --stages;
   p.stages = stages;
@@ -820,7 +847,7 @@ static int launch_reduce(ReduceParams& p, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributePreferredSharedMemoryCarveout;  // see collm_lora_shrink
   attr[0].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
   cfg.attrs = attr;
-  cfg.numAttrs = g_reduce_lean ? 1 : 0;
+  cfg.numAttrs = reduce_lean ? 1 : 0;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_reduce_kernel<QT, MINB>, p));
   return COLLM_OK;
 }
