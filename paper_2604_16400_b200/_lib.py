@@ -49,6 +49,11 @@ SIGNATURES: dict[str, tuple] = {
     "collm_expand_segments": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P]),
     "collm_lora_shrink": (_I, [_P, _I, _P, _LL, _I, _P, _I, _P, _IP, _I, _P, _P, _P, _I, _P, _P,
                                _P, _P, _P, _P]),
+    "collm_set_rank_sms": (_I, [_I]),
+    "collm_get_rank_sms": (_I, []),
+    "collm_plan_shrink_items": (_I, [_IP, _I, _I, _I, _IP, _I, _IP, _IP]),
+    "collm_lora_shrink_tc": (_I, [_P, _I, _I, _P, _LL, _I, _I, _P, _P, _I, _P, _IP, _I, _P, _P,
+                                  _P, _I, _P, _P, _P, _P]),
     "collm_cross_entropy": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _F, _P]),
     "collm_attention_workspace_bytes": (_SZ, [_I, _I, _I, _I]),
     "collm_paged_attention": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _I, _P, _I, _P, _P, _I, _F,

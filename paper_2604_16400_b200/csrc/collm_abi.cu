@@ -20,6 +20,7 @@
 #include "ce.cuh"
 #include "segments.cuh"
 #include "shrink.cuh"
+#include "shrink_tc.cuh"
 
 using namespace collm;
 
@@ -120,6 +121,28 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, ui
     return fail(COLLM_ECUDA, "cuTensorMapEncodeTiled failed (%d): cols=%llu rows=%llu ld=%llu",
                 (int)r, (unsigned long long)cols, (unsigned long long)rows,
                 (unsigned long long)ld);
+  return COLLM_OK;
+}
+
+// 3-D bf16 tensor map viewing a row-major [rows, ld] matrix as [k-block][row][64 columns]:
+// dims (64, rows, nkb) with strides (ld*2 B per row, 128 B per k-block); a box (64, box_rows,
+// box_kb) lands in shared memory k-block-major, each k-block a [box_rows][128 B] SWIZZLE_128B
+// tile — the K-major UMMA operand layout (lora_shrink_tc_kernel).
+int make_tmap_kblocks(CUtensorMap* m, const void* base, uint64_t rows, uint64_t ld, uint64_t nkb,
+                      uint32_t box_rows, uint32_t box_kb) {
+  auto fn = encode_fn();
+  if (!fn) return fail(COLLM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, rows, nkb};
+  cuuint64_t strides[2] = {ld * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, box_kb};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(COLLM_ECUDA, "cuTensorMapEncodeTiled (k-block view) failed (%d): rows=%llu ld=%llu nkb=%llu box=%ux%u",
+                (int)r, (unsigned long long)rows, (unsigned long long)ld, (unsigned long long)nkb,
+                box_rows, box_kb);
   return COLLM_OK;
 }
 
@@ -303,6 +326,9 @@ static unsigned long long* g_shrink_dbg = nullptr;  // debug only (COLLM_SHRINK_
 // Shared-memory budget of the K5 reduction: lean = next to a GEMM CTA on the same SM (the
 // two-stream overlap, collm_set_gemm_lean), else up to the full ring depth.
 static std::atomic<bool> g_reduce_lean[kMaxDevices];
+// Rank-space partition: SMs (whole TPCs) reserved for lora_shrink_tc_kernel; GEMM grids are capped
+// at the rest so both are always co-resident (collm_set_rank_sms).
+static std::atomic<int> g_rank_sms[kMaxDevices];
 
 // ------------------------------------------------------------------------------------ K1
 
@@ -402,6 +428,154 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
   return COLLM_OK;
 }
 
+
+// ------------------------------------------------------------------------------------ K1 (tc)
+int collm_set_rank_sms(int n) {
+  CHECK_ARG(n >= 0 && n % 2 == 0 && n <= 64, "rank SMs %d must be even and in [0, 64]", n);
+  g_rank_sms[cur_device()] = n;
+  return COLLM_OK;
+}
+int collm_get_rank_sms(void) { return g_rank_sms[cur_device()].load(); }
+
+// Host: merge the <= 16-row shrink tiles (collm_plan_segments) into items of <= max_rows
+// consecutive rows of one adapter, class = the smallest X box height (16/32/64/128) holding them,
+// and assign them to n_ctas CTAs longest-processing-time first (cost ~ rows of the class + the
+// adapter's rank rows, both streamed over the whole K range; base-only items cost ~nothing).
+// items[4*i] = row_start, n_rows, adapter, class; CTA c owns items [cta_ptr[c], cta_ptr[c+1]).
+int collm_plan_shrink_items(const int32_t* tiles, int n_tiles, int n_ctas, int max_rows,
+                            int32_t* items, int item_cap, int32_t* n_items, int32_t* cta_ptr) {
+  CHECK_ARG(n_tiles >= 0 && n_ctas >= 1, "n_tiles=%d n_ctas=%d", n_tiles, n_ctas);
+  CHECK_ARG(max_rows == 16 || max_rows == 32 || max_rows == 64 || max_rows == 128,
+            "max_rows=%d must be 16/32/64/128", max_rows);
+  struct It { int r0, n, a, cls; long long cost; };
+  std::vector<It> v;
+  for (int i = 0; i < n_tiles;) {
+    const int r0 = tiles[3 * i], a = tiles[3 * i + 2];
+    int n = tiles[3 * i + 1];
+    int j = i + 1;
+    while (j < n_tiles && tiles[3 * j + 2] == a && tiles[3 * j] == r0 + n &&
+           n + tiles[3 * j + 1] <= max_rows) {
+      n += tiles[3 * j + 1];
+      ++j;
+    }
+    int cls = 0;
+    while ((16 << cls) < n) ++cls;
+    v.push_back({r0, n, a, cls, a < 0 ? 1 : (long long)(16 << cls) + 64});
+    i = j;
+  }
+  CHECK_ARG((int)v.size() <= item_cap, "shrink item capacity %d exceeded (%zu)", item_cap, v.size());
+  std::vector<int> order(v.size());
+  for (size_t i = 0; i < v.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return v[x].cost > v[y].cost; });
+  std::vector<long long> load(n_ctas, 0);
+  std::vector<std::vector<int>> per(n_ctas);
+  for (int i : order) {
+    int c = 0;
+    for (int k = 1; k < n_ctas; ++k)
+      if (load[k] < load[c]) c = k;
+    load[c] += v[i].cost;
+    per[c].push_back(i);
+  }
+  int w = 0;
+  for (int c = 0; c < n_ctas; ++c) {
+    if (cta_ptr) cta_ptr[c] = w;
+    for (int i : per[c]) {
+      if (items) {
+        items[4 * w] = v[i].r0;
+        items[4 * w + 1] = v[i].n;
+        items[4 * w + 2] = v[i].a;
+        items[4 * w + 3] = v[i].cls;
+      }
+      ++w;
+    }
+  }
+  if (cta_ptr) cta_ptr[n_ctas] = w;
+  if (n_items) *n_items = w;
+  return COLLM_OK;
+}
+
+int collm_lora_shrink_tc(const void* X, int ldx, int x_rows, const void* A, long long a_stride,
+                         int lda, int a_rows, const int32_t* items, const int32_t* cta_ptr,
+                         int n_ctas, const float* scale, const int32_t* groups, int n_groups,
+                         float* H32, void* H16, void* H16lo, int ldh, void* Hslots,
+                         const int32_t* slot_of_row, const int32_t* tile_slot_ptr, void* stream) {
+  CHECK_ARG(X && A && items && cta_ptr && scale && groups, "null input");
+  CHECK_ARG(!H16lo || H16, "H16lo needs H16");
+  CHECK_ARG(n_ctas >= 2 && n_ctas % 2 == 0, "n_ctas=%d must be even (TPC pairs)", n_ctas);
+  CHECK_ARG(n_groups >= 1 && n_groups <= kShrinkTcMaxGroups, "n_groups=%d out of [1,%d]", n_groups,
+            kShrinkTcMaxGroups);
+  CHECK_ARG(ldx % 8 == 0 && lda % 8 == 0 && ldh % 16 == 0, "ldx/lda must be x8, ldh x16");
+  CHECK_ARG(a_stride % lda == 0, "a_stride must be a multiple of lda");
+  CHECK_ARG(aligned16(X) && aligned16(A), "X/A must be 16-byte aligned");
+  CHECK_ARG(!Hslots || (slot_of_row && tile_slot_ptr), "Hslots needs slot_of_row, tile_slot_ptr");
+  CHECK_ARG(x_rows >= 1 && a_rows >= 1, "empty X/A");
+  ShrinkTcParams p{};
+  p.n_groups = n_groups;
+  p.nr = groups[1];
+  int k_end = 0;
+  for (int g = 0; g < n_groups; ++g) {
+    const int ro = groups[4 * g], nr = groups[4 * g + 1], klo = groups[4 * g + 2], khi = groups[4 * g + 3];
+    CHECK_ARG(nr == p.nr && nr % 16 == 0 && nr >= 16 && nr <= 256,
+              "group %d: n_ranks=%d (all groups equal, multiple of 16 in [16,256])", g, nr);
+    CHECK_ARG(klo >= 0 && khi > klo && klo % 64 == 0 && khi % 64 == 0,
+              "group %d: K range [%d,%d) must be non-empty and 64-aligned", g, klo, khi);
+    CHECK_ARG(ro >= 0 && ro + nr <= ldh, "group %d: ranks [%d,%d) exceed ldh=%d", g, ro, ro + nr, ldh);
+    p.groups[g] = {ro, klo, khi};
+    k_end = std::max(k_end, khi);
+  }
+  CHECK_ARG(k_end <= ldx && k_end <= lda, "K range %d exceeds ldx=%d / lda=%d", k_end, ldx, lda);
+  p.items = items;
+  p.cta_ptr = cta_ptr;
+  p.a_rows_per_adapter = (int)(a_stride / lda);
+  p.scale = scale;
+  p.H32 = H32;
+  p.H16 = (bf16*)H16;
+  p.H16lo = (bf16*)H16lo;
+  p.ldh = ldh;
+  p.Hslots = (bf16*)Hslots;
+  p.slot_of_row = slot_of_row;
+  p.tile_slot_ptr = tile_slot_ptr;
+  { const char* e = getenv("COLLM_DEBUG_SHRINK_NO_MMA"); p.debug_no_mma = e ? atoi(e) : 0; }
+  CUtensorMap tx[kShrinkTcClasses], ta[kShrinkTcClasses];
+  for (int c = 0; c < kShrinkTcClasses; ++c) {
+    const int nb = 16 << c;
+    // k-blocks per stage: fill the ~64 KB stage (bigger copies stream faster per SM, tools/sm_bw.py)
+    int kb = (int)(kShrinkTcStageBytes / ((uint32_t)(nb + p.nr) * 128));
+    kb = std::max(1, std::min(16, kb));
+    p.nb[c] = nb;
+    p.kb[c] = kb;
+    int rc = make_tmap_kblocks(&tx[c], X, x_rows, ldx, k_end / 64, nb, kb);
+    if (rc) return rc;
+    rc = make_tmap_kblocks(&ta[c], A, a_rows, lda, k_end / 64, p.nr, kb);
+    if (rc) return rc;
+  }
+  {
+    static bool configured[kMaxDevices] = {};
+    const int dev = cur_device();
+    std::lock_guard<std::mutex> lk(g_state_mu);
+    if (!configured[dev]) {
+      CUDA_TRY(cudaFuncSetAttribute(lora_shrink_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    ShrinkTcSmem::kTotal));
+      configured[dev] = true;
+    }
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(n_ctas);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = ShrinkTcSmem::kTotal;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // CTA pairs: the grid holds whole TPCs
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_tc_kernel, tx[0], tx[1], tx[2], tx[3], ta[0], ta[1],
+                              ta[2], ta[3], p));
+  return COLLM_OK;
+}
+
 // ------------------------------------------------------------------------------------ K2/K3
 
 
@@ -452,7 +626,9 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
   // N tile: 256 unless the sub-projection boundaries (or a narrow N) call for 128; stream-K
   // removes the wave-quantization reason to prefer narrower tiles.
   static const int max_sms_env = [] { const char* e = getenv("COLLM_GEMM_MAX_SMS"); return e ? atoi(e) : 0; }();
-  const int sms = max_sms_env > 0 ? std::min(num_sms_cached(), max_sms_env) : num_sms_cached();  // debug cap
+  const int rank_sms = g_rank_sms[cur_device()].load();  // reserved for the rank-space kernels
+  const int sms_avail = num_sms_cached() - rank_sms;
+  const int sms = max_sms_env > 0 ? std::min(sms_avail, max_sms_env) : sms_avail;  // debug cap
   auto aligned_to = [&](int t) {
     if (!lora || !sub_n_start) return true;
     for (int i = 1; i < n_sub; ++i)
@@ -503,7 +679,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
           // pairs only, needs 2 x tiles <= units); calibrated swap cost ~4 us
           if (cg != 2 || 2 * tiles > units || nk < 2) continue;  // both halves non-empty
           if (mc == 2 && tiles > (b == 256 ? max_gemm_clusters<256, 6, 2, 2>()
-                                           : max_gemm_clusters<128, 8, 2, 2>()))
+                                           : max_gemm_clusters<128, 8, 2, 2>()) - rank_sms / 2)
             continue;
           cost = std::ceil(nk / 2.0) * kb + (mc == 2 ? 1.5 : 4.0);
         } else if (mc == 2) {
@@ -675,6 +851,7 @@ int collm_preload(void) {
   COLLM_PRELOAD((lora_shrink_kernel<4, 3>));
   COLLM_PRELOAD((lora_shrink_kernel<6, 2>));
   COLLM_PRELOAD((lora_shrink_kernel<8, 2>));
+  COLLM_PRELOAD(lora_shrink_tc_kernel);
   COLLM_PRELOAD((gemm_lora_kernel<256, 6, 2, 1>));
   COLLM_PRELOAD((gemm_lora_kernel<128, 8, 2, 1>));
   COLLM_PRELOAD((gemm_lora_kernel<256, 5, 2, 1>));

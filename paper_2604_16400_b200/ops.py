@@ -138,6 +138,71 @@ def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: 
               _p(gen), _stream())
 
 
+_rank_sms: dict[int, int] = {}
+
+
+def set_rank_sms(n: int, device: torch.device | None = None) -> None:
+    """Reserve ``n`` SMs (even, whole TPCs) of ``device`` for the rank-space kernels
+    (collm_set_rank_sms): shrinks then run as ``collm_lora_shrink_tc`` on that partition and every
+    GEMM grid is capped at the remaining SMs.  0 switches back to the whole-GPU shrink."""
+    d = (device or torch.device("cuda", torch.cuda.current_device())).index or 0
+    with torch.cuda.device(d):
+        _lib.call("collm_set_rank_sms", int(n))
+    _rank_sms[d] = int(n)
+
+
+def rank_sms(device: torch.device | None = None) -> int:
+    d = (device or torch.device("cuda", torch.cuda.current_device())).index or 0
+    if d not in _rank_sms:
+        n = int(__import__("os").environ.get("COLLM_RANK_SMS", "0"))
+        if n:
+            set_rank_sms(n, torch.device("cuda", d))
+        else:
+            _rank_sms[d] = 0
+    return _rank_sms[d]
+
+
+def shrink_tc_groups(groups: list[tuple[int, int, int, int]]) -> list[tuple[int, int, int, int]] | None:
+    """The group table for collm_lora_shrink_tc, or None when it does not apply: adjacent groups
+    over the same K range merge into one (<= 256 ranks), every group must then have the same
+    width (a multiple of 16) and 64-aligned K ranges."""
+    out: list[list[int]] = []
+    for ro, nr, klo, khi in groups:
+        if out and out[-1][2] == klo and out[-1][3] == khi and out[-1][0] + out[-1][1] == ro \
+                and out[-1][1] + nr <= 256:
+            out[-1][1] += nr
+        else:
+            out.append([ro, nr, klo, khi])
+    if len({g[1] for g in out}) != 1 or len(out) > 8:
+        return None
+    if any(g[1] % 16 or g[2] % 64 or g[3] % 64 for g in out):
+        return None
+    return [tuple(g) for g in out]
+
+
+def lora_shrink_tc(X: torch.Tensor, A: torch.Tensor, items: torch.Tensor, cta_ptr: torch.Tensor,
+                   n_ctas: int, scale: torch.Tensor, groups: list[tuple[int, int, int, int]],
+                   ldh: int, *, a_stride: int | None = None, H32: torch.Tensor | None = None,
+                   H16: torch.Tensor | None = None, H16lo: torch.Tensor | None = None,
+                   Hslots: torch.Tensor | None = None, slot_of_row: torch.Tensor | None = None,
+                   tile_slot_ptr: torch.Tensor | None = None) -> None:
+    """K1 on the rank-space SM partition (collm_lora_shrink_tc): same outputs as lora_shrink;
+    ``groups`` from :func:`shrink_tc_groups`, items / cta_ptr from the plan."""
+    _need(X, torch.bfloat16, "X")
+    _need(A, torch.bfloat16, "A")
+    if not _launch("shrink"):
+        return
+    lda = A.stride(-2)
+    if a_stride is None:
+        a_stride = A.stride(0) if A.dim() == 3 else 0
+    a_rows = A.numel() // lda
+    flat = [v for g in groups for v in g]
+    _lib.call("collm_lora_shrink_tc", X.data_ptr(), X.stride(0), X.shape[0], A.data_ptr(),
+              int(a_stride), lda, a_rows, items.data_ptr(), cta_ptr.data_ptr(), n_ctas,
+              scale.data_ptr(), _lib.int_array(flat), len(groups), _p(H32), _p(H16), _p(H16lo),
+              ldh, _p(Hslots), _p(slot_of_row), _p(tile_slot_ptr), _stream())
+
+
 def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | None = None,
               Hslots: torch.Tensor | None = None, h_rows: int = 0, LB: torch.Tensor | None = None,
               lb_rows: int = 0, tile_slot_ptr: torch.Tensor | None = None,

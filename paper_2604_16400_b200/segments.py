@@ -113,6 +113,26 @@ def plan_segments(seg_start, seg_adapter) -> HostPlan:
     return HostPlan(ss, sa, tsp, slots[: ns.value].copy(), tiles[: nt.value].copy())
 
 
+def plan_shrink_items(host: HostPlan, n_ctas: int, max_rows: int | None = None):
+    """collm_plan_shrink_items: the shrink tiles merged into <=max_rows-row items and assigned
+    longest-first to ``n_ctas`` CTAs -> (items [n, 4], cta_ptr [n_ctas + 1]).  Without
+    ``max_rows`` the largest of 128/64/32 that still yields an item per CTA is used."""
+    tiles = np.ascontiguousarray(host.shrink_tiles.reshape(-1, 3).astype(np.int32))
+    nt = int(tiles.shape[0])
+    ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))  # noqa: E731
+    cands = [max_rows] if max_rows else [128, 64, 32]
+    for mr in cands:
+        cap = max(1, int(host.seg_start[-1]) // 16 + nt + 1)
+        items = np.zeros((cap, 4), np.int32)
+        ptr = np.zeros(n_ctas + 1, np.int32)
+        n = C.c_int32(0)
+        _lib.call("collm_plan_shrink_items", ip(tiles), nt, n_ctas, mr, ip(items), cap,
+                  C.byref(n), ip(ptr))
+        if n.value >= n_ctas:
+            break
+    return items[: max(1, n.value)].copy(), ptr
+
+
 def uniform_plan(n_rows: int, adapter: int) -> HostPlan:
     """Plan for rows [0, n_rows) that all use one adapter (the training rows' backward)."""
     return plan_segments([0, n_rows], [adapter])
@@ -122,15 +142,24 @@ class DevicePlan:
     """Device-resident plan of one pass, shared by every projection of every layer."""
 
     def __init__(self, host: HostPlan, device: torch.device | str = "cuda",
-                 stream: torch.cuda.Stream | None = None, expand: bool = True):
+                 stream: torch.cuda.Stream | None = None, expand: bool = True,
+                 tc_ctas: int | None = None):
         self.host = host
         self.n_rows = int(host.seg_start[-1])
         self.n_tiles_m = (self.n_rows + TILE_M - 1) // TILE_M
         dev = torch.device(device)
-        # one packed upload: [seg_start | seg_adapter | tile_slot_ptr | slot_adapter | shrink_tiles]
+        if tc_ctas is None:  # the rank-space partition of this device (collm_set_rank_sms)
+            from . import ops
+            tc_ctas = ops.rank_sms(dev) if dev.type == "cuda" else 0
+        self.tc_ctas = int(tc_ctas)
+        items, cta_ptr = (plan_shrink_items(host, self.tc_ctas) if self.tc_ctas
+                          else (np.zeros((1, 4), np.int32), np.zeros(1, np.int32)))
+        # one packed upload: [seg_start | seg_adapter | tile_slot_ptr | slot_adapter | shrink_tiles
+        #                     | shrink items | item ranges per CTA]
         parts = [host.seg_start, host.seg_adapter, host.tile_slot_ptr,
                  host.slot_adapter if host.n_slots else np.zeros(1, np.int32),
-                 host.shrink_tiles.reshape(-1) if host.shrink_tiles.size else np.zeros(3, np.int32)]
+                 host.shrink_tiles.reshape(-1) if host.shrink_tiles.size else np.zeros(3, np.int32),
+                 items.reshape(-1), cta_ptr]
         sizes = [p.size for p in parts]
         packed = torch.from_numpy(np.concatenate(parts).astype(np.int32)).pin_memory()
         self.h2d_bytes = packed.numel() * 4
@@ -144,6 +173,8 @@ class DevicePlan:
         self.tile_slot_ptr = buf[offs[2]:offs[3]]
         self.slot_adapter = buf[offs[3]:offs[4]]
         self.shrink_tiles = buf[offs[4]:offs[5]]
+        self.tc_items = buf[offs[5]:offs[6]]
+        self.tc_cta_ptr = buf[offs[6]:offs[7]]
         self.n_slots = host.n_slots
         self.max_adapter = int(host.seg_adapter.max()) if host.seg_adapter.size else -1
         self.n_shrink_tiles = int(host.shrink_tiles.shape[0])

@@ -88,8 +88,18 @@ def _stack_inputs(st, plan, l=0):
     return out
 
 
+@pytest.fixture(params=[0, 16], ids=["shrink-all-sms", "shrink-rank-partition"])
+def rank_sms(request):
+    """0: the whole-GPU shrink; 16: the rank-space SM partition (collm_lora_shrink_tc, GEMM grids
+    capped at the other 132 SMs)."""
+    from paper_2604_16400_b200 import ops
+    ops.set_rank_sms(request.param)
+    yield request.param
+    ops.set_rank_sms(0)
+
+
 @pytest.mark.parametrize("key", CONFIGS)
-def test_baseline_layer_matches_oracle(key):
+def test_baseline_layer_matches_oracle(key, rank_sms):
     from paper_2604_16400_b200.replica import ReplicaStack
     cfg = _one_layer(key)
     train, items = cfg.batch(0)

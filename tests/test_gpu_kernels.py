@@ -149,6 +149,83 @@ def test_shrink(R, K):
     _close_bf16(H16.cpu(), ref)
 
 
+@pytest.mark.parametrize("R,K,n_ctas,dh", [(16, 512, 2, False), (48, 4096, 16, False),
+                                           (96, 1024, 8, False), (192, 5120, 16, False),
+                                           (48, 11008, 8, True), (192, 2048, 4, True)])
+def test_shrink_tc(R, K, n_ctas, dh):
+    """K1 on the rank-space partition (collm_lora_shrink_tc: TMA k-block boxes -> tcgen05 ->
+    TMEM): items of <= 128 rows merged from ragged 16-row tiles (1-row tile, a base-only
+    segment, a >128-row run, rows crossing a 256-row slot tile), fused rank groups up to 192,
+    K up to 11008; per-sub K ranges with one adapter (the dH shape, ``dh``).  H32 vs an fp32
+    reference (rel <= 1e-4), H16 / H16lo pair, Hslots (own slot = H16, other slots of the row's
+    256-row tile = 0), bitwise repeatable."""
+    import numpy as np
+    from paper_2604_16400_b200 import ops, segments
+    g = torch.Generator().manual_seed(R + K)
+    n_ad = 5
+    if dh:
+        seg, seg_ad = [0, 300], [3]
+    else:
+        seg, seg_ad = [0, 40, 41, 90, 150, 160, 430], [2, 0, 3, -1, 1, 4]
+    T = seg[-1]
+    X = _bf(T, K, gen=g)
+    A = _bf(n_ad, R, K, scale=0.05, gen=g)
+    scale = torch.tensor([1.0, 2.0, 0.5, 3.0, 0.25]).cuda()
+    host = segments.plan_segments(seg, seg_ad)
+    items, ptr = segments.plan_shrink_items(host, n_ctas)
+    it_d = torch.from_numpy(items).cuda()
+    ptr_d = torch.from_numpy(ptr).cuda()
+    if dh:  # per-sub K ranges (N ranges of the fused projection), one group per sub
+        n_sub = 3 if R % 3 == 0 else 2
+        rp = R // n_sub
+        bnd = [0] + [K * (s + 1) // n_sub // 64 * 64 for s in range(n_sub - 1)] + [K]
+        groups = [(s * rp, rp, bnd[s], bnd[s + 1]) for s in range(n_sub)]
+    else:
+        groups = [(0, R, 0, K)]
+    tc = ops.shrink_tc_groups(groups)
+    assert tc is not None
+    H32 = torch.zeros(T, R, device="cuda")
+    H16 = torch.zeros(T, R, dtype=torch.bfloat16, device="cuda")
+    H16lo = torch.zeros(T, R, dtype=torch.bfloat16, device="cuda")
+    dp = segments.DevicePlan(host, "cuda", tc_ctas=0)
+    torch.cuda.synchronize()
+    n_slots = host.n_slots
+    Hs = torch.full((max(1, n_slots) * 256, R), 7.0, dtype=torch.bfloat16, device="cuda")
+    kw = dict(H32=H32, H16=H16, H16lo=H16lo)
+    if not dh:
+        kw.update(Hslots=Hs, slot_of_row=dp.slot_of_row, tile_slot_ptr=dp.tile_slot_ptr)
+    ops.lora_shrink_tc(X, A, it_d, ptr_d, n_ctas, scale, tc, R, **kw)
+    H32b = torch.zeros_like(H32)
+    ops.lora_shrink_tc(X, A, it_d, ptr_d, n_ctas, scale, tc, R, H32=H32b)
+    torch.cuda.synchronize()
+    assert torch.equal(H32, H32b)
+    ref = torch.zeros(T, R)
+    Xc, Ac = X.float().cpu(), A.float().cpu()
+    for s in range(len(seg_ad)):
+        a = seg_ad[s]
+        if a < 0:
+            continue
+        rows = slice(seg[s], seg[s + 1])
+        for ro, nr, klo, khi in groups:
+            ref[rows, ro:ro + nr] = scale[a].item() * (Xc[rows, klo:khi] @ Ac[a, ro:ro + nr, klo:khi].t())
+    has = torch.tensor(np.repeat(np.array(seg_ad) >= 0, np.diff(seg)))
+    rel = (H32.cpu()[has] - ref[has]).norm() / ref.norm()
+    assert rel < 1e-4, rel
+    _close_bf16(H16.cpu()[has], ref[has])
+    pair = H16.cpu().double() + H16lo.cpu().double()
+    assert torch.allclose(pair[has], H32.cpu().double()[has], rtol=1e-5, atol=1e-7)
+    if not dh:
+        tsp = host.tile_slot_ptr
+        slot_of_row = dp.slot_of_row.cpu().numpy()
+        Hs_c = Hs.cpu()
+        for t in range(T):
+            m = t // 256
+            for sl in range(tsp[m], tsp[m + 1]):
+                got = Hs_c[sl * 256 + t % 256]
+                want = H16.cpu()[t] if (has[t] and sl == slot_of_row[t]) else torch.zeros(R, dtype=torch.bfloat16)
+                assert torch.equal(got, want), (t, sl)
+
+
 def test_reduce_adamw():
     from paper_2604_16400_b200 import _lib, ops
     g = torch.Generator().manual_seed(5)

@@ -147,3 +147,32 @@ def test_flop_accounting_matches_survey():
     specs = cfg.projections
     assert [s.name for s in specs] == ["qkv", "o", "gate_up", "down"]
     assert sum(2 * s.in_features * s.out_features for s in specs) * 32 == per_row
+
+
+@pytest.mark.parametrize("n_ctas", [2, 8, 16])
+def test_plan_shrink_items(lib, n_ctas):
+    """collm_plan_shrink_items (host): the <=16-row shrink tiles merge into items of consecutive
+    rows of ONE adapter (never across adapters or base-only runs, never above max_rows), every
+    row is covered exactly once, the class is the smallest box height holding the item, and the
+    longest-first assignment keeps the CTA loads within one item of each other."""
+    import numpy as np
+    from paper_2604_16400_b200 import segments
+    g = np.random.default_rng(n_ctas)
+    lens = g.integers(1, 300, 40)
+    ads = g.integers(-1, 12, 40)
+    ads[1:][ads[1:] == ads[:-1]] = 12  # break equal neighbours (the planner merges runs anyway)
+    seg = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    host = segments.plan_segments(seg, ads)
+    for mr in (128, 32):
+        items, ptr = segments.plan_shrink_items(host, n_ctas, max_rows=mr)
+        assert ptr[0] == 0 and ptr[-1] == len(items) and np.all(np.diff(ptr) >= 0)
+        row_ad = np.repeat(ads, lens)
+        covered = np.zeros(seg[-1], np.int32)
+        for r0, n, a, cls in items:
+            assert 1 <= n <= mr and (16 << cls) >= n and (cls == 0 or (16 << (cls - 1)) < n)
+            assert np.all(row_ad[r0:r0 + n] == a)
+            covered[r0:r0 + n] += 1
+        assert np.all(covered == 1)
+        cost = [(16 << c) + 64 if a >= 0 else 1 for _, _, a, c in items]
+        loads = [sum(cost[ptr[c]:ptr[c + 1]]) for c in range(n_ctas)]
+        assert max(loads) - min(loads) <= max(cost)

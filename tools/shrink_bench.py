@@ -9,7 +9,10 @@ import torch  # noqa: E402
 from paper_2604_16400_b200 import ops, segments  # noqa: E402
 from paper_2604_16400_b200.configs import CONFIGS  # noqa: E402
 
-cfg = CONFIGS["llama2-7b"]
+cfg = CONFIGS[os.environ.get("CFG", "llama2-7b")]
+TC = int(os.environ.get("TC", "0"))  # rank-space partition size: collm_lora_shrink_tc
+if TC:
+    ops.set_rank_sms(TC)
 mb = segments.build_mixed_batch(*cfg.batch(0))
 plan = segments.DevicePlan(segments.plan_segments(mb.seg_start, mb.seg_adapter))
 tplan = segments.DevicePlan(segments.uniform_plan(mb.n_train_rows, mb.train_adapter))
@@ -32,6 +35,11 @@ for name, K, R, fwd, subs in (("fwd qkv", 4096, 48, True, 1), ("fwd o", 4096, 16
         groups = [(g, min(64, R - g), 0, K) for g in range(0, R, 64)]
 
         def run(i):
+            if TC:
+                ops.lora_shrink_tc(Xs[i % reps], A, plan.tc_items, plan.tc_cta_ptr, TC, scale,
+                                   ops.shrink_tc_groups(groups), R, H16=H16, Hslots=Hs,
+                                   slot_of_row=plan.slot_of_row, tile_slot_ptr=plan.tile_slot_ptr)
+                return
             ops.lora_shrink(Xs[i % reps], A, plan.shrink_tiles, plan.n_shrink_tiles, scale, groups, R,
                             H16=H16, Hslots=Hs, slot_of_row=plan.slot_of_row,
                             tile_slot_ptr=plan.tile_slot_ptr)
@@ -47,6 +55,10 @@ for name, K, R, fwd, subs in (("fwd qkv", 4096, 48, True, 1), ("fwd o", 4096, 16
         groups = [(s * rp, rp, s * n, (s + 1) * n) for s in range(subs)]
 
         def run(i):
+            if TC:
+                ops.lora_shrink_tc(Xs[i % reps], BT, tplan.tc_items, tplan.tc_cta_ptr, TC, scale,
+                                   ops.shrink_tc_groups(groups), R, a_stride=0, H16=H16, H16lo=H16lo)
+                return
             ops.lora_shrink(Xs[i % reps], BT, tplan.shrink_tiles, tplan.n_shrink_tiles, scale, groups,
                             R, a_stride=0, H16=H16, H16lo=H16lo)
         nbytes = 2 * Ttr * K + 2 * R * K
@@ -70,5 +82,5 @@ for name, K, R, fwd, subs in (("fwd qkv", 4096, 48, True, 1), ("fwd o", 4096, 16
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / n * 1e3
     res.append((name, us, nbytes / us / 1e6))
-print(f"COLLM_SHRINK_CTAS_PER_SM={os.environ.get('COLLM_SHRINK_CTAS_PER_SM', '6')}: " +
+print(f"TC={TC}: " +
       "  ".join(f"{n} {us:.1f}us {tb:.2f}TB/s" for n, us, tb in res))
