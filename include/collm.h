@@ -215,6 +215,29 @@ int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_h
                           const int32_t* row_pos, int max_ctx, float scale, void* out, int ldo,
                           void* workspace, size_t ws_bytes, void* stream);
 
+/* ---- K9: causal self-attention of packed sequences, forward + backward ------------------------
+ * Sequences are row ranges [seq_start[s], seq_start[s+1]) (device int32, n_seq + 1 entries) — the
+ * training sequences and prefill segments of the mixed batch; row i attends to rows
+ * [seq_start[s], i] of its sequence.  q [T, ldq] (head h at columns h*128), k / v [T, ldk/ldv]
+ * (kv head h/G), typically column blocks of the fused q|k|v projection output.  max_seqlen >= the
+ * longest sequence.  head_dim 128; GQA with n_heads a multiple of n_kv_heads.
+ * fwd: out [T, ldo] bf16, lse [n_heads, T] fp32 = base-2 log-sum-exp of scale*log2(e)*scores
+ *      (kept for the backward).
+ * bwd: delta [n_heads, T] fp32 workspace; dq / dk / dv bf16 (dk/dv per kv head: the G query heads
+ *      of a group summed in a fixed order).  Deterministic: no atomics (dK/dV and dQ in separate
+ *      kernels, each output element owned by one CTA).  fp32 softmax and accumulation.
+ * Replaces: nothing in the reference (it has no attention); SURVEY §8(f) row 1. */
+int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
+                              void* out, int ldo, float* lse, int T, int n_heads, int n_kv_heads,
+                              int head_dim, const int32_t* seq_start, int n_seq, int max_seqlen,
+                              float scale, void* stream);
+int collm_flash_attention_bwd(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
+                              const void* out, int ldo, const void* dout, int lddo, const float* lse,
+                              float* delta, void* dq, int lddq, void* dk, int lddk, void* dv, int lddv,
+                              int T, int n_heads, int n_kv_heads, int head_dim,
+                              const int32_t* seq_start, int n_seq, int max_seqlen, float scale,
+                              void* stream);
+
 /* ---- K7: softmax cross-entropy forward + backward over LM-head logits ------------------------
  * For each row t of logits [T, ld] (bf16, V used columns, V and ld multiples of 8):
  *   loss_rows[t] = logsumexp(z_t) - z_t[labels[t]]  (0 when labels[t] < 0 or >= V: ignored)

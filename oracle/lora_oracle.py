@@ -28,6 +28,7 @@ __all__ = [
     "bf16_round", "bf16_to_bits", "bits_to_f32", "build_rows", "expand_segments", "tile_slots",
     "slot_of_row", "shrink_tiles", "lora_shrink", "lora_forward", "lora_backward", "adamw_step", "AdamWState",
     "fedavg", "AggregationError", "projection_flops", "cross_entropy", "paged_attention",
+    "causal_attention",
 ]
 
 
@@ -270,6 +271,54 @@ def cross_entropy(logits, labels, grad_scale=None):
     d *= g
     d[~valid] = 0.0
     return loss_rows, mean, d
+
+
+# --------------------------------------------------------------------------- attention (K9)
+def causal_attention(q, k, v, seq_start, n_heads, n_kv_heads, scale=None, dout=None):
+    """Causal self-attention of packed sequences (row ranges seq_start[s]..seq_start[s+1]; row i
+    attends to rows [seq_start[s], i]) and, with ``dout``, its backward — float64 restatement of
+    the standard softmax attention gradient (dV = P^T dO, dP = dO V^T, dS = P (dP - rowsum(dO O)),
+    dQ = scale dS K, dK = scale dS^T Q; GQA: dK/dV summed over the G heads of a kv head).
+    q [T, n_heads*D], k / v [T, n_kv_heads*D].  Returns out, lse2 [n_heads, T] (base-2
+    log-sum-exp of scale*log2(e)*scores) and, with dout, (dq, dk, dv)."""
+    q = np.asarray(q, np.float64)
+    k = np.asarray(k, np.float64)
+    v = np.asarray(v, np.float64)
+    T = q.shape[0]
+    D = q.shape[1] // n_heads
+    G = n_heads // n_kv_heads
+    sc = D ** -0.5 if scale is None else scale
+    out = np.zeros_like(q)
+    lse2 = np.zeros((n_heads, T))
+    grads = None
+    if dout is not None:
+        dout = np.asarray(dout, np.float64)
+        grads = (np.zeros_like(q), np.zeros_like(k), np.zeros_like(v))
+    for s in range(len(seq_start) - 1):
+        a, b = int(seq_start[s]), int(seq_start[s + 1])
+        n = b - a
+        mask = np.tril(np.ones((n, n), bool))
+        for h in range(n_heads):
+            hk = h // G
+            Q = q[a:b, h * D:(h + 1) * D]
+            K = k[a:b, hk * D:(hk + 1) * D]
+            V = v[a:b, hk * D:(hk + 1) * D]
+            S = np.where(mask, Q @ K.T * sc, -np.inf)
+            m = S.max(axis=1, keepdims=True)
+            E = np.exp(S - m)
+            Z = E.sum(axis=1, keepdims=True)
+            P = E / Z
+            O = P @ V
+            out[a:b, h * D:(h + 1) * D] = O
+            lse2[h, a:b] = (m[:, 0] + np.log(Z[:, 0])) / np.log(2.0)
+            if grads is not None:
+                dO = dout[a:b, h * D:(h + 1) * D]
+                dP = dO @ V.T
+                dS = P * (dP - (dO * O).sum(axis=1, keepdims=True))
+                grads[0][a:b, h * D:(h + 1) * D] += sc * dS @ K
+                grads[1][a:b, hk * D:(hk + 1) * D] += sc * dS.T @ Q
+                grads[2][a:b, hk * D:(hk + 1) * D] += P.T @ dO
+    return (out, lse2) if grads is None else (out, lse2, grads)
 
 
 # --------------------------------------------------------------------------- attention (K8)

@@ -349,3 +349,47 @@ def test_paged_attention_vs_oracle(n_heads, n_kv):
     torch.cuda.synchronize()
     assert torch.equal(out, out2)
     assert np.isfinite(out.float().cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("lens,n_heads,n_kv", [([512], 4, 4), ([1, 63, 64, 65, 200], 4, 2),
+                                               ([130, 7, 300], 8, 2), ([1024], 2, 1)])
+def test_flash_attention_vs_oracle(lens, n_heads, n_kv):
+    """K9: causal attention of packed sequences (ragged lengths incl. 1, tile boundaries 63/64/65,
+    GQA G = 1/2/4) forward + backward against the float64 oracle; q/k/v are column views of one
+    fused q|k|v buffer as in the step; the backward is bitwise repeatable."""
+    import numpy as np
+    import oracle
+    from paper_2604_16400_b200 import ops
+    g = torch.Generator().manual_seed(sum(lens) + n_heads)
+    D = 128
+    T = sum(lens)
+    seq = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    W = (n_heads + 2 * n_kv) * D
+    qkv = _bf(T, W, gen=g)
+    q, k, v = qkv[:, :n_heads * D], qkv[:, n_heads * D:(n_heads + n_kv) * D], qkv[:, (n_heads + n_kv) * D:]
+    dout = _bf(T, n_heads * D, gen=g)
+    out = torch.zeros(T, n_heads * D, dtype=torch.bfloat16, device="cuda")
+    lse = torch.zeros(n_heads, T, device="cuda")
+    ss = torch.from_numpy(seq).cuda()
+    kw = dict(T=T, n_heads=n_heads, n_kv_heads=n_kv, max_seqlen=max(lens))
+    ops.flash_attention(q, k, v, out, lse, ss, **kw)
+    dqkv = torch.zeros_like(qkv)
+    dq, dk, dv = dqkv[:, :n_heads * D], dqkv[:, n_heads * D:(n_heads + n_kv) * D], dqkv[:, (n_heads + n_kv) * D:]
+    delta = torch.zeros(n_heads, T, device="cuda")
+    ops.flash_attention_bwd(q, k, v, out, dout, lse, delta, dq, dk, dv, ss, **kw)
+    dqkv2 = torch.zeros_like(qkv)
+    ops.flash_attention_bwd(q, k, v, out, dout, lse, delta, dqkv2[:, :n_heads * D],
+                            dqkv2[:, n_heads * D:(n_heads + n_kv) * D],
+                            dqkv2[:, (n_heads + n_kv) * D:], ss, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(dqkv, dqkv2)
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    ref, lse_ref, (dq_r, dk_r, dv_r) = oracle.causal_attention(f(q), f(k), f(v), seq, n_heads, n_kv,
+                                                               dout=f(dout))
+    for got, want, what in ((f(out), ref, "out"), (f(dq), dq_r, "dq"), (f(dk), dk_r, "dk"),
+                            (f(dv), dv_r, "dv")):
+        err = np.abs(got - want).max()
+        assert err <= 1e-2 * np.abs(want).max() + 1e-3, (what, err)
+        rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert rel <= 1e-2, (what, rel)
+    assert np.abs(lse.cpu().numpy() - lse_ref).max() <= 1e-3

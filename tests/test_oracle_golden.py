@@ -165,3 +165,37 @@ def test_paged_attention_oracle_vs_torch_sdpa():
                                           is_causal=True)
     np.testing.assert_allclose(got[1:], ref1.permute(1, 0, 2).reshape(lens[1], -1).numpy(),
                                rtol=1e-10, atol=1e-10)
+
+
+def test_causal_attention_oracle_vs_torch_autograd():
+    """Pin K9's oracle (oracle.causal_attention fwd + bwd, packed causal sequences, GQA) against
+    torch float64 autograd of softmax attention written independently (masked full matrices)."""
+    import numpy as np
+    import torch
+    import oracle
+    g = np.random.default_rng(3)
+    lens, H, Hk, D = [5, 1, 9], 4, 2, 16
+    T = sum(lens)
+    seq = np.concatenate([[0], np.cumsum(lens)])
+    q = g.standard_normal((T, H * D))
+    k = g.standard_normal((T, Hk * D))
+    v = g.standard_normal((T, Hk * D))
+    do = g.standard_normal((T, H * D))
+    out, lse2, (dq, dk, dv) = oracle.causal_attention(q, k, v, seq, H, Hk, dout=do)
+    tq, tk, tv = (torch.tensor(a, requires_grad=True) for a in (q, k, v))
+    seg = np.repeat(np.arange(len(lens)), lens)
+    allowed = torch.tensor((seg[:, None] == seg[None, :]) & (np.arange(T)[:, None] >= np.arange(T)[None, :]))
+    outs = []
+    for h in range(H):
+        hk = h // (H // Hk)
+        s = tq[:, h * D:(h + 1) * D] @ tk[:, hk * D:(hk + 1) * D].T * D ** -0.5
+        s = s.masked_fill(~allowed, float("-inf"))
+        outs.append(torch.softmax(s, dim=1) @ tv[:, hk * D:(hk + 1) * D])
+        if h == 0:
+            lse_h0 = torch.logsumexp(s, dim=1) / np.log(2.0)
+    o = torch.cat(outs, dim=1)
+    o.backward(torch.tensor(do))
+    assert np.allclose(out, o.detach().numpy(), atol=1e-12)
+    assert np.allclose(lse2[0], lse_h0.detach().numpy(), atol=1e-12)
+    for a, t in ((dq, tq), (dk, tk), (dv, tv)):
+        assert np.allclose(a, t.grad.numpy(), atol=1e-10)
