@@ -55,6 +55,10 @@ def parse_args(argv=None):
     ap.add_argument("--sync", choices=["grad", "fedavg"], default="grad",
                     help="cross-replica adapter sync for N > 1 (default: per-step gradient "
                          "allreduce; fedavg = parameter averaging every --round-steps steps)")
+    ap.add_argument("--attention", action="store_true",
+                    help="K9 causal attention between q|k|v and o inside the timed step (its "
+                         "output feeds o, its backward feeds q|k|v's dY); not part of the default "
+                         "LoRA-layer metric")
     ap.add_argument("--round-steps", type=int, default=0,
                     help="fedavg round length in steps (default: --steps, one round per run)")
     return ap.parse_args(argv)
@@ -270,7 +274,7 @@ def run_ours(args, cfg, workload):
     _lib.load()
     st_dev = torch.cuda.current_stream()
 
-    stack = ReplicaStack(cfg, dev, seed=args.seed)
+    stack = ReplicaStack(cfg, dev, seed=args.seed, attention=args.attention)
     stack.overlap = not args.no_overlap
     train, items = cfg.batch(args.seed)
     plan = stack.plan(train, items)
@@ -576,6 +580,9 @@ def workload_for(cfg, args) -> dict:
         "intermediate": cfg.model.intermediate,
         "projections": ",".join(s.name for s in cfg.projections) + " (all 7, q|k|v and gate|up fused)",
         "parallelism": f"replicas x{args.gpus}",
+        **({"attention": "K9 causal attention of every sequence (training sequences, prefill "
+                         "segments, 1-row decode sequences without cached context) between q|k|v "
+                         "and o, backward over the training sequences"} if args.attention else {}),
         "l2": "inputs larger than L2 (all frozen weights, ~2x the model in bf16 with W^T, stream "
               "through HBM every step)",
     }

@@ -216,27 +216,28 @@ int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_h
                           void* workspace, size_t ws_bytes, void* stream);
 
 /* ---- K9: causal self-attention of packed sequences, forward + backward ------------------------
- * Sequences are row ranges [seq_start[s], seq_start[s+1]) (device int32, n_seq + 1 entries) — the
- * training sequences and prefill segments of the mixed batch; row i attends to rows
- * [seq_start[s], i] of its sequence.  q [T, ldq] (head h at columns h*128), k / v [T, ldk/ldv]
- * (kv head h/G), typically column blocks of the fused q|k|v projection output.  max_seqlen >= the
- * longest sequence.  head_dim 128; GQA with n_heads a multiple of n_kv_heads.
- * fwd: out [T, ldo] bf16, lse [n_heads, T] fp32 = base-2 log-sum-exp of scale*log2(e)*scores
- *      (kept for the backward).
- * bwd: delta [n_heads, T] fp32 workspace; dq / dk / dv bf16 (dk/dv per kv head: the G query heads
+ * Sequences are row ranges of the mixed batch (training sequences, prefill segments, decode rows)
+ * given per row: row_start[t] / row_end[t] (device int32 [T]) = first / one-past-last row of row
+ * t's sequence (sequences contiguous and in row order); row t attends to rows [row_start[t], t].
+ * CTAs take 64 consecutive rows (packed: short sequences share a tile).  q [T, ldq] (head h at columns h*128), k / v [T, ldk/ldv]
+ * (kv head h/G), typically column blocks of the fused q|k|v projection output.  head_dim 128; GQA with n_heads a multiple of n_kv_heads.
+ * fwd: out [T, ldo] bf16, lse [n_heads, stat_ld] fp32 = base-2 log-sum-exp of
+ *      scale*log2(e)*scores (kept for the backward); stat_ld <= 0 means T.
+ * bwd: over the sequences given (e.g. the training rows [0, T) of a pass whose forward covered
+ *      more rows: stat_ld = the forward's row count); delta [n_heads, stat_ld] fp32 workspace; dq / dk / dv bf16 (dk/dv per kv head: the G query heads
  *      of a group summed in a fixed order).  Deterministic: no atomics (dK/dV and dQ in separate
  *      kernels, each output element owned by one CTA).  fp32 softmax and accumulation.
  * Replaces: nothing in the reference (it has no attention); SURVEY §8(f) row 1. */
 int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
                               void* out, int ldo, float* lse, int T, int n_heads, int n_kv_heads,
-                              int head_dim, const int32_t* seq_start, int n_seq, int max_seqlen,
-                              float scale, void* stream);
+                              int head_dim, const int32_t* row_start, const int32_t* row_end,
+                              float scale, int stat_ld, void* stream);
 int collm_flash_attention_bwd(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
                               const void* out, int ldo, const void* dout, int lddo, const float* lse,
                               float* delta, void* dq, int lddq, void* dk, int lddk, void* dv, int lddv,
                               int T, int n_heads, int n_kv_heads, int head_dim,
-                              const int32_t* seq_start, int n_seq, int max_seqlen, float scale,
-                              void* stream);
+                              const int32_t* row_start, const int32_t* row_end, float scale,
+                              int stat_ld, void* stream);
 
 /* ---- K7: softmax cross-entropy forward + backward over LM-head logits ------------------------
  * For each row t of logits [T, ld] (bf16, V used columns, V and ld multiples of 8):

@@ -54,10 +54,10 @@ SIGNATURES: dict[str, tuple] = {
     "collm_plan_shrink_items": (_I, [_IP, _I, _I, _I, _IP, _I, _IP, _IP]),
     "collm_lora_shrink_tc": (_I, [_P, _I, _I, _P, _LL, _I, _I, _P, _P, _I, _P, _IP, _I, _P, _P,
                                   _P, _I, _P, _P, _P, _P]),
-    "collm_flash_attention_fwd": (_I, [_P, _I, _P, _I, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _I,
-                                       _I, _F, _P]),
+    "collm_flash_attention_fwd": (_I, [_P, _I, _P, _I, _P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _P,
+                                       _F, _I, _P]),
     "collm_flash_attention_bwd": (_I, [_P, _I, _P, _I, _P, _I, _P, _I, _P, _I, _P, _P, _P, _I, _P,
-                                       _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _F, _P]),
+                                       _I, _P, _I, _I, _I, _I, _I, _P, _P, _F, _I, _P]),
     "collm_cross_entropy": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _F, _P]),
     "collm_attention_workspace_bytes": (_SZ, [_I, _I, _I, _I]),
     "collm_paged_attention": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _I, _P, _I, _P, _P, _I, _F,

@@ -581,12 +581,12 @@ int collm_lora_shrink_tc(const void* X, int ldx, int x_rows, const void* A, long
 // ------------------------------------------------------------------------------------ K9
 static int flash_setup(FlashParams& p, const void* q, int ldq, const void* k, int ldk, const void* v,
                        int ldv, int T, int n_heads, int n_kv_heads, int head_dim,
-                       const int32_t* seq_start, int n_seq, float scale) {
-  CHECK_ARG(q && k && v && seq_start, "null input");
+                       const int32_t* row_start, const int32_t* row_end, float scale) {
+  CHECK_ARG(q && k && v && row_start && row_end, "null input");
   CHECK_ARG(head_dim == kFaD, "head_dim=%d (this build: %d)", head_dim, kFaD);
   CHECK_ARG(n_heads >= 1 && n_kv_heads >= 1 && n_heads % n_kv_heads == 0,
             "n_heads=%d must be a multiple of n_kv_heads=%d", n_heads, n_kv_heads);
-  CHECK_ARG(T >= 1 && n_seq >= 1, "empty batch (T=%d, n_seq=%d)", T, n_seq);
+  CHECK_ARG(T >= 1, "empty batch (T=%d)", T);
   CHECK_ARG(ldq % 8 == 0 && ldk % 8 == 0 && ldv % 8 == 0 && aligned16(q) && aligned16(k) && aligned16(v),
             "q/k/v must be 16-byte aligned with x8 leading dimensions");
   CHECK_ARG(ldq >= n_heads * kFaD && ldk >= n_kv_heads * kFaD && ldv >= n_kv_heads * kFaD,
@@ -594,10 +594,12 @@ static int flash_setup(FlashParams& p, const void* q, int ldq, const void* k, in
   p = FlashParams{};
   p.q = (const bf16*)q; p.k = (const bf16*)k; p.v = (const bf16*)v;
   p.ldq = ldq; p.ldk = ldk; p.ldv = ldv;
-  p.seq_start = seq_start;
-  p.n_seq = n_seq; p.T = T; p.n_heads = n_heads; p.n_kv_heads = n_kv_heads;
+  p.row_start = row_start;
+  p.row_end = row_end;
+  p.T = T; p.n_heads = n_heads; p.n_kv_heads = n_kv_heads;
   p.scale = scale;
   p.scale_log2 = scale * 1.4426950408889634f;
+  p.stat_ld = T;
   return COLLM_OK;
 }
 
@@ -605,7 +607,7 @@ static int flash_launch(void (*kernel)(const FlashParams), int smem, dim3 grid, 
   static std::mutex mu;
   static bool done[kMaxDevices][4] = {};
   const int dev = cur_device();
-  const int slot = smem == 81920 ? 0 : smem == 99328 ? 1 : 2;
+  const int slot = smem == 81920 ? 0 : smem == 99840 ? 1 : 2;
   {
     std::lock_guard<std::mutex> lk(mu);
     if (!done[dev][slot]) {
@@ -620,15 +622,16 @@ static int flash_launch(void (*kernel)(const FlashParams), int smem, dim3 grid, 
 
 int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
                               void* out, int ldo, float* lse, int T, int n_heads, int n_kv_heads,
-                              int head_dim, const int32_t* seq_start, int n_seq, int max_seqlen,
-                              float scale, void* stream) {
+                              int head_dim, const int32_t* row_start, const int32_t* row_end,
+                              float scale, int stat_ld, void* stream) {
   FlashParams p;
-  int rc = flash_setup(p, q, ldq, k, ldk, v, ldv, T, n_heads, n_kv_heads, head_dim, seq_start, n_seq, scale);
+  int rc = flash_setup(p, q, ldq, k, ldk, v, ldv, T, n_heads, n_kv_heads, head_dim, row_start, row_end, scale);
   if (rc) return rc;
   CHECK_ARG(out && lse && ldo % 8 == 0 && ldo >= n_heads * kFaD && aligned16(out), "bad out/lse");
-  CHECK_ARG(max_seqlen >= 1, "max_seqlen=%d", max_seqlen);
   p.out = (bf16*)out; p.ldo = ldo; p.lse = lse;
-  return flash_launch(flash_fwd_kernel, 81920, dim3((max_seqlen + kFaBM - 1) / kFaBM, n_seq, n_heads), p,
+  if (stat_ld > 0) p.stat_ld = stat_ld;
+  CHECK_ARG(p.stat_ld >= T, "stat_ld=%d < T=%d", p.stat_ld, T);
+  return flash_launch(flash_fwd_kernel, 81920, dim3((T + kFaBM - 1) / kFaBM, n_heads), p,
                       (cudaStream_t)stream);
 }
 
@@ -636,28 +639,29 @@ int collm_flash_attention_bwd(const void* q, int ldq, const void* k, int ldk, co
                               const void* out, int ldo, const void* dout, int lddo, const float* lse,
                               float* delta, void* dq, int lddq, void* dk, int lddk, void* dv, int lddv,
                               int T, int n_heads, int n_kv_heads, int head_dim,
-                              const int32_t* seq_start, int n_seq, int max_seqlen, float scale,
-                              void* stream) {
+                              const int32_t* row_start, const int32_t* row_end, float scale,
+                              int stat_ld, void* stream) {
   FlashParams p;
-  int rc = flash_setup(p, q, ldq, k, ldk, v, ldv, T, n_heads, n_kv_heads, head_dim, seq_start, n_seq, scale);
+  int rc = flash_setup(p, q, ldq, k, ldk, v, ldv, T, n_heads, n_kv_heads, head_dim, row_start, row_end, scale);
   if (rc) return rc;
   CHECK_ARG(out && dout && lse && delta && dq && dk && dv, "null backward operand");
   CHECK_ARG(ldo % 8 == 0 && lddo % 8 == 0 && lddq % 2 == 0 && lddk % 2 == 0 && lddv % 2 == 0 &&
                 aligned16(dout) && aligned16(out),
             "bad backward leading dimensions / alignment");
-  CHECK_ARG(max_seqlen >= 1, "max_seqlen=%d", max_seqlen);
   p.out = (bf16*)out; p.ldo = ldo; p.lse = const_cast<float*>(lse);
   p.dout = (const bf16*)dout; p.lddo = lddo; p.delta = delta;
   p.dq = (bf16*)dq; p.dk = (bf16*)dk; p.dv = (bf16*)dv;
   p.lddq = lddq; p.lddk = lddk; p.lddv = lddv;
+  if (stat_ld > 0) p.stat_ld = stat_ld;
+  CHECK_ARG(p.stat_ld >= T, "stat_ld=%d < T=%d", p.stat_ld, T);
   cudaStream_t st = (cudaStream_t)stream;
   const int warps = T * n_heads;
   flash_delta_kernel<<<(warps + 7) / 8, 256, 0, st>>>(p);
   CUDA_TRY(cudaGetLastError());
-  const int tiles = (max_seqlen + kFaBM - 1) / kFaBM;
-  rc = flash_launch(flash_bwd_dkdv_kernel, 99328, dim3(tiles, n_seq, n_kv_heads), p, st);
+  const int tiles = (T + kFaBM - 1) / kFaBM;
+  rc = flash_launch(flash_bwd_dkdv_kernel, 99840, dim3(tiles, n_kv_heads), p, st);
   if (rc) return rc;
-  return flash_launch(flash_bwd_dq_kernel, 98304, dim3(tiles, n_seq, n_heads), p, st);
+  return flash_launch(flash_bwd_dq_kernel, 98304, dim3(tiles, n_heads), p, st);
 }
 
 // ------------------------------------------------------------------------------------ K2/K3

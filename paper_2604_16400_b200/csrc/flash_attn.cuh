@@ -4,19 +4,27 @@
 //
 //   out[i, h] = sum_{j in seq(i), j <= i} softmax_j(scale * q[i,h] . k[j,h/G]) v[j,h/G]
 //
-// Sequences are row ranges [seq_start[s], seq_start[s+1]) of the mixed batch (a training sequence
-// or a prefill segment); q / k / v are column blocks of the fused q|k|v projection output (any
-// row stride), GQA with G = n_heads / n_kv_heads, head_dim 128.  Decode rows attend to the paged
-// KV cache instead (K8, attn.cuh).
+// Sequences are row ranges of the mixed batch (a training sequence, a prefill segment, a decode
+// row), given per row as row_start[t] / row_end[t]; q / k / v are column blocks of the fused q|k|v
+// projection output (any row stride), GQA with G = n_heads / n_kv_heads, head_dim 128.  Decode
+// rows' cached context is the paged KV cache's (K8, attn.cuh).
+//
+// Packed tiling: CTAs take 64 CONSECUTIVE ROWS of the batch, not of a sequence, so a tile of
+// short prefill / decode sequences costs one CTA (keys: from the first row's sequence start to
+// the tile's last row, masked by same-sequence-and-causal) — grid = T/64 x heads whatever the
+// sequence mix (7B step: 293 sequences in 1024 rows -> 16 tiles per head).
 //
 // Tensor-core flash attention (mma.sync m16n8k16 bf16 -> fp32, ldmatrix from XOR-swizzled shared
-// memory, cp.async double buffers).  Why not tcgen05 here: per step the attention is < 1 % of the
-// projection FLOPs at every BASELINE shape (7B: 2 x 512 x 512/2 x 128 x 32 heads x 2 = 4.3
-// GFLOP fwd vs 19.9 TFLOP), so its kernels are latency/occupancy-bound, not tensor-bound.
-//   forward : CTA = (64 query rows, head); online base-2 softmax; writes out and the base-2
+// memory, cp.async double buffers) — the legacy warp-level MMA path, not tcgen05: attention is
+// 0.3 % of the 7B step's FLOPs (2.1 GFLOP fwd per layer vs 620 GFLOP of projections) and 5.7 % at
+// 13B (8 x 2048-token training sequences); measured (tools/flash_bench.py) 64-69 TFLOP/s at the
+// 7B shape, 126-157 at 8B, 157-211 at 13B — a tcgen05/TMEM version is the next step for the
+// long-sequence configs.
+//   forward : CTA = (64 rows, head); online base-2 softmax; writes out and the base-2
 //             log-sum-exp of the scaled scores (lse [n_heads, T]) for the backward.
 //   backward: delta = rowsum(dout * out); dK/dV: CTA = (64 keys, kv head) looping over the G query
-//             heads of its group and the query tiles at or after it (recomputing P from lse);
+//             heads of its group and the query tiles from its first key to the end of its last
+//             key's sequence (recomputing P from lse);
 //             dQ: CTA = (64 queries, head) looping over the key tiles up to the diagonal.  Every
 //             output element is owned by one CTA and accumulated in a fixed order: bitwise
 //             deterministic (no atomics).
@@ -33,13 +41,15 @@ struct FlashParams {
   const bf16* q; const bf16* k; const bf16* v;
   int ldq, ldk, ldv;
   bf16* out; int ldo;
-  float* lse;            // [n_heads, T] base-2 log-sum-exp of scale*log2(e)*scores
+  float* lse;            // [n_heads, stat_ld] base-2 log-sum-exp of scale*log2(e)*scores
   const bf16* dout; int lddo;
-  float* delta;          // [n_heads, T]
+  float* delta;          // [n_heads, stat_ld]
   bf16* dq; bf16* dk; bf16* dv;
   int lddq, lddk, lddv;
-  const int32_t* seq_start;
-  int n_seq, T, n_heads, n_kv_heads;
+  const int32_t* row_start;  // [T] first row of each row's sequence
+  const int32_t* row_end;    // [T] one past the last row of each row's sequence
+  int T, n_heads, n_kv_heads;
+  int stat_ld;           // row stride of lse / delta per head (>= the rows indexed)
   float scale_log2;      // scale * log2(e)
   float scale;
 };
@@ -106,35 +116,41 @@ __device__ __forceinline__ void fa_c2a(uint32_t (&a)[4], const float (&c0)[4], c
 // ----------------------------------------------------------------------------------- forward
 __global__ void __launch_bounds__(kFaThreads) flash_fwd_kernel(const FlashParams p) {
   extern __shared__ __align__(128) uint8_t fsm[];
-  const int s = blockIdx.y, h = blockIdx.z;
-  const int s0 = p.seq_start[s], L = p.seq_start[s + 1] - s0;
+  // packed tiling: a CTA takes 64 consecutive rows of the batch whatever their sequences; its
+  // keys run from the first row's sequence start to its last row, masked per (query, key) by
+  // "same sequence and not after the query" — short prefill / decode sequences share a tile
+  const int h = blockIdx.y;
   const int q0 = blockIdx.x * kFaBM;
-  if (q0 >= L) return;
+  if (q0 >= p.T) return;
   const int hk = h / (p.n_heads / p.n_kv_heads);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   uint8_t* Qs = fsm;
   uint8_t* Ks = fsm + 16384;   // [2] stages
   uint8_t* Vs = fsm + 49152;   // [2] stages
   const uint32_t qb = smem_u32(Qs), kb0 = smem_u32(Ks), vb0 = smem_u32(Vs);
-  const int nq = min(kFaBM, L - q0);
-  const int n_kt = (min(q0 + kFaBM, L) + kFaBM - 1) / kFaBM;  // key tiles up to the diagonal
+  const int nq = min(kFaBM, p.T - q0);
+  const int kstart = p.row_start[q0], kend = q0 + nq;
+  const int n_kt = (kend - kstart + kFaBM - 1) / kFaBM;
 
-  fa_load_tile(Qs, p.q, p.ldq, s0 + q0, nq, h * kFaD);
-  fa_load_tile(Ks, p.k, p.ldk, s0, min(kFaBM, L), hk * kFaD);
-  fa_load_tile(Vs, p.v, p.ldv, s0, min(kFaBM, L), hk * kFaD);
+  fa_load_tile(Qs, p.q, p.ldq, q0, nq, h * kFaD);
+  fa_load_tile(Ks, p.k, p.ldk, kstart, min(kFaBM, kend - kstart), hk * kFaD);
+  fa_load_tile(Vs, p.v, p.ldv, kstart, min(kFaBM, kend - kstart), hk * kFaD);
   cp_async_commit();
+  const int qrow0 = q0 + warp * 16 + g;  // this thread's rows qrow0, qrow0 + 8 (batch rows)
+  int qs[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) qs[r] = qrow0 + r * 8 < p.T ? p.row_start[qrow0 + r * 8] : 0x7fffffff;
 
   float o[16][4];
 #pragma unroll
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m_i[2] = {-INFINITY, -INFINITY}, l_i[2] = {0.f, 0.f};
-  const int qrow0 = q0 + warp * 16 + g;  // this thread's rows qrow0, qrow0 + 8 (sequence-local)
 
   for (int j = 0; j < n_kt; ++j) {
     if (j + 1 < n_kt) {
-      const int kr = (j + 1) * kFaBM;
-      fa_load_tile(Ks + ((j + 1) & 1) * 16384, p.k, p.ldk, s0 + kr, min(kFaBM, L - kr), hk * kFaD);
-      fa_load_tile(Vs + ((j + 1) & 1) * 16384, p.v, p.ldv, s0 + kr, min(kFaBM, L - kr), hk * kFaD);
+      const int kr = kstart + (j + 1) * kFaBM;
+      fa_load_tile(Ks + ((j + 1) & 1) * 16384, p.k, p.ldk, kr, min(kFaBM, kend - kr), hk * kFaD);
+      fa_load_tile(Vs + ((j + 1) & 1) * 16384, p.v, p.ldv, kr, min(kFaBM, kend - kr), hk * kFaD);
     }
     cp_async_commit();
     cp_async_wait<1>();
@@ -161,9 +177,9 @@ __global__ void __launch_bounds__(kFaThreads) flash_fwd_kernel(const FlashParams
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int key = j * kFaBM + nt * 8 + 2 * c + (e & 1);
+        const int key = kstart + j * kFaBM + nt * 8 + 2 * c + (e & 1);
         const int qr = qrow0 + (e >> 1) * 8;
-        const bool ok = key <= qr && key < L;
+        const bool ok = key <= qr && key >= qs[e >> 1];
         sc[nt][e] = ok ? sc[nt][e] * p.scale_log2 : -INFINITY;
         mx[e >> 1] = fmaxf(mx[e >> 1], sc[nt][e]);
       }
@@ -215,14 +231,14 @@ __global__ void __launch_bounds__(kFaThreads) flash_fwd_kernel(const FlashParams
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int qr = qrow0 + r * 8;
-    if (qr >= L) continue;
+    if (qr >= p.T) continue;
     const float inv = 1.f / l_i[r];
-    bf16* dst = p.out + (size_t)(s0 + qr) * p.ldo + h * kFaD;
+    bf16* dst = p.out + (size_t)qr * p.ldo + h * kFaD;
 #pragma unroll
     for (int dt = 0; dt < 16; ++dt)
       *reinterpret_cast<uint32_t*>(dst + dt * 8 + 2 * c) =
           pack_bf16x2(o[dt][2 * r] * inv, o[dt][2 * r + 1] * inv);
-    if (c == 0) p.lse[(size_t)h * p.T + s0 + qr] = m_i[r] + log2f(l_i[r]);
+    if (c == 0) p.lse[(size_t)h * p.stat_ld + qr] = m_i[r] + log2f(l_i[r]);
   }
 }
 
@@ -241,7 +257,7 @@ __global__ void flash_delta_kernel(const FlashParams p) {
   float v = a0.x * b0.x + a0.y * b0.y + a1.x * b1.x + a1.y * b1.y;
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) p.delta[(size_t)h * p.T + i] = v;
+  if (lane == 0) p.delta[(size_t)h * p.stat_ld + i] = v;
 }
 
 // dK, dV of 64 keys of one kv head: for every query head of the group and every query tile at or
@@ -249,10 +265,9 @@ __global__ void flash_delta_kernel(const FlashParams p) {
 // dS^T = P^T (dP^T - delta); dV += P^T dO, dK += dS^T Q (warp w owns keys 16w..16w+15).
 __global__ void __launch_bounds__(kFaThreads) flash_bwd_dkdv_kernel(const FlashParams p) {
   extern __shared__ __align__(128) uint8_t fsm[];
-  const int s = blockIdx.y, hk = blockIdx.z;
-  const int s0 = p.seq_start[s], L = p.seq_start[s + 1] - s0;
+  const int hk = blockIdx.y;
   const int k0 = blockIdx.x * kFaBM;
-  if (k0 >= L) return;
+  if (k0 >= p.T) return;
   const int G = p.n_heads / p.n_kv_heads;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   uint8_t* Ks = fsm;
@@ -261,23 +276,25 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dkdv_kernel(const FlashP
   uint8_t* Os = fsm + 65536;    // [2] dO
   float* lse_s = reinterpret_cast<float*>(fsm + 98304);    // [2][64]
   float* dl_s = lse_s + 2 * kFaBM;                          // [2][64]
+  int* qs_s = reinterpret_cast<int*>(dl_s + 2 * kFaBM);     // [2][64] queries' sequence starts
   const uint32_t kb = smem_u32(Ks), vb = smem_u32(Vs), qb0 = smem_u32(Qs), ob0 = smem_u32(Os);
-  const int nk = min(kFaBM, L - k0);
-  fa_load_tile(Ks, p.k, p.ldk, s0 + k0, nk, hk * kFaD);
-  fa_load_tile(Vs, p.v, p.ldv, s0 + k0, nk, hk * kFaD);
+  const int nk = min(kFaBM, p.T - k0);
+  fa_load_tile(Ks, p.k, p.ldk, k0, nk, hk * kFaD);
+  fa_load_tile(Vs, p.v, p.ldv, k0, nk, hk * kFaD);
 
-  const int n_qt = (L + kFaBM - 1) / kFaBM;
-  const int qt0 = k0 / kFaBM;  // causal: query tiles at or after the key tile
-  const int per_head = n_qt - qt0, total = G * per_head;
+  // queries that see these keys: rows [k0, row_end of the last key) (row_end is non-decreasing)
+  const int qend = p.row_end[k0 + nk - 1];
+  const int per_head = (qend - k0 + kFaBM - 1) / kFaBM, total = G * per_head;
   auto issue = [&](int it, int buf) {
-    const int hq = hk * G + it / per_head, qt = qt0 + it % per_head;
-    const int qr = qt * kFaBM, nq = min(kFaBM, L - qr);
-    fa_load_tile(Qs + buf * 16384, p.q, p.ldq, s0 + qr, nq, hq * kFaD);
-    fa_load_tile(Os + buf * 16384, p.dout, p.lddo, s0 + qr, nq, hq * kFaD);
+    const int hq = hk * G + it / per_head;
+    const int qr = k0 + (it % per_head) * kFaBM, nq = min(kFaBM, qend - qr);
+    fa_load_tile(Qs + buf * 16384, p.q, p.ldq, qr, nq, hq * kFaD);
+    fa_load_tile(Os + buf * 16384, p.dout, p.lddo, qr, nq, hq * kFaD);
     for (int i = threadIdx.x; i < kFaBM; i += kFaThreads) {
       const bool ok = i < nq;
-      lse_s[buf * kFaBM + i] = ok ? p.lse[(size_t)hq * p.T + s0 + qr + i] : 0.f;
-      dl_s[buf * kFaBM + i] = ok ? p.delta[(size_t)hq * p.T + s0 + qr + i] : 0.f;
+      lse_s[buf * kFaBM + i] = ok ? p.lse[(size_t)hq * p.stat_ld + qr + i] : 0.f;
+      dl_s[buf * kFaBM + i] = ok ? p.delta[(size_t)hq * p.stat_ld + qr + i] : 0.f;
+      qs_s[buf * kFaBM + i] = ok ? p.row_start[qr + i] : 0x7fffffff;
     }
   };
   issue(0, 0);
@@ -295,10 +312,11 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dkdv_kernel(const FlashP
     cp_async_wait<1>();
     __syncthreads();
     const int buf = it & 1;
-    const int qr = (qt0 + it % per_head) * kFaBM;
+    const int qr = k0 + (it % per_head) * kFaBM;
     const uint32_t qb = qb0 + buf * 16384, ob = ob0 + buf * 16384;
     const float* lse_b = lse_s + buf * kFaBM;
     const float* dl_b = dl_s + buf * kFaBM;
+    const int* qs_b = qs_s + buf * kFaBM;
     // S^T = K_w Q^T and dP^T = V_w dO^T  (16 keys x 64 queries each)
     float st[8][4], dpt[8][4];
 #pragma unroll
@@ -328,7 +346,7 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dkdv_kernel(const FlashP
         const int ql = nt * 8 + 2 * c + (e & 1);  // query within the tile
         const int key = key_r0 + (e >> 1) * 8;
         const int q = qr + ql;
-        const bool ok = key <= q && q < L && key < L;
+        const bool ok = key <= q && q < qend && qs_b[ql] <= key;
         const float pv = ok ? exp2f(st[nt][e] * p.scale_log2 - lse_b[ql]) : 0.f;
         st[nt][e] = pv;
         dpt[nt][e] = pv * (dpt[nt][e] - dl_b[ql]);
@@ -356,9 +374,9 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dkdv_kernel(const FlashP
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int key = key_r0 + r * 8;
-    if (key >= L) continue;
-    bf16* dkd = p.dk + (size_t)(s0 + key) * p.lddk + hk * kFaD;
-    bf16* dvd = p.dv + (size_t)(s0 + key) * p.lddv + hk * kFaD;
+    if (key >= p.T) continue;
+    bf16* dkd = p.dk + (size_t)key * p.lddk + hk * kFaD;
+    bf16* dvd = p.dv + (size_t)key * p.lddv + hk * kFaD;
 #pragma unroll
     for (int dt = 0; dt < 16; ++dt) {
       *reinterpret_cast<uint32_t*>(dkd + dt * 8 + 2 * c) =
@@ -372,10 +390,9 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dkdv_kernel(const FlashP
 // Q K^T - lse), dP = dO V^T, dS = P (dP - delta), dQ += dS K (warp w owns queries 16w..16w+15).
 __global__ void __launch_bounds__(kFaThreads) flash_bwd_dq_kernel(const FlashParams p) {
   extern __shared__ __align__(128) uint8_t fsm[];
-  const int s = blockIdx.y, h = blockIdx.z;
-  const int s0 = p.seq_start[s], L = p.seq_start[s + 1] - s0;
+  const int h = blockIdx.y;
   const int q0 = blockIdx.x * kFaBM;
-  if (q0 >= L) return;
+  if (q0 >= p.T) return;
   const int hk = h / (p.n_heads / p.n_kv_heads);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   uint8_t* Qs = fsm;
@@ -383,20 +400,24 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dq_kernel(const FlashPar
   uint8_t* Ks = fsm + 32768;  // [2]
   uint8_t* Vs = fsm + 65536;  // [2]
   const uint32_t qb = smem_u32(Qs), ob = smem_u32(Os), kb0 = smem_u32(Ks), vb0 = smem_u32(Vs);
-  const int nq = min(kFaBM, L - q0);
-  const int n_kt = (min(q0 + kFaBM, L) + kFaBM - 1) / kFaBM;
-  fa_load_tile(Qs, p.q, p.ldq, s0 + q0, nq, h * kFaD);
-  fa_load_tile(Os, p.dout, p.lddo, s0 + q0, nq, h * kFaD);
-  fa_load_tile(Ks, p.k, p.ldk, s0, min(kFaBM, L), hk * kFaD);
-  fa_load_tile(Vs, p.v, p.ldv, s0, min(kFaBM, L), hk * kFaD);
+  const int nq = min(kFaBM, p.T - q0);
+  const int kstart = p.row_start[q0], kend = q0 + nq;
+  const int n_kt = (kend - kstart + kFaBM - 1) / kFaBM;
+  fa_load_tile(Qs, p.q, p.ldq, q0, nq, h * kFaD);
+  fa_load_tile(Os, p.dout, p.lddo, q0, nq, h * kFaD);
+  fa_load_tile(Ks, p.k, p.ldk, kstart, min(kFaBM, kend - kstart), hk * kFaD);
+  fa_load_tile(Vs, p.v, p.ldv, kstart, min(kFaBM, kend - kstart), hk * kFaD);
   cp_async_commit();
   const int qrow0 = q0 + warp * 16 + g;
   float lse_r[2], dl_r[2];
+  int qs[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int qr = qrow0 + r * 8;
-    lse_r[r] = qr < L ? p.lse[(size_t)h * p.T + s0 + qr] : 0.f;
-    dl_r[r] = qr < L ? p.delta[(size_t)h * p.T + s0 + qr] : 0.f;
+    const bool ok = qr < p.T;
+    lse_r[r] = ok ? p.lse[(size_t)h * p.stat_ld + qr] : 0.f;
+    dl_r[r] = ok ? p.delta[(size_t)h * p.stat_ld + qr] : 0.f;
+    qs[r] = ok ? p.row_start[qr] : 0x7fffffff;
   }
   float dq[16][4];
 #pragma unroll
@@ -404,9 +425,9 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dq_kernel(const FlashPar
 
   for (int j = 0; j < n_kt; ++j) {
     if (j + 1 < n_kt) {
-      const int kr = (j + 1) * kFaBM;
-      fa_load_tile(Ks + ((j + 1) & 1) * 16384, p.k, p.ldk, s0 + kr, min(kFaBM, L - kr), hk * kFaD);
-      fa_load_tile(Vs + ((j + 1) & 1) * 16384, p.v, p.ldv, s0 + kr, min(kFaBM, L - kr), hk * kFaD);
+      const int kr = kstart + (j + 1) * kFaBM;
+      fa_load_tile(Ks + ((j + 1) & 1) * 16384, p.k, p.ldk, kr, min(kFaBM, kend - kr), hk * kFaD);
+      fa_load_tile(Vs + ((j + 1) & 1) * 16384, p.v, p.ldv, kr, min(kFaBM, kend - kr), hk * kFaD);
     }
     cp_async_commit();
     cp_async_wait<1>();
@@ -436,9 +457,9 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dq_kernel(const FlashPar
     for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int key = j * kFaBM + nt * 8 + 2 * c + (e & 1);
+        const int key = kstart + j * kFaBM + nt * 8 + 2 * c + (e & 1);
         const int qr = qrow0 + (e >> 1) * 8;
-        const bool ok = key <= qr && key < L && qr < L;
+        const bool ok = key <= qr && key >= qs[e >> 1] && qr < p.T;
         const float pv = ok ? exp2f(sc[nt][e] * p.scale_log2 - lse_r[e >> 1]) : 0.f;
         dp[nt][e] = pv * (dp[nt][e] - dl_r[e >> 1]);
       }
@@ -460,8 +481,8 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dq_kernel(const FlashPar
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int qr = qrow0 + r * 8;
-    if (qr >= L) continue;
-    bf16* dst = p.dq + (size_t)(s0 + qr) * p.lddq + h * kFaD;
+    if (qr >= p.T) continue;
+    bf16* dst = p.dq + (size_t)qr * p.lddq + h * kFaD;
 #pragma unroll
     for (int dt = 0; dt < 16; ++dt)
       *reinterpret_cast<uint32_t*>(dst + dt * 8 + 2 * c) =

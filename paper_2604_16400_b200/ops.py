@@ -339,31 +339,45 @@ def paged_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tenso
               _p(ws), 0 if ws is None else ws.numel(), _stream())
 
 
+def seq_rows(bounds, device) -> tuple[torch.Tensor, torch.Tensor]:
+    """Per-row sequence bounds for K9 from sequence boundaries [0, b1, ..., T]: (row_start,
+    row_end) int32 [T] on ``device``."""
+    import numpy as np
+    b = np.asarray(bounds, np.int64)
+    lens = np.diff(b)
+    rs = np.repeat(b[:-1], lens).astype(np.int32)
+    re = np.repeat(b[1:], lens).astype(np.int32)
+    return torch.from_numpy(rs).to(device), torch.from_numpy(re).to(device)
+
+
 def flash_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor,
-                    lse: torch.Tensor, seq_start: torch.Tensor, *, T: int, n_heads: int,
-                    n_kv_heads: int, max_seqlen: int, scale: float | None = None) -> None:
+                    lse: torch.Tensor, row_start: torch.Tensor, row_end: torch.Tensor, *, T: int,
+                    n_heads: int, n_kv_heads: int, scale: float | None = None,
+                    stat_ld: int = 0) -> None:
     """K9 forward: causal attention of the packed sequences (see collm.h).  q / k / v / out may be
-    column views of the fused q|k|v output (row stride = its width); lse fp32 [n_heads, T]."""
+    column views of the fused q|k|v output (row stride = its width); lse fp32 [n_heads, stat_ld];
+    row_start / row_end from :func:`seq_rows`."""
     for t, n in ((q, "q"), (k, "k"), (v, "v"), (out, "out")):
         _need(t, torch.bfloat16, n)
     _need(lse, torch.float32, "lse")
-    _need(seq_start, torch.int32, "seq_start")
+    _need(row_start, torch.int32, "row_start")
+    _need(row_end, torch.int32, "row_end")
     if not _launch("attention"):
         return
     D = 128
     _lib.call("collm_flash_attention_fwd", q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0),
               v.data_ptr(), v.stride(0), out.data_ptr(), out.stride(0), lse.data_ptr(), T,
-              n_heads, n_kv_heads, D, seq_start.data_ptr(), seq_start.shape[0] - 1, max_seqlen,
-              float(scale if scale is not None else D ** -0.5), _stream())
+              n_heads, n_kv_heads, D, row_start.data_ptr(), row_end.data_ptr(),
+              float(scale if scale is not None else D ** -0.5), stat_ld or lse.stride(0), _stream())
 
 
 def flash_attention_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor,
                         dout: torch.Tensor, lse: torch.Tensor, delta: torch.Tensor,
                         dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor,
-                        seq_start: torch.Tensor, *, T: int, n_heads: int, n_kv_heads: int,
-                        max_seqlen: int, scale: float | None = None) -> None:
-    """K9 backward: dq / dk / dv of :func:`flash_attention` (deterministic; delta fp32
-    [n_heads, T] workspace)."""
+                        row_start: torch.Tensor, row_end: torch.Tensor, *, T: int, n_heads: int,
+                        n_kv_heads: int, scale: float | None = None, stat_ld: int = 0) -> None:
+    """K9 backward: dq / dk / dv of :func:`flash_attention` over rows [0, T) (deterministic;
+    delta fp32 [n_heads, stat_ld] workspace)."""
     for t, n in ((q, "q"), (k, "k"), (v, "v"), (out, "out"), (dout, "dout"), (dq, "dq"),
                  (dk, "dk"), (dv, "dv")):
         _need(t, torch.bfloat16, n)
@@ -376,5 +390,5 @@ def flash_attention_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: 
               v.data_ptr(), v.stride(0), out.data_ptr(), out.stride(0), dout.data_ptr(),
               dout.stride(0), lse.data_ptr(), delta.data_ptr(), dq.data_ptr(), dq.stride(0),
               dk.data_ptr(), dk.stride(0), dv.data_ptr(), dv.stride(0), T, n_heads, n_kv_heads, D,
-              seq_start.data_ptr(), seq_start.shape[0] - 1, max_seqlen,
-              float(scale if scale is not None else D ** -0.5), _stream())
+              row_start.data_ptr(), row_end.data_ptr(),
+              float(scale if scale is not None else D ** -0.5), stat_ld or lse.stride(0), _stream())

@@ -54,6 +54,11 @@ class StepPlan:
     device: DevicePlan
     train_host: HostPlan | None
     train_device: DevicePlan | None
+    # K9 attention (ReplicaStack(attention=True)): sequences of the pass as row ranges — the
+    # training sequences (train.batch x train.seq_len) then each inference request's rows — and
+    # the training sequences alone (the backward); device int32 + the longest length
+    attn_seq: list | None = None           # sequence boundaries [0, ..., T] (host)
+    attn_rows: tuple | None = None         # (row_start, row_end) int32 [T] on the device
 
     @property
     def n_rows(self) -> int:
@@ -67,8 +72,16 @@ class StepPlan:
 class ReplicaStack:
     def __init__(self, cfg: LayerConfig, device: torch.device | str = "cuda", seed: int = 0,
                  optimizer: AdamWConfig | None = None, init: bool = True, lm_head: bool = False,
-                 trainer: bool = True):
+                 trainer: bool = True, attention: bool = False):
         self.cfg = cfg
+        # attention: K9 causal attention between q|k|v and o (its output IS o's input; its
+        # backward turns o's dX into q|k|v's dY) over the pass's sequences
+        self.attention = attention
+        if attention:
+            if cfg.projections[0].name != "qkv" or cfg.model.hidden % 128 or cfg.model.kv_dim % 128:
+                raise ConfigurationError("attention needs a fused q|k|v projection and 128-wide heads")
+            self.n_heads = cfg.model.hidden // 128
+            self.n_kv_heads = cfg.model.kv_dim // 128
         self.device = torch.device(device)
         self.specs = cfg.projections
         L = cfg.model.layers
@@ -271,7 +284,23 @@ class ReplicaStack:
                     f"{self.train_slot}")
             th = uniform_plan(mb.n_train_rows, mb.train_adapter)
             td = DevicePlan(th, self.device)
-        return StepPlan(mb, hp, dp, th, td)
+        sp = StepPlan(mb, hp, dp, th, td)
+        if self.attention:
+            # sequences: training sequences of seq_len rows, then maximal runs of one request
+            bounds = []
+            if train is not None:
+                bounds = list(range(0, mb.n_train_rows + 1, train.seq_len))
+            else:
+                bounds = [0]
+            req = mb.row_request
+            for t in range(mb.n_train_rows + 1, mb.n_rows):
+                if req[t] != req[t - 1]:
+                    bounds.append(t)
+            if mb.n_rows > bounds[-1]:
+                bounds.append(mb.n_rows)
+            sp.attn_seq = bounds
+            sp.attn_rows = ops.seq_rows(bounds, self.device)
+        return sp
 
     # ------------------------------------------------------------------ activations
     def allocate(self, plan: StepPlan, distinct_synthetic: bool | None = None, seed: int = 1,
@@ -300,6 +329,8 @@ class ReplicaStack:
         dev = self.device
         bf = torch.bfloat16
         per_layer_bytes = 2 * (T * h + T * i + Ttr * sum(s.out_features for s in self.specs))
+        if self.attention:  # per-layer q|k|v outputs and their gradients (the attention backward)
+            per_layer_bytes += 2 * (T + Ttr) * self.specs[0].out_features
         if distinct_synthetic is None:
             free, _ = torch.cuda.mem_get_info(dev)
             distinct_synthetic = per_layer_bytes * L < 0.5 * free
@@ -326,6 +357,14 @@ class ReplicaStack:
                    for s in self.specs} if Ttr else {},
         }
         acts["X"][0].copy_(rnd(T, h))
+        if self.attention:
+            nq = self.specs[0].out_features
+            # attention outputs (o's inputs) per layer, written by K9 every pass
+            acts["Xo"] = [torch.empty(T, h, dtype=bf, device=dev) for _ in range(L)]
+            acts["Yqkv"] = [torch.empty(T, nq, dtype=bf, device=dev) for _ in range(L)]
+            acts["lse"] = torch.zeros(L, self.n_heads, T, dtype=torch.float32, device=dev)
+            acts["dqkv"] = [torch.empty(Ttr, nq, dtype=bf, device=dev) for _ in range(L)] if Ttr else []
+            acts["delta"] = torch.zeros(self.n_heads, max(1, T), dtype=torch.float32, device=dev)
         if self.head is not None and Ttr:
             # next-token targets of the training rows (synthetic token ids; no dataset offline)
             acts["labels"] = torch.randint(0, self.cfg.model.vocab, (Ttr,), device=dev,
@@ -424,19 +463,28 @@ class ReplicaStack:
             syn = l if a["distinct_synthetic"] else 0
             for proj in layer:
                 name = proj.spec.name
-                X = a["X"][l] if name in ENTRY else (a["Xo"][syn] if name == "o" else a["Xd"][syn])
+                if self.attention and name == "o":
+                    X = a["Xo"][l]
+                else:
+                    X = a["X"][l] if name in ENTRY else (a["Xo"][syn] if name == "o" else a["Xd"][syn])
                 Y = a["X"][l + 1] if name == "down" else a["Y"][name]
+                if self.attention and name == "qkv":
+                    Y = a["Yqkv"][l]
                 sig = signal()
                 if pdl:
                     cache = proj.forward_lora(X, plan.device, n_train=Ttr)
                     proj.forward_gemm(cache, plan.device, Y, pdl=True)
                     caches[l][name] = cache
+                    if self.attention and name == "qkv":
+                        self._attention_fwd(l, plan)
                     continue
                 box = {}
                 on_side(lambda: box.setdefault("c", proj.forward_lora(X, plan.device, n_train=Ttr,
                                                                     signal=sig)), prev)
                 caches[l][name] = box["c"]
                 proj.forward_gemm(box["c"], plan.device, Y, wait=sig)
+                if self.attention and name == "qkv":
+                    self._attention_fwd(l, plan)
                 prev = after(main)
         if Ttr and backward and self.head is not None:
             # K2 logits -> K7 softmax-CE fwd+bwd -> K3 dX: the real dY entering the top layer
@@ -469,6 +517,11 @@ class ReplicaStack:
                     name = proj.spec.name
                     dY = (a["dY_top"] if l == L - 1 else a["dX_first"][l + 1]) if name == "down" \
                         else a["dY"][syn][name]
+                    if self.attention and name == "qkv":
+                        # K9 backward: o's dX (the gradient of the attention output) -> q|k|v's dY
+                        self._attention_bwd(l, plan)
+                        dY = a["dqkv"][l]
+                        prev = after(main)  # the side-stream dH shrink reads this dY
                     dX = a["dX_first"][l] if name == first else a["dX"][name]
                     cache = caches[l][name]
                     sig = signal()
@@ -489,6 +542,31 @@ class ReplicaStack:
         if overlap:
             main.wait_stream(side)
         return a["X"][L]
+
+    def _qkv_views(self, t: torch.Tensor):
+        H, Hk, D = self.n_heads, self.n_kv_heads, 128
+        return t[:, :H * D], t[:, H * D:(H + Hk) * D], t[:, (H + Hk) * D:]
+
+    def _attention_fwd(self, l: int, plan: StepPlan) -> None:
+        """K9 forward of layer l over every sequence of the pass: q|k|v output -> o's input."""
+        a = self._acts
+        T = plan.n_rows
+        q, k, v = self._qkv_views(a["Yqkv"][l][:T])
+        ops.flash_attention(q, k, v, a["Xo"][l][:T], a["lse"][l], *plan.attn_rows, T=T,
+                            n_heads=self.n_heads, n_kv_heads=self.n_kv_heads,
+                            stat_ld=a["lse"].shape[-1])
+
+    def _attention_bwd(self, l: int, plan: StepPlan) -> None:
+        """K9 backward of layer l over the training sequences: o's dX -> q|k|v's dY."""
+        a = self._acts
+        Ttr = plan.n_train
+        q, k, v = self._qkv_views(a["Yqkv"][l][:Ttr])
+        dq, dk, dv = self._qkv_views(a["dqkv"][l][:Ttr])
+        # the training sequences are rows [0, Ttr): the same per-row bounds, first Ttr rows
+        ops.flash_attention_bwd(q, k, v, a["Xo"][l][:Ttr], a["dX"]["o"][:Ttr], a["lse"][l],
+                                a["delta"], dq, dk, dv, *plan.attn_rows, T=Ttr,
+                                n_heads=self.n_heads, n_kv_heads=self.n_kv_heads,
+                                stat_ld=a["lse"].shape[-1])
 
     def last_loss(self) -> float:
         """Training loss of the last step that ran the LM head (reads the device scalar back)."""

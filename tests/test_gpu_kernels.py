@@ -352,10 +352,11 @@ def test_paged_attention_vs_oracle(n_heads, n_kv):
 
 
 @pytest.mark.parametrize("lens,n_heads,n_kv", [([512], 4, 4), ([1, 63, 64, 65, 200], 4, 2),
-                                               ([130, 7, 300], 8, 2), ([1024], 2, 1)])
+                                               ([130, 7, 300], 8, 2), ([1024], 2, 1),
+                                               ([1] * 40 + [3, 17, 90] + [1] * 30, 4, 1)])
 def test_flash_attention_vs_oracle(lens, n_heads, n_kv):
     """K9: causal attention of packed sequences (ragged lengths incl. 1, tile boundaries 63/64/65,
-    GQA G = 1/2/4) forward + backward against the float64 oracle; q/k/v are column views of one
+    many 1-row decode sequences sharing tiles with short prefills, GQA G = 1/2/4) forward + backward against the float64 oracle; q/k/v are column views of one
     fused q|k|v buffer as in the step; the backward is bitwise repeatable."""
     import numpy as np
     import oracle
@@ -370,17 +371,17 @@ def test_flash_attention_vs_oracle(lens, n_heads, n_kv):
     dout = _bf(T, n_heads * D, gen=g)
     out = torch.zeros(T, n_heads * D, dtype=torch.bfloat16, device="cuda")
     lse = torch.zeros(n_heads, T, device="cuda")
-    ss = torch.from_numpy(seq).cuda()
-    kw = dict(T=T, n_heads=n_heads, n_kv_heads=n_kv, max_seqlen=max(lens))
-    ops.flash_attention(q, k, v, out, lse, ss, **kw)
+    rows = ops.seq_rows(seq, "cuda")
+    kw = dict(T=T, n_heads=n_heads, n_kv_heads=n_kv)
+    ops.flash_attention(q, k, v, out, lse, *rows, **kw)
     dqkv = torch.zeros_like(qkv)
     dq, dk, dv = dqkv[:, :n_heads * D], dqkv[:, n_heads * D:(n_heads + n_kv) * D], dqkv[:, (n_heads + n_kv) * D:]
     delta = torch.zeros(n_heads, T, device="cuda")
-    ops.flash_attention_bwd(q, k, v, out, dout, lse, delta, dq, dk, dv, ss, **kw)
+    ops.flash_attention_bwd(q, k, v, out, dout, lse, delta, dq, dk, dv, *rows, **kw)
     dqkv2 = torch.zeros_like(qkv)
     ops.flash_attention_bwd(q, k, v, out, dout, lse, delta, dqkv2[:, :n_heads * D],
                             dqkv2[:, n_heads * D:(n_heads + n_kv) * D],
-                            dqkv2[:, (n_heads + n_kv) * D:], ss, **kw)
+                            dqkv2[:, (n_heads + n_kv) * D:], *rows, **kw)
     torch.cuda.synchronize()
     assert torch.equal(dqkv, dqkv2)
     f = lambda t: t.float().cpu().numpy()  # noqa: E731
