@@ -182,6 +182,18 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
+def cpu_model() -> str:
+    """Host CPU model (the `lscpu` 'Model name'), for the CPU baseline record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def time_cpu_sample(cfg, repeats: int = 1) -> dict:
     s = cpu_layer_sample(cfg)
     s["fn"]()  # warm
@@ -193,6 +205,7 @@ def time_cpu_sample(cfg, repeats: int = 1) -> dict:
     t_layer = statistics.median(ts)
     step_s = t_layer * s["layers"]
     return {"value": s["rows"] / step_s, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": (f"numpy float64 oracle (oracle/lora_oracle.py), 1 of {s['layers']} layers "
                        f"(all projections fwd over {s['rows']} rows + training bwd + AdamW), "
                        f"{t_layer:.2f} s/layer, extrapolated x{s['layers']}"),
@@ -222,6 +235,7 @@ def run_reference(args, cfg, workload):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": (f"each step = 1 of {s['layers']} layers of the workload "
                                     f"through the numpy oracle (all projections, fwd + training "
                                     f"bwd + AdamW), time x{s['layers']}")},
