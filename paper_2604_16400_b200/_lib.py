@@ -9,6 +9,7 @@ classes (``ConfigurationError`` / ``InvariantViolation``, /root/reference/pkg/sr
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -85,7 +86,8 @@ def load(path: Path | None = None) -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # COLLM_LIB: an alternative build of the same library (A/B timing tools only)
+        p = Path(path) if path else Path(os.environ.get("COLLM_LIB", LIB_PATH))
         if not p.exists():
             raise CollmError(
                 f"{p} is missing: build it with `python -m paper_2604_16400_b200.build` "

@@ -966,6 +966,7 @@ int collm_preload(void) {
   COLLM_PRELOAD((lora_reduce_kernel<16, 3>));
   COLLM_PRELOAD((lora_reduce_kernel<32, 3>));
   COLLM_PRELOAD((lora_reduce_kernel<48, 3>));
+  COLLM_PRELOAD((lora_reduce_kernel<64, 3>));
   COLLM_PRELOAD(lora_apply_kernel);
   COLLM_PRELOAD((cross_entropy_kernel<8, 512>));
   COLLM_PRELOAD(paged_attention_kernel<1>);
@@ -991,12 +992,18 @@ static int expand_reduce_groups(const collm_reduce_group* groups, int n_groups,
                                 collm_reduce_group* out, int* n_out) {
   CHECK_ARG(groups && n_groups >= 1 && n_groups <= kReduceMaxGroups, "n_groups=%d out of [1,%d]",
             n_groups, kReduceMaxGroups);
+  // One launch runs one tile width for all its groups (the MMAs of narrower groups are padded),
+  // so 64-wide tiles pay only when every group is 64 wide (13B: r = 64 dB, 64-rank dA chunks —
+  // each U then streams once per group instead of twice); otherwise groups are cut to <= 48.
+  bool all64 = true;
+  for (int g = 0; g < n_groups; ++g) all64 = all64 && groups[g].Q == 64;
+  const int max_q = all64 ? 64 : 48;
   int n = 0;
   for (int g = 0; g < n_groups; ++g) {
     const collm_reduce_group& s = groups[g];
     CHECK_ARG(s.P > 0 && s.P % 8 == 0 && s.Q > 0 && s.Q % 8 == 0 && s.Q <= 64,
               "group %d: P=%d, Q=%d (need multiples of 8, Q <= 64)", g, s.P, s.Q);
-    const int chunks = (s.Q + kReduceMaxQ - 1) / kReduceMaxQ;
+    const int chunks = (s.Q + max_q - 1) / max_q;
     int off = 0;
     for (int c = 0; c < chunks; ++c) {
       const int q = ((s.Q / 8) * (c + 1) / chunks - (s.Q / 8) * c / chunks) * 8;
@@ -1152,6 +1159,9 @@ int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int
   }
   cudaStream_t st = (cudaStream_t)stream;
   static const int minb = [] { const char* e = getenv("COLLM_K5_MINB"); return e ? atoi(e) : 4; }();
+  // 64-wide tiles (r = 64 dB, 64-rank dA chunks: each U = dY / X_tr read once per ABI group
+  // instead of twice) carry 32 accumulators per thread: 3 CTAs/SM register budget
+  if (qmax > 48) return launch_reduce<64, 3>(p, st);
   if (minb == 3) {
     if (qmax <= 16) return launch_reduce<16, 3>(p, st);
     if (qmax <= 32) return launch_reduce<32, 3>(p, st);

@@ -28,7 +28,7 @@
 namespace collm {
 
 constexpr int kReduceMaxGroups = 16;  // ABI limit per launch: a whole layer's projections
-constexpr int kReduceMaxQ = 48;       // widest group a CTA reduces (wider ABI groups are split)
+constexpr int kReduceMaxQ = 64;       // widest group a CTA reduces (wider ABI groups are split)
 constexpr int kReduceMaxInner = 32;   // groups after that split
 constexpr int kReducePT = 128;     // P rows per CTA tile (8 warps x 16)
 constexpr int kReduceTC = 32;      // T rows per pipeline stage

@@ -10,12 +10,15 @@ from paper_2604_16400_b200 import _lib, ops  # noqa: E402
 from paper_2604_16400_b200.configs import CONFIGS  # noqa: E402
 from paper_2604_16400_b200.layer import ForwardCache, LoraProjection, OptimizerState  # noqa: E402
 
-cfg = CONFIGS["llama2-7b"]
-Ttr, T = 512, 1024
+cfg = CONFIGS[os.environ.get("CFG", "llama2-7b")]
+_tr, _items = cfg.batch(0)
+Ttr = _tr.batch * _tr.seq_len
+T = Ttr + sum(it.n_rows for it in _items)
+NL = int(os.environ.get("LAYERS", "4"))
 opt = OptimizerState()
 opt.advance()
 layers = []
-for l in range(4):
+for l in range(NL):
     groups = []
     for spec in cfg.projections:
         pr = LoraProjection(spec, 2, "cuda")
@@ -57,4 +60,5 @@ g.replay()
 e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / n * 1e3
-print(f"K5 one 7B layer (lean={lean}): {us:.1f} us, ~{nbytes / 1e6:.0f} MB -> {nbytes / us / 1e6:.2f} TB/s")
+print(f"K5 one {cfg.key} layer (lean={lean}): {us:.1f} us, ~{nbytes / 1e6:.0f} MB algorithmic "
+      f"-> {nbytes / us / 1e6:.2f} TB/s")
