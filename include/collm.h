@@ -150,6 +150,27 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
                     const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
                     const int32_t* lora_flag, const int32_t* gen, int lora_pdl, void* stream);
 
+/* Same, with tile_skip (device int32 per 256-row slot tile, may be NULL): tiles marked 1 get no
+ * fused expand (only their base GEMM) — for many-adapter tiles, expanded afterwards by
+ * collm_lora_expand_rows. */
+int collm_gemm_lora_ex(const void* A, int lda, const void* B, int ldb, void* Y, int ldy, int M,
+                       int N, int K, const void* Hslots, int ldh, int h_rows, const void* LB,
+                       int ld_lb, int lb_rows, const int32_t* tile_slot_ptr,
+                       const int32_t* slot_adapter, int lora_rank, int lb_rows_per_adapter,
+                       int n_sub, const int32_t* sub_n_start, const int32_t* sub_h_col, int bn,
+                       void* workspace, size_t ws_bytes, const int32_t* lora_flag,
+                       const int32_t* gen, int lora_pdl, const int32_t* tile_skip, void* stream);
+
+/* Per-row LoRA expand of the 256-row slot tiles listed in `tiles` (device int32, n_tiles):
+ *   Y[t, n] += sum_j H16[t, sub_h_col[s(n)] + j] * B[row_adapter[t]][n, j]   (j < r_pad)
+ * B = [n_adapters, N, r_pad] bf16 (the registry layout), H16 = the shrink's s_a-scaled output.
+ * HBM-bound on the rows' adapters' B (one warp per row and 256 columns); the many-adapter
+ * alternative to the GEMM's fused expand (whose cost grows with slots x r).  Deterministic. */
+int collm_lora_expand_rows(void* Y, int ldy, int N, const void* H16, int ldh, const void* B,
+                           int r_pad, const int32_t* row_adapter, const int32_t* tiles, int n_tiles,
+                           int T, int n_sub, const int32_t* sub_n_start, const int32_t* sub_h_col,
+                           void* stream);
+
 /* Co-residence mode of the kernels (process-wide): 0 (default) -> deepest GEMM pipelines, default
  * carveouts; 1 -> lean GEMM pipelines (~181 KB shared memory per CTA) and the rank-space kernels
  * (shrink, K5) configured to fit next to a GEMM CTA (max-shared carveout, shallower K5 ring) — for

@@ -67,6 +67,9 @@ SIGNATURES: dict[str, tuple] = {
     "collm_set_gemm_lean": (_I, [_I]),
     "collm_gemm_lora": (_I, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _P,
                              _I, _I, _I, _IP, _IP, _I, _P, _SZ, _P, _P, _I, _P]),
+    "collm_gemm_lora_ex": (_I, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P,
+                                _P, _I, _I, _I, _IP, _IP, _I, _P, _SZ, _P, _P, _I, _P, _P]),
+    "collm_lora_expand_rows": (_I, [_P, _I, _I, _P, _I, _P, _I, _P, _P, _I, _I, _I, _IP, _IP, _P]),
     "collm_reduce_workspace_bytes": (_SZ, [_RGP, _I, _I]),
     "collm_lora_reduce": (_I, [_I, _RGP, _I, _I, _I, _F, _P, _I, _P, _SZ, _P]),
     "collm_lora_apply": (_I, [_RGP, _I, _I, _P, _P]),

@@ -22,6 +22,7 @@
 #include "shrink.cuh"
 #include "shrink_tc.cuh"
 #include "flash_attn.cuh"
+#include "expand_rows.cuh"
 
 using namespace collm;
 
@@ -664,6 +665,38 @@ int collm_flash_attention_bwd(const void* q, int ldq, const void* k, int ldk, co
   return flash_launch(flash_bwd_dq_kernel, 98304, dim3(tiles, n_heads), p, st);
 }
 
+
+// ------------------------------------------------------------------------------------ expand rows
+int collm_lora_expand_rows(void* Y, int ldy, int N, const void* H16, int ldh, const void* B,
+                           int r_pad, const int32_t* row_adapter, const int32_t* tiles, int n_tiles,
+                           int T, int n_sub, const int32_t* sub_n_start, const int32_t* sub_h_col,
+                           void* stream) {
+  CHECK_ARG(Y && H16 && B && row_adapter && tiles, "null input");
+  CHECK_ARG(n_tiles >= 0 && T >= 1 && N >= 8 && N % 8 == 0, "n_tiles=%d T=%d N=%d", n_tiles, T, N);
+  if (n_tiles == 0) return COLLM_OK;
+  CHECK_ARG(r_pad == 16 || r_pad == 32 || r_pad == 64, "r_pad=%d must be 16, 32 or 64", r_pad);
+  CHECK_ARG(ldy % 8 == 0 && ldh % 8 == 0 && aligned16(Y) && aligned16(H16) && aligned16(B),
+            "Y/H16/B must be 16-byte aligned with x8 leading dimensions");
+  CHECK_ARG(n_sub >= 1 && n_sub <= 4, "n_sub=%d", n_sub);
+  ExpandRowsParams p{};
+  p.Y = (bf16*)Y; p.ldy = ldy; p.N = N;
+  p.H = (const bf16*)H16; p.ldh = ldh;
+  p.B = (const bf16*)B; p.r_pad = r_pad;
+  p.row_adapter = row_adapter; p.tiles = tiles; p.n_tiles = n_tiles; p.T = T;
+  p.n_sub = n_sub;
+  for (int i = 0; i <= 4; ++i) p.sub_n_start[i] = (i <= n_sub && sub_n_start) ? sub_n_start[i] : N;
+  if (!sub_n_start) p.sub_n_start[0] = 0;
+  for (int i = 0; i < 4; ++i) {
+    p.sub_h_col[i] = (i < n_sub && sub_h_col) ? sub_h_col[i] : 0;
+    CHECK_ARG(p.sub_h_col[i] % 8 == 0 && p.sub_h_col[i] + r_pad <= ldh, "sub %d: H columns exceed ldh", i);
+  }
+  for (int i = 1; i < n_sub; ++i)
+    CHECK_ARG(p.sub_n_start[i] % 128 == 0, "sub boundaries must be multiples of 128");
+  lora_expand_rows_kernel<<<dim3(n_tiles * 32, (N + 127) / 128), 256, 0, (cudaStream_t)stream>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  return COLLM_OK;
+}
+
 // ------------------------------------------------------------------------------------ K2/K3
 
 
@@ -700,6 +733,19 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
                     int lora_rank, int lb_rows_per_adapter, int n_sub, const int32_t* sub_n_start,
                     const int32_t* sub_h_col, int bn, void* workspace, size_t ws_bytes,
                     const int32_t* lora_flag, const int32_t* gen, int lora_pdl, void* stream) {
+  return collm_gemm_lora_ex(A, lda, B, ldb, Y, ldy, M, N, K, Hslots, ldh, h_rows, LB, ld_lb,
+                            lb_rows, tile_slot_ptr, slot_adapter, lora_rank, lb_rows_per_adapter,
+                            n_sub, sub_n_start, sub_h_col, bn, workspace, ws_bytes, lora_flag, gen,
+                            lora_pdl, nullptr, stream);
+}
+
+int collm_gemm_lora_ex(const void* A, int lda, const void* B, int ldb, void* Y, int ldy, int M,
+                       int N, int K, const void* Hslots, int ldh, int h_rows, const void* LB,
+                       int ld_lb, int lb_rows, const int32_t* tile_slot_ptr,
+                       const int32_t* slot_adapter, int lora_rank, int lb_rows_per_adapter,
+                       int n_sub, const int32_t* sub_n_start, const int32_t* sub_h_col, int bn,
+                       void* workspace, size_t ws_bytes, const int32_t* lora_flag,
+                       const int32_t* gen, int lora_pdl, const int32_t* tile_skip, void* stream) {
   CHECK_ARG(A && B && Y, "null operand");
   CHECK_ARG(!lora_flag == !gen, "lora_flag and gen go together");
   CHECK_ARG(M >= 1 && N >= 1 && K >= 1, "empty GEMM M=%d N=%d K=%d", M, N, K);
@@ -824,6 +870,7 @@ int collm_gemm_lora(const void* A, int lda, const void* B, int ldb, void* Y, int
     // widest TMA/UMMA chunk (64/32/16 columns = 128/64/32-byte swizzle) dividing the LoRA width
     const int lrc = (lora_rank % 64 == 0) ? 64 : (lora_rank % 32 == 0) ? 32 : 16;
     p.tile_slot_ptr = tile_slot_ptr;
+    p.tile_skip = tile_skip;
     p.slot_adapter = slot_adapter;
     p.lora_rc = lrc;
     p.lora_chunks = lora_rank / lrc;
@@ -941,6 +988,7 @@ int collm_preload(void) {
   COLLM_PRELOAD((lora_shrink_kernel<8, 2>));
   COLLM_PRELOAD(lora_shrink_tc_kernel);
   COLLM_PRELOAD(flash_fwd_kernel);
+  COLLM_PRELOAD(lora_expand_rows_kernel);
   COLLM_PRELOAD(flash_delta_kernel);
   COLLM_PRELOAD(flash_bwd_dkdv_kernel);
   COLLM_PRELOAD(flash_bwd_dq_kernel);

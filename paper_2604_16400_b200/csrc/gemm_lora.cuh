@@ -60,6 +60,7 @@ struct GemmLoraParams {
   int ldy;  // elements
   // ---- LoRA K-extension (tile_slot_ptr == nullptr -> plain GEMM)
   const int32_t* tile_slot_ptr;  // [num_m_tiles + 1] slot range of each 128-row tile
+  const int32_t* tile_skip;      // optional [slot tiles]: 1 = no fused expand (expand_rows.cuh)
   const int32_t* slot_adapter;   // [n_slots] adapter id of each slot
   int lora_rc;                   // columns per LoRA chunk: 16 / 32 / 64 (one TMA box each)
   int lora_chunks;               // chunks per slot (= lora width / rc)
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(256, 2)  // <= 128 registers: a LoRA CTA can c
   auto lora_items = [&](int m) {
     if (!has_lora) return 0;
     const int st = (m * (int)UNIT_M) / kSlotTileM;
+    if (p.tile_skip && p.tile_skip[st]) return 0;
     return (p.tile_slot_ptr[st + 1] - p.tile_slot_ptr[st]) * p.lora_chunks;
   };
   auto lora_stages = [&](int m) {

@@ -291,7 +291,11 @@ class LoraProjection:
                           lora_rank=rp, lb_rows_per_adapter=spec.out_features, sub_n_start=bnd,
                           sub_h_col=[s * rp for s in range(len(spec.subs))],
                           lora_flag=wait[0][1:] if wait else None, gen=wait[1] if wait else None,
-                          lora_pdl=pdl)
+                          lora_pdl=pdl, tile_skip=plan.tile_skip)
+            if plan.n_expand_tiles:  # many-adapter tiles: per-row expand after the base GEMM
+                ops.lora_expand_rows(Y, cache.H16, self.B, plan.row_adapter, plan.expand_tiles,
+                                     plan.n_expand_tiles, T, r_pad=rp, sub_n_start=bnd,
+                                     sub_h_col=[s * rp for s in range(len(spec.subs))])
         else:
             ops.gemm_lora(X, self.W, Y, M=T)
         return Y

@@ -210,7 +210,7 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
               lb_rows_per_adapter: int = 0, sub_n_start: list[int] | None = None,
               sub_h_col: list[int] | None = None, bn: int = 0,
               lora_flag: torch.Tensor | None = None, gen: torch.Tensor | None = None,
-              lora_pdl: bool = False) -> None:
+              lora_pdl: bool = False, tile_skip: torch.Tensor | None = None) -> None:
     """K2/K3: Y[M,N] = A[M,K] . B[N,K]^T (+ fused multi-adapter LoRA expand), bf16 -> bf16.
     ``lora_flag``/``gen``: wait for a concurrently running shrink's signal before the LoRA
     stages (see collm.h); ``lora_pdl``: launch programmatically dependent on the shrink launched
@@ -233,7 +233,7 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
     n_sub = len(sub_n_start) - 1 if (lora and sub_n_start) else 1
     ws = _gemm_ws.get(_lib.load().collm_gemm_workspace_bytes(0), A.device)
     _lib.call(
-        "collm_gemm_lora", A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), Y.data_ptr(),
+        "collm_gemm_lora_ex", A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), Y.data_ptr(),
         Y.stride(0), M, N, K,
         _p(Hslots) if lora else None, Hslots.stride(0) if lora else 0, h_rows,
         _p(LB) if lora else None, LB.stride(-2) if lora else 0, lb_rows,
@@ -242,7 +242,26 @@ def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | Non
         _lib.int_array(sub_n_start) if (lora and sub_n_start) else None,
         _lib.int_array(sub_h_col) if (lora and sub_h_col) else None, bn, _p(ws),
         0 if ws is None else ws.numel(), _p(lora_flag) if lora else None,
-        _p(gen) if lora else None, int(bool(lora_pdl and lora)), _stream())
+        _p(gen) if lora else None, int(bool(lora_pdl and lora)),
+        _p(tile_skip) if lora else None, _stream())
+
+
+def lora_expand_rows(Y: torch.Tensor, H16: torch.Tensor, B: torch.Tensor, row_adapter: torch.Tensor,
+                     tiles: torch.Tensor, n_tiles: int, T: int, *, r_pad: int,
+                     sub_n_start: list[int] | None = None,
+                     sub_h_col: list[int] | None = None) -> None:
+    """Per-row expand of the many-adapter slot tiles the GEMM skipped (collm_lora_expand_rows):
+    Y[t] += H16[t, sub's ranks] . B_{a(t)}^T.  B = the registry's [n_adapters, N, r_pad]."""
+    for t, n in ((Y, "Y"), (H16, "H16"), (B, "B")):
+        _need(t, torch.bfloat16, n)
+    if n_tiles == 0 or not _launch("shrink"):  # rank-space work (timing kinds, see enabled())
+        return
+    N = B.shape[-2]
+    n_sub = len(sub_n_start) - 1 if sub_n_start else 1
+    _lib.call("collm_lora_expand_rows", Y.data_ptr(), Y.stride(0), N, H16.data_ptr(),
+              H16.stride(0), B.data_ptr(), r_pad, row_adapter.data_ptr(), tiles.data_ptr(),
+              n_tiles, T, n_sub, _lib.int_array(sub_n_start) if sub_n_start else None,
+              _lib.int_array(sub_h_col) if sub_h_col else None, _stream())
 
 
 def reduce_tsplit(T: int, n_tiles: int, device: torch.device) -> int:

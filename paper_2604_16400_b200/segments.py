@@ -14,6 +14,7 @@ lists and the shrink work list are planned by the native host planner (``collm_p
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -154,12 +155,20 @@ class DevicePlan:
         self.tc_ctas = int(tc_ctas)
         items, cta_ptr = (plan_shrink_items(host, self.tc_ctas) if self.tc_ctas
                           else (np.zeros((1, 4), np.int32), np.zeros(1, np.int32)))
+        # many-adapter slot tiles: more LoRA slots than this and the tile's expand leaves the GEMM
+        # (whose fused expand costs slots x r / 64 extra k-stages) for the per-row expand kernel
+        slots = np.diff(host.tile_slot_ptr)
+        thr = int(os.environ.get("COLLM_EXPAND_ROWS_SLOTS", "32"))
+        skip = (slots > thr).astype(np.int32)
+        expand_tiles = np.nonzero(skip)[0].astype(np.int32)
+        self.n_expand_tiles = int(expand_tiles.size)
         # one packed upload: [seg_start | seg_adapter | tile_slot_ptr | slot_adapter | shrink_tiles
         #                     | shrink items | item ranges per CTA]
         parts = [host.seg_start, host.seg_adapter, host.tile_slot_ptr,
                  host.slot_adapter if host.n_slots else np.zeros(1, np.int32),
                  host.shrink_tiles.reshape(-1) if host.shrink_tiles.size else np.zeros(3, np.int32),
-                 items.reshape(-1), cta_ptr]
+                 items.reshape(-1), cta_ptr, skip if skip.size else np.zeros(1, np.int32),
+                 expand_tiles if expand_tiles.size else np.zeros(1, np.int32)]
         sizes = [p.size for p in parts]
         packed = torch.from_numpy(np.concatenate(parts).astype(np.int32)).pin_memory()
         self.h2d_bytes = packed.numel() * 4
@@ -175,6 +184,8 @@ class DevicePlan:
         self.shrink_tiles = buf[offs[4]:offs[5]]
         self.tc_items = buf[offs[5]:offs[6]]
         self.tc_cta_ptr = buf[offs[6]:offs[7]]
+        self.tile_skip = buf[offs[7]:offs[8]] if self.n_expand_tiles else None
+        self.expand_tiles = buf[offs[8]:offs[9]]
         self.n_slots = host.n_slots
         self.max_adapter = int(host.seg_adapter.max()) if host.seg_adapter.size else -1
         self.n_shrink_tiles = int(host.shrink_tiles.shape[0])

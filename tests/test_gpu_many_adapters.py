@@ -30,8 +30,13 @@ def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
 
 
-@pytest.mark.parametrize("rank,T_tr,rank_sms", [(16, 0, 0), (64, 0, 0), (16, 64, 0), (16, 64, 16)])
-def test_many_adapter_decode(rank, T_tr, rank_sms):
+@pytest.mark.parametrize("rank,T_tr,rank_sms,fused", [(16, 0, 0, False), (64, 0, 0, False),
+                                                    (16, 64, 0, False), (16, 64, 16, False),
+                                                    (16, 0, 0, True), (64, 64, 0, True)])
+def test_many_adapter_decode(rank, T_tr, rank_sms, fused, monkeypatch):
+    """fused=False: tiles with > 32 slots skip the GEMM's fused expand and take the per-row
+    expand kernel (collm_lora_expand_rows); fused=True forces the fused expand everywhere."""
+    monkeypatch.setenv("COLLM_EXPAND_ROWS_SLOTS", "100000" if fused else "32")
     from paper_2604_16400_b200 import ops, segments
     from paper_2604_16400_b200.domain import InferenceItem, RowRole, TrainItem
     from paper_2604_16400_b200.layer import LoraProjection, ProjectionSpec
@@ -54,6 +59,7 @@ def test_many_adapter_decode(rank, T_tr, rank_sms):
         slots_per_tile = np.diff(hp.tile_slot_ptr)
         assert slots_per_tile.max() >= 190, slots_per_tile
         plan = segments.DevicePlan(hp)
+        assert (plan.n_expand_tiles > 0) != fused
         spec = ProjectionSpec("many", K, subs, rank, alpha=16.0)
         inp = projection_inputs(g, T, T_tr, K, subs, rank, spec.r_pad, n_ad)
         proj = LoraProjection(spec, n_ad)

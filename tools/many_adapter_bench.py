@@ -46,13 +46,15 @@ def timed(fn, reps=50):
 
 res = {}
 res["base GEMM only"] = timed(lambda: ops.gemm_lora(X, proj.W, Y, M=T))
-for n_distinct in (1, 32, 256):
+for n_distinct, expand_rows in ((1, True), (32, True), (256, False), (256, True)):
+    os.environ["COLLM_EXPAND_ROWS_SLOTS"] = "32" if expand_rows else "100000"
     items = [InferenceItem(i, i * n_distinct // T, 1, RowRole.DECODE) for i in range(T)]
     mb = segments.build_mixed_batch(None, items)
     plan = segments.DevicePlan(segments.plan_segments(mb.seg_start, mb.seg_adapter))
     torch.cuda.synchronize()
-    res[f"{n_distinct} adapters: shrink+GEMM"] = timed(lambda: proj.forward(X, plan, Y))
+    tag = f"{n_distinct} adapters" + (" [per-row expand]" if plan.n_expand_tiles else "")
+    res[f"{tag}: shrink+GEMM"] = timed(lambda: proj.forward(X, plan, Y))
     cache = proj.forward_lora(X, plan)
-    res[f"{n_distinct} adapters: GEMM (fused expand)"] = timed(lambda: proj.forward_gemm(cache, plan, Y))
-    res[f"{n_distinct} adapters: shrink"] = timed(lambda: proj.forward_lora(X, plan))
+    res[f"{tag}: GEMM+expand"] = timed(lambda: proj.forward_gemm(cache, plan, Y))
+    res[f"{tag}: shrink"] = timed(lambda: proj.forward_lora(X, plan))
 print(f"rank {rank}: " + " | ".join(f"{k} {v:.1f} us" for k, v in res.items()))
