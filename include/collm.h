@@ -100,26 +100,35 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
  * collm_set_rank_sms(n): reserve n SMs (even: whole TPCs; 0 = off, the default) of the caller's
  * current device for collm_lora_shrink_tc; every GEMM grid is capped at the other SMs, so a
  * shrink and the GEMM it overlaps are always co-resident.
- * collm_plan_shrink_items (HOST): merges collm_plan_segments' shrink tiles into items of <= max_rows
- * (16/32/64/128) consecutive rows of one adapter (items[4*i] = row_start, n_rows, adapter, class =
- * log2(box rows / 16)) and assigns them longest-first to n_ctas CTAs (CTA c: items
- * [cta_ptr[c], cta_ptr[c+1])).
+ * collm_plan_shrink_windows (HOST): work units over windows of 128 consecutive rows; the distinct
+ * adapters of a window (from collm_plan_segments' shrink tiles) are cut into runs of consecutive
+ * ids whose span rounded up to 2^c keeps 2^c * nr <= 256; base-only rows get a zero unit
+ * (a_lo = -1); big units' K ranges are split into S <= 8 parts (about 2 chunks per CTA); chunks
+ * (items[8*i] = row0, n_rows, a_lo, c, S, part, first chunk of the unit, unit) are assigned
+ * longest-first to n_ctas CTAs (CTA k: chunks [cta_ptr[k], cta_ptr[k+1])).
  * collm_lora_shrink_tc: the collm_lora_shrink contract (same outputs, same group table; here every
  * group has the same n_ranks, a multiple of 16 <= 256, and 64-aligned K ranges) computed by n_ctas
- * CTAs (the rank-space partition) streaming X rows and adapter rank rows through 64 KB TMA stages
- * into tcgen05 MMAs (accumulators in TMEM).  x_rows / a_rows bound the X / A row ranges (rows
- * past them read as zero); A row of (adapter a, rank j) = a * (a_stride / lda) + j.  The kernel
- * lets a programmatically dependent GEMM launch at once (collm_gemm_lora lora_pdl = 1).
+ * CTAs (the rank-space partition): per unit and 64 K, one TMA box of the window's X rows and one of
+ * the 2^c adapters' rank rows, ONE tcgen05.mma per 16 K with the adapters stacked in N (a row
+ * keeps its own adapter's columns); accumulators in TMEM; split units: each part stores its fp32
+ * partial in `workspace` (collm_shrink_tc_workspace_bytes(n_chunks, n_groups), zero-filled once:
+ * arrival counters are restored) and the last part to arrive sums them in part order
+ * (deterministic).  row_adapter [T] (the plan's device expansion).  x_rows / a_rows bound the X / A row ranges (rows past them read as zero); A row of
+ * (adapter a, rank j) = a * (a_stride / lda) + j.  The kernel lets a programmatically dependent
+ * GEMM launch at once (collm_gemm_lora lora_pdl = 1).
  * Replaces: the inference half of perf.true_infer_latency (perf.py:62-74). */
 int collm_set_rank_sms(int n);
 int collm_get_rank_sms(void);
-int collm_plan_shrink_items(const int32_t* tiles, int n_tiles, int n_ctas, int max_rows,
-                            int32_t* items, int item_cap, int32_t* n_items, int32_t* cta_ptr);
+int collm_plan_shrink_windows(const int32_t* tiles, int n_tiles, int nr, int n_ctas,
+                              int32_t* items, int item_cap, int32_t* n_items, int32_t* cta_ptr);
+size_t collm_shrink_tc_workspace_bytes(int n_chunks, int n_groups);
 int collm_lora_shrink_tc(const void* X, int ldx, int x_rows, const void* A, long long a_stride,
                          int lda, int a_rows, const int32_t* items, const int32_t* cta_ptr,
-                         int n_ctas, const float* scale, const int32_t* groups, int n_groups,
-                         float* H32, void* H16, void* H16lo, int ldh, void* Hslots,
-                         const int32_t* slot_of_row, const int32_t* tile_slot_ptr, void* stream);
+                         int n_ctas, int n_chunks, const int32_t* row_adapter, const float* scale,
+                         const int32_t* groups, int n_groups, float* H32, void* H16, void* H16lo,
+                         int ldh, void* Hslots, const int32_t* slot_of_row,
+                         const int32_t* tile_slot_ptr, void* workspace, size_t ws_bytes,
+                         void* stream);
 
 /* ---- K2 / K3: base projection on tcgen05 with the LoRA expand fused into the accumulator ------
  * Y[M,N] = A[M,K] . B[N,K]^T + sum over the LoRA slots s of each 256-row slot tile of

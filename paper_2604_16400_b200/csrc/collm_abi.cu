@@ -439,54 +439,90 @@ int collm_set_rank_sms(int n) {
 }
 int collm_get_rank_sms(void) { return g_rank_sms[cur_device()].load(); }
 
-// Host: merge the <= 16-row shrink tiles (collm_plan_segments) into items of <= max_rows
-// consecutive rows of one adapter, class = the smallest X box height (16/32/64/128) holding them,
-// and assign them to n_ctas CTAs longest-processing-time first (cost ~ rows of the class + the
-// adapter's rank rows, both streamed over the whole K range; base-only items cost ~nothing).
-// items[4*i] = row_start, n_rows, adapter, class; CTA c owns items [cta_ptr[c], cta_ptr[c+1]).
-int collm_plan_shrink_items(const int32_t* tiles, int n_tiles, int n_ctas, int max_rows,
-                            int32_t* items, int item_cap, int32_t* n_items, int32_t* cta_ptr) {
+// Host: work units of collm_lora_shrink_tc.  Rows go in windows of 128 consecutive rows; the
+// distinct adapters of a window (from collm_plan_segments' shrink tiles) are cut into runs of
+// consecutive ids whose span, rounded up to a power of two 2^c, keeps 2^c * nr <= 256 (the MMA's
+// N; ids in the span without rows in the window are loaded and ignored).  Windows with base-only
+// rows get one zero unit (a_lo = -1).  Units are assigned longest-first (cost ~ 128 + 2^c * nr
+// rows streamed per k-block) to n_ctas CTAs.  units[4*i] = row0, n_rows, a_lo, c.
+int collm_plan_shrink_windows(const int32_t* tiles, int n_tiles, int nr, int n_ctas,
+                              int32_t* items, int item_cap, int32_t* n_items, int32_t* cta_ptr) {
   CHECK_ARG(n_tiles >= 0 && n_ctas >= 1, "n_tiles=%d n_ctas=%d", n_tiles, n_ctas);
-  CHECK_ARG(max_rows == 16 || max_rows == 32 || max_rows == 64 || max_rows == 128,
-            "max_rows=%d must be 16/32/64/128", max_rows);
-  struct It { int r0, n, a, cls; long long cost; };
-  std::vector<It> v;
-  for (int i = 0; i < n_tiles;) {
-    const int r0 = tiles[3 * i], a = tiles[3 * i + 2];
-    int n = tiles[3 * i + 1];
-    int j = i + 1;
-    while (j < n_tiles && tiles[3 * j + 2] == a && tiles[3 * j] == r0 + n &&
-           n + tiles[3 * j + 1] <= max_rows) {
-      n += tiles[3 * j + 1];
-      ++j;
+  CHECK_ARG(nr >= 16 && nr % 16 == 0 && nr <= 256, "nr=%d must be a multiple of 16 <= 256", nr);
+  int T = 0;
+  for (int i = 0; i < n_tiles; ++i) T = std::max(T, tiles[3 * i] + tiles[3 * i + 1]);
+  std::vector<int> row_ad(T, -1);
+  for (int i = 0; i < n_tiles; ++i)
+    for (int r = 0; r < tiles[3 * i + 1]; ++r) row_ad[tiles[3 * i] + r] = tiles[3 * i + 2];
+  int max_span = 1;
+  while (max_span * 2 <= 16 && max_span * 2 * nr <= 256) max_span *= 2;
+  struct U { int r0, n, a, c; long long cost; };
+  std::vector<U> v;
+  for (int w = 0; w < T; w += kShrinkTcWindow) {
+    const int n = std::min(kShrinkTcWindow, T - w);
+    std::vector<int> ads;
+    bool base = false;
+    for (int r = w; r < w + n; ++r) {
+      if (row_ad[r] < 0) base = true;
+      else ads.push_back(row_ad[r]);
     }
-    int cls = 0;
-    while ((16 << cls) < n) ++cls;
-    v.push_back({r0, n, a, cls, a < 0 ? 1 : (long long)(16 << cls) + 64});
-    i = j;
+    std::sort(ads.begin(), ads.end());
+    ads.erase(std::unique(ads.begin(), ads.end()), ads.end());
+    for (size_t k = 0; k < ads.size();) {
+      const int a0 = ads[k];
+      size_t e = k + 1;
+      while (e < ads.size() && ads[e] - a0 + 1 <= max_span) ++e;
+      const int span = ads[e - 1] - a0 + 1;
+      int c = 0;
+      while ((1 << c) < span) ++c;
+      v.push_back({w, n, a0, c, (long long)kShrinkTcWindow + (1LL << c) * nr});
+      k = e;
+    }
+    if (base) v.push_back({w, n, -1, 0, 1});
   }
-  CHECK_ARG((int)v.size() <= item_cap, "shrink item capacity %d exceeded (%zu)", item_cap, v.size());
-  std::vector<int> order(v.size());
-  for (size_t i = 0; i < v.size(); ++i) order[i] = (int)i;
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return v[x].cost > v[y].cost; });
+  // split the K range of big units so there are about 2 chunks per CTA: S parts, the last part
+  // to finish sums the fp32 partials in part order (deterministic)
+  long long total = 0;
+  int n_real = 0;
+  for (const U& u : v) {
+    total += u.a >= 0 ? u.cost : 0;
+    n_real += u.a >= 0;
+  }
+  // measured (profiles/r02_rank_partition.md): splitting pays only when the units cannot fill
+  // the CTAs at all (7B fwd down / dH gate|up: 8 units on 16 CTAs, 75 -> 38 us); with >= 3/4 of
+  // a unit per CTA the partial round trip costs more than the imbalance (fwd q|k|v 25 -> 39 us)
+  if (4 * n_real >= 3 * n_ctas) total = 0;
+  struct Ch { int u, S, part, chunk0; long long cost; };
+  std::vector<Ch> ch;
+  for (size_t k = 0; k < v.size(); ++k) {
+    int S = 1;
+    if (v[k].a >= 0 && total > 0)
+      S = (int)std::max(1LL, std::min(8LL, (2LL * n_ctas * v[k].cost + total / 2) / total));
+    const int c0 = (int)ch.size();
+    for (int j = 0; j < S; ++j) ch.push_back({(int)k, S, j, c0, v[k].cost / S + (S > 1 ? 8 : 0)});
+  }
+  CHECK_ARG((int)ch.size() <= item_cap, "shrink chunk capacity %d exceeded (%zu)", item_cap, ch.size());
+  std::vector<int> order(ch.size());
+  for (size_t i = 0; i < ch.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return ch[x].cost > ch[y].cost; });
   std::vector<long long> load(n_ctas, 0);
   std::vector<std::vector<int>> per(n_ctas);
   for (int i : order) {
     int c = 0;
     for (int k = 1; k < n_ctas; ++k)
       if (load[k] < load[c]) c = k;
-    load[c] += v[i].cost;
+    load[c] += ch[i].cost;
     per[c].push_back(i);
   }
   int w = 0;
   for (int c = 0; c < n_ctas; ++c) {
     if (cta_ptr) cta_ptr[c] = w;
     for (int i : per[c]) {
+      const U& u = v[ch[i].u];
       if (items) {
-        items[4 * w] = v[i].r0;
-        items[4 * w + 1] = v[i].n;
-        items[4 * w + 2] = v[i].a;
-        items[4 * w + 3] = v[i].cls;
+        int32_t* o = items + 8 * w;
+        o[0] = u.r0; o[1] = u.n; o[2] = u.a; o[3] = u.c;
+        o[4] = ch[i].S; o[5] = ch[i].part; o[6] = ch[i].chunk0; o[7] = ch[i].u;
       }
       ++w;
     }
@@ -496,18 +532,24 @@ int collm_plan_shrink_items(const int32_t* tiles, int n_tiles, int n_ctas, int m
   return COLLM_OK;
 }
 
+size_t collm_shrink_tc_workspace_bytes(int n_chunks, int n_groups) {
+  return kCounterBytes + (size_t)std::max(0, n_chunks) * std::max(1, n_groups) * 128 * 256 * sizeof(float);
+}
+
 int collm_lora_shrink_tc(const void* X, int ldx, int x_rows, const void* A, long long a_stride,
                          int lda, int a_rows, const int32_t* items, const int32_t* cta_ptr,
-                         int n_ctas, const float* scale, const int32_t* groups, int n_groups,
-                         float* H32, void* H16, void* H16lo, int ldh, void* Hslots,
-                         const int32_t* slot_of_row, const int32_t* tile_slot_ptr, void* stream) {
-  CHECK_ARG(X && A && items && cta_ptr && scale && groups, "null input");
+                         int n_ctas, int n_chunks, const int32_t* row_adapter, const float* scale,
+                         const int32_t* groups, int n_groups, float* H32, void* H16, void* H16lo,
+                         int ldh, void* Hslots, const int32_t* slot_of_row,
+                         const int32_t* tile_slot_ptr, void* workspace, size_t ws_bytes,
+                         void* stream) {
+  CHECK_ARG(X && A && items && cta_ptr && scale && groups && row_adapter, "null input");
   CHECK_ARG(!H16lo || H16, "H16lo needs H16");
   CHECK_ARG(n_ctas >= 2 && n_ctas % 2 == 0, "n_ctas=%d must be even (TPC pairs)", n_ctas);
   CHECK_ARG(n_groups >= 1 && n_groups <= kShrinkTcMaxGroups, "n_groups=%d out of [1,%d]", n_groups,
             kShrinkTcMaxGroups);
   CHECK_ARG(ldx % 8 == 0 && lda % 8 == 0 && ldh % 16 == 0, "ldx/lda must be x8, ldh x16");
-  CHECK_ARG(a_stride % lda == 0, "a_stride must be a multiple of lda");
+  CHECK_ARG(a_stride % lda == 0 && a_stride >= 0, "a_stride must be a multiple of lda");
   CHECK_ARG(aligned16(X) && aligned16(A), "X/A must be 16-byte aligned");
   CHECK_ARG(!Hslots || (slot_of_row && tile_slot_ptr), "Hslots needs slot_of_row, tile_slot_ptr");
   CHECK_ARG(x_rows >= 1 && a_rows >= 1, "empty X/A");
@@ -526,9 +568,15 @@ int collm_lora_shrink_tc(const void* X, int ldx, int x_rows, const void* A, long
     k_end = std::max(k_end, khi);
   }
   CHECK_ARG(k_end <= ldx && k_end <= lda, "K range %d exceeds ldx=%d / lda=%d", k_end, ldx, lda);
+  CHECK_ARG(n_chunks >= 1 && n_chunks <= (int)kCounterCap, "n_chunks=%d", n_chunks);
+  const size_t need = collm_shrink_tc_workspace_bytes(n_chunks, n_groups);
+  CHECK_ARG(workspace && ws_bytes >= need, "shrink_tc workspace too small: %zu < %zu", ws_bytes, need);
+  p.counters = (int32_t*)workspace;
+  p.partials = (float*)((char*)workspace + kCounterBytes);
   p.items = items;
   p.cta_ptr = cta_ptr;
-  p.a_rows_per_adapter = (int)(a_stride / lda);
+  p.row_adapter = row_adapter;
+  p.a_single = a_stride == 0;
   p.scale = scale;
   p.H32 = H32;
   p.H16 = (bf16*)H16;
@@ -537,19 +585,37 @@ int collm_lora_shrink_tc(const void* X, int ldx, int x_rows, const void* A, long
   p.Hslots = (bf16*)Hslots;
   p.slot_of_row = slot_of_row;
   p.tile_slot_ptr = tile_slot_ptr;
-  { const char* e = getenv("COLLM_DEBUG_SHRINK_NO_MMA"); p.debug_no_mma = e ? atoi(e) : 0; }
-  CUtensorMap tx[kShrinkTcClasses], ta[kShrinkTcClasses];
+  // A viewed as [adapter][rank row][K]: rows per adapter = a_stride / lda (single adapter when
+  // a_stride == 0: all a_rows rows)
+  const long long rows_per_ad = a_stride > 0 ? a_stride / lda : a_rows;
+  const long long n_ad = a_stride > 0 ? std::max(1LL, (long long)a_rows / rows_per_ad) : 1;
+  auto fn = encode_fn();
+  if (!fn) return fail(COLLM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  ShrinkTcMaps maps;
   for (int c = 0; c < kShrinkTcClasses; ++c) {
-    const int nb = 16 << c;
-    // k-blocks per stage: fill the ~64 KB stage (bigger copies stream faster per SM, tools/sm_bw.py)
-    int kb = (int)(kShrinkTcStageBytes / ((uint32_t)(nb + p.nr) * 128));
+    const int na = 1 << c;
+    if (c > 0 && na * p.nr > 256) {  // class unusable at this width (the planner never emits it)
+      maps.x[c] = maps.x[0];
+      maps.a[c] = maps.a[0];
+      p.kb[c] = p.kb[0];
+      continue;
+    }
+    // k-blocks per stage: fill the ~64 KB stage (bigger copies stream faster per SM, sm_bw.py)
+    int kb = (int)(kShrinkTcStageBytes / ((uint32_t)(kShrinkTcWindow + na * p.nr) * 128));
     kb = std::max(1, std::min(16, kb));
-    p.nb[c] = nb;
     p.kb[c] = kb;
-    int rc = make_tmap_kblocks(&tx[c], X, x_rows, ldx, k_end / 64, nb, kb);
+    int rc = make_tmap_kblocks(&maps.x[c], X, x_rows, ldx, k_end / 64, kShrinkTcWindow, kb);
     if (rc) return rc;
-    rc = make_tmap_kblocks(&ta[c], A, a_rows, lda, k_end / 64, p.nr, kb);
-    if (rc) return rc;
+    cuuint64_t dims[4] = {64, (cuuint64_t)rows_per_ad, (cuuint64_t)n_ad, (cuuint64_t)(k_end / 64)};
+    cuuint64_t strides[3] = {(cuuint64_t)lda * 2,
+                             (cuuint64_t)(a_stride > 0 ? a_stride * 2 : rows_per_ad * lda * 2), 128};
+    cuuint32_t box[4] = {64, (cuuint32_t)p.nr, (cuuint32_t)na, (cuuint32_t)kb};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(&maps.a[c], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(A), dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(COLLM_ECUDA, "cuTensorMapEncodeTiled (stacked adapters) failed (%d)", (int)r);
   }
   {
     static bool configured[kMaxDevices] = {};
@@ -573,11 +639,9 @@ int collm_lora_shrink_tc(const void* X, int ldx, int x_rows, const void* A, long
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_tc_kernel, tx[0], tx[1], tx[2], tx[3], ta[0], ta[1],
-                              ta[2], ta[3], p));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, lora_shrink_tc_kernel, maps, p));
   return COLLM_OK;
 }
-
 
 // ------------------------------------------------------------------------------------ K9
 static int flash_setup(FlashParams& p, const void* q, int ldq, const void* k, int ldk, const void* v,

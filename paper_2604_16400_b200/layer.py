@@ -254,8 +254,9 @@ class LoraProjection:
             Hs = Hslots[: plan.n_slots * TILE_M]
             groups = [(g, min(64, R - g), 0, K) for g in range(0, R, 64)]
             tc = ops.shrink_tc_groups(groups) if plan.tc_ctas and signal is None else None
-            if tc:  # the rank-space SM partition (collm_lora_shrink_tc)
-                ops.lora_shrink_tc(X, self.A, plan.tc_items, plan.tc_cta_ptr, plan.tc_ctas,
+            units = plan.tc_units(tc[0][1]) if tc else None
+            if units:  # the rank-space SM partition (collm_lora_shrink_tc)
+                ops.lora_shrink_tc(X, self.A, *units, plan.tc_ctas, plan.row_adapter,
                                    self.scale, tc, R, H16=H16, Hslots=Hs,
                                    slot_of_row=plan.slot_of_row, tile_slot_ptr=plan.tile_slot_ptr)
             else:
@@ -365,10 +366,10 @@ class LoraProjection:
         groups = [(s * rp + g, min(64, rp - g), bnd[s], bnd[s + 1])
                   for s in range(len(spec.subs)) for g in range(0, rp, 64)]
         tc = ops.shrink_tc_groups(groups) if train_plan.tc_ctas and signal is None else None
-        if tc:  # the rank-space SM partition (collm_lora_shrink_tc)
-            ops.lora_shrink_tc(dY, st.BT16, train_plan.tc_items, train_plan.tc_cta_ptr,
-                               train_plan.tc_ctas, self.scale, tc, R, a_stride=0, H16=dH16,
-                               H16lo=self._dh_lo(Ttr))
+        units = train_plan.tc_units(tc[0][1]) if tc else None
+        if units:  # the rank-space SM partition (collm_lora_shrink_tc)
+            ops.lora_shrink_tc(dY, st.BT16, *units, train_plan.tc_ctas, train_plan.row_adapter,
+                               self.scale, tc, R, a_stride=0, H16=dH16, H16lo=self._dh_lo(Ttr))
         else:
             ops.lora_shrink(dY, st.BT16, train_plan.shrink_tiles, train_plan.n_shrink_tiles,
                             self.scale, groups, R, a_stride=0, H16=dH16, H16lo=self._dh_lo(Ttr),

@@ -111,6 +111,7 @@ class Workspace:
 
 _reduce_ws = Workspace()
 _gemm_ws = Workspace()
+_shrink_tc_ws = Workspace()  # its own: a partition shrink runs concurrently with a GEMM
 
 
 def lora_shrink(X: torch.Tensor, A: torch.Tensor, tiles: torch.Tensor, n_tiles: int,
@@ -181,13 +182,15 @@ def shrink_tc_groups(groups: list[tuple[int, int, int, int]]) -> list[tuple[int,
 
 
 def lora_shrink_tc(X: torch.Tensor, A: torch.Tensor, items: torch.Tensor, cta_ptr: torch.Tensor,
-                   n_ctas: int, scale: torch.Tensor, groups: list[tuple[int, int, int, int]],
+                   n_ctas: int, row_adapter: torch.Tensor, scale: torch.Tensor,
+                   groups: list[tuple[int, int, int, int]],
                    ldh: int, *, a_stride: int | None = None, H32: torch.Tensor | None = None,
                    H16: torch.Tensor | None = None, H16lo: torch.Tensor | None = None,
                    Hslots: torch.Tensor | None = None, slot_of_row: torch.Tensor | None = None,
                    tile_slot_ptr: torch.Tensor | None = None) -> None:
     """K1 on the rank-space SM partition (collm_lora_shrink_tc): same outputs as lora_shrink;
-    ``groups`` from :func:`shrink_tc_groups`, items / cta_ptr from the plan."""
+    ``groups`` from :func:`shrink_tc_groups`, units / cta_ptr from ``plan.tc_units(nr)``,
+    ``row_adapter`` the plan's device expansion."""
     _need(X, torch.bfloat16, "X")
     _need(A, torch.bfloat16, "A")
     if not _launch("shrink"):
@@ -197,10 +200,14 @@ def lora_shrink_tc(X: torch.Tensor, A: torch.Tensor, items: torch.Tensor, cta_pt
         a_stride = A.stride(0) if A.dim() == 3 else 0
     a_rows = A.numel() // lda
     flat = [v for g in groups for v in g]
+    n_chunks = items.numel() // 8
+    ws = _shrink_tc_ws.get(_lib.load().collm_shrink_tc_workspace_bytes(n_chunks, len(groups)),
+                           X.device)
     _lib.call("collm_lora_shrink_tc", X.data_ptr(), X.stride(0), X.shape[0], A.data_ptr(),
-              int(a_stride), lda, a_rows, items.data_ptr(), cta_ptr.data_ptr(), n_ctas,
-              scale.data_ptr(), _lib.int_array(flat), len(groups), _p(H32), _p(H16), _p(H16lo),
-              ldh, _p(Hslots), _p(slot_of_row), _p(tile_slot_ptr), _stream())
+              int(a_stride), lda, a_rows, items.data_ptr(), cta_ptr.data_ptr(), n_ctas, n_chunks,
+              row_adapter.data_ptr(), scale.data_ptr(), _lib.int_array(flat), len(groups), _p(H32),
+              _p(H16), _p(H16lo), ldh, _p(Hslots), _p(slot_of_row), _p(tile_slot_ptr), _p(ws),
+              0 if ws is None else ws.numel(), _stream())
 
 
 def gemm_lora(A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, *, M: int | None = None,

@@ -114,23 +114,22 @@ def plan_segments(seg_start, seg_adapter) -> HostPlan:
     return HostPlan(ss, sa, tsp, slots[: ns.value].copy(), tiles[: nt.value].copy())
 
 
-def plan_shrink_items(host: HostPlan, n_ctas: int, max_rows: int | None = None):
-    """collm_plan_shrink_items: the shrink tiles merged into <=max_rows-row items and assigned
-    longest-first to ``n_ctas`` CTAs -> (items [n, 4], cta_ptr [n_ctas + 1]).  Without
-    ``max_rows`` the largest of 128/64/32 that still yields an item per CTA is used."""
+TC_RANKS = (16, 32, 48, 64, 96, 128, 192, 256)  # group widths the K1' units are planned for
+
+
+def plan_shrink_windows(host: HostPlan, nr: int, n_ctas: int):
+    """collm_plan_shrink_windows: K1' work chunks (128-row windows x runs of consecutive adapter
+    ids stacked in the MMA's N <= 256 for groups of ``nr`` ranks, big units split along K),
+    assigned longest-first to ``n_ctas`` CTAs -> (chunks [n, 8], cta_ptr [n_ctas + 1])."""
     tiles = np.ascontiguousarray(host.shrink_tiles.reshape(-1, 3).astype(np.int32))
     nt = int(tiles.shape[0])
     ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))  # noqa: E731
-    cands = [max_rows] if max_rows else [128, 64, 32]
-    for mr in cands:
-        cap = max(1, int(host.seg_start[-1]) // 16 + nt + 1)
-        items = np.zeros((cap, 4), np.int32)
-        ptr = np.zeros(n_ctas + 1, np.int32)
-        n = C.c_int32(0)
-        _lib.call("collm_plan_shrink_items", ip(tiles), nt, n_ctas, mr, ip(items), cap,
-                  C.byref(n), ip(ptr))
-        if n.value >= n_ctas:
-            break
+    cap = max(1, 8 * (2 * (int(host.seg_start[-1]) // 128 + 1) + nt))
+    items = np.zeros((cap, 8), np.int32)
+    ptr = np.zeros(n_ctas + 1, np.int32)
+    n = C.c_int32(0)
+    _lib.call("collm_plan_shrink_windows", ip(tiles), nt, nr, n_ctas, ip(items), cap, C.byref(n),
+              ip(ptr))
     return items[: max(1, n.value)].copy(), ptr
 
 
@@ -153,8 +152,9 @@ class DevicePlan:
             from . import ops
             tc_ctas = ops.rank_sms(dev) if dev.type == "cuda" else 0
         self.tc_ctas = int(tc_ctas)
-        items, cta_ptr = (plan_shrink_items(host, self.tc_ctas) if self.tc_ctas
-                          else (np.zeros((1, 4), np.int32), np.zeros(1, np.int32)))
+        # K1' units per group width (the rank-space partition, collm_set_rank_sms)
+        tc_plans = [plan_shrink_windows(host, nr, self.tc_ctas) for nr in TC_RANKS] \
+            if self.tc_ctas else []
         # many-adapter slot tiles: more LoRA slots than this and the tile's expand leaves the GEMM
         # (whose fused expand costs slots x r / 64 extra k-stages) for the per-row expand kernel
         slots = np.diff(host.tile_slot_ptr)
@@ -167,8 +167,10 @@ class DevicePlan:
         parts = [host.seg_start, host.seg_adapter, host.tile_slot_ptr,
                  host.slot_adapter if host.n_slots else np.zeros(1, np.int32),
                  host.shrink_tiles.reshape(-1) if host.shrink_tiles.size else np.zeros(3, np.int32),
-                 items.reshape(-1), cta_ptr, skip if skip.size else np.zeros(1, np.int32),
+                 skip if skip.size else np.zeros(1, np.int32),
                  expand_tiles if expand_tiles.size else np.zeros(1, np.int32)]
+        for it, ptr in tc_plans:
+            parts += [it.reshape(-1), ptr]
         sizes = [p.size for p in parts]
         packed = torch.from_numpy(np.concatenate(parts).astype(np.int32)).pin_memory()
         self.h2d_bytes = packed.numel() * 4
@@ -182,10 +184,10 @@ class DevicePlan:
         self.tile_slot_ptr = buf[offs[2]:offs[3]]
         self.slot_adapter = buf[offs[3]:offs[4]]
         self.shrink_tiles = buf[offs[4]:offs[5]]
-        self.tc_items = buf[offs[5]:offs[6]]
-        self.tc_cta_ptr = buf[offs[6]:offs[7]]
-        self.tile_skip = buf[offs[7]:offs[8]] if self.n_expand_tiles else None
-        self.expand_tiles = buf[offs[8]:offs[9]]
+        self.tile_skip = buf[offs[5]:offs[6]] if self.n_expand_tiles else None
+        self.expand_tiles = buf[offs[6]:offs[7]]
+        self._tc = {nr: (buf[offs[7 + 2 * k]:offs[8 + 2 * k]], buf[offs[8 + 2 * k]:offs[9 + 2 * k]])
+                    for k, nr in enumerate(TC_RANKS)} if self.tc_ctas else {}
         self.n_slots = host.n_slots
         self.max_adapter = int(host.seg_adapter.max()) if host.seg_adapter.size else -1
         self.n_shrink_tiles = int(host.shrink_tiles.shape[0])
@@ -193,6 +195,10 @@ class DevicePlan:
         self.slot_of_row = torch.empty(self.n_rows, dtype=torch.int32, device=dev)
         if expand:
             self.expand(stream)
+
+    def tc_units(self, nr: int):
+        """(units, cta_ptr) of K1' for groups of ``nr`` ranks, or None (no partition / width)."""
+        return self._tc.get(nr)
 
     def upload(self) -> int:
         """Re-send the (pinned) host tables to the same device buffers on the current stream —

@@ -149,10 +149,11 @@ def test_shrink(R, K):
     _close_bf16(H16.cpu(), ref)
 
 
-@pytest.mark.parametrize("R,K,n_ctas,dh", [(16, 512, 2, False), (48, 4096, 16, False),
-                                           (96, 1024, 8, False), (192, 5120, 16, False),
-                                           (48, 11008, 8, True), (192, 2048, 4, True)])
-def test_shrink_tc(R, K, n_ctas, dh):
+@pytest.mark.parametrize("R,K,n_ctas,dh,n_ad", [(16, 512, 2, False, 5), (48, 4096, 16, False, 5),
+                                                (96, 1024, 8, False, 5), (192, 5120, 16, False, 5),
+                                                (16, 1024, 8, False, 40), (48, 2048, 16, False, 40),
+                                                (48, 11008, 8, True, 5), (192, 2048, 4, True, 5)])
+def test_shrink_tc(R, K, n_ctas, dh, n_ad):
     """K1 on the rank-space partition (collm_lora_shrink_tc: TMA k-block boxes -> tcgen05 ->
     TMEM): items of <= 128 rows merged from ragged 16-row tiles (1-row tile, a base-only
     segment, a >128-row run, rows crossing a 256-row slot tile), fused rank groups up to 192,
@@ -162,19 +163,20 @@ def test_shrink_tc(R, K, n_ctas, dh):
     import numpy as np
     from paper_2604_16400_b200 import ops, segments
     g = torch.Generator().manual_seed(R + K)
-    n_ad = 5
     if dh:
         seg, seg_ad = [0, 300], [3]
-    else:
+    elif n_ad == 5:
         seg, seg_ad = [0, 40, 41, 90, 150, 160, 430], [2, 0, 3, -1, 1, 4]
+    else:  # many short runs of consecutive (and skipped) ids: windows stack several adapters
+        ids = [i for i in range(n_ad) if i % 7 != 3]
+        lens = [1 + (i * 5) % 11 for i in range(len(ids))]
+        seg = [0] + list(np.cumsum(lens))
+        seg_ad = ids
     T = seg[-1]
     X = _bf(T, K, gen=g)
     A = _bf(n_ad, R, K, scale=0.05, gen=g)
-    scale = torch.tensor([1.0, 2.0, 0.5, 3.0, 0.25]).cuda()
+    scale = torch.tensor([0.25 * (1 + i % 7) for i in range(n_ad)]).cuda()
     host = segments.plan_segments(seg, seg_ad)
-    items, ptr = segments.plan_shrink_items(host, n_ctas)
-    it_d = torch.from_numpy(items).cuda()
-    ptr_d = torch.from_numpy(ptr).cuda()
     if dh:  # per-sub K ranges (N ranges of the fused projection), one group per sub
         n_sub = 3 if R % 3 == 0 else 2
         rp = R // n_sub
@@ -184,19 +186,25 @@ def test_shrink_tc(R, K, n_ctas, dh):
         groups = [(0, R, 0, K)]
     tc = ops.shrink_tc_groups(groups)
     assert tc is not None
+    items, ptr = segments.plan_shrink_windows(host, tc[0][1], n_ctas)
+    it_d = torch.from_numpy(items).cuda()
+    ptr_d = torch.from_numpy(ptr).cuda()
     H32 = torch.zeros(T, R, device="cuda")
     H16 = torch.zeros(T, R, dtype=torch.bfloat16, device="cuda")
     H16lo = torch.zeros(T, R, dtype=torch.bfloat16, device="cuda")
-    dp = segments.DevicePlan(host, "cuda", tc_ctas=0)
+    dp = segments.DevicePlan(host, "cuda", tc_ctas=0)  # (its device row_adapter / slot tables)
     torch.cuda.synchronize()
     n_slots = host.n_slots
     Hs = torch.full((max(1, n_slots) * 256, R), 7.0, dtype=torch.bfloat16, device="cuda")
     kw = dict(H32=H32, H16=H16, H16lo=H16lo)
     if not dh:
         kw.update(Hslots=Hs, slot_of_row=dp.slot_of_row, tile_slot_ptr=dp.tile_slot_ptr)
-    ops.lora_shrink_tc(X, A, it_d, ptr_d, n_ctas, scale, tc, R, **kw)
+    ra = dp.row_adapter
+    a_stride = 0 if dh else None
+    Ad = A[seg_ad[0]] if dh else A  # dH: one adapter's B_t^T-like [R, K] operand
+    ops.lora_shrink_tc(X, Ad, it_d, ptr_d, n_ctas, ra, scale, tc, R, a_stride=a_stride, **kw)
     H32b = torch.zeros_like(H32)
-    ops.lora_shrink_tc(X, A, it_d, ptr_d, n_ctas, scale, tc, R, H32=H32b)
+    ops.lora_shrink_tc(X, Ad, it_d, ptr_d, n_ctas, ra, scale, tc, R, a_stride=a_stride, H32=H32b)
     torch.cuda.synchronize()
     assert torch.equal(H32, H32b)
     ref = torch.zeros(T, R)

@@ -149,30 +149,43 @@ def test_flop_accounting_matches_survey():
     assert sum(2 * s.in_features * s.out_features for s in specs) * 32 == per_row
 
 
-@pytest.mark.parametrize("n_ctas", [2, 8, 16])
-def test_plan_shrink_items(lib, n_ctas):
-    """collm_plan_shrink_items (host): the <=16-row shrink tiles merge into items of consecutive
-    rows of ONE adapter (never across adapters or base-only runs, never above max_rows), every
-    row is covered exactly once, the class is the smallest box height holding the item, and the
-    longest-first assignment keeps the CTA loads within one item of each other."""
+@pytest.mark.parametrize("n_ctas,nr", [(2, 16), (8, 48), (16, 32), (16, 256)])
+def test_plan_shrink_windows(lib, n_ctas, nr):
+    """collm_plan_shrink_windows (host): units are 128-row windows x runs of consecutive adapter
+    ids whose span rounded to 2^c keeps 2^c * nr <= 256; every (row, adapter) of the batch is in
+    exactly one unit's window and adapter range, base-only rows in a zero unit; the longest-first
+    assignment keeps the CTA loads within one unit of each other."""
     import numpy as np
     from paper_2604_16400_b200 import segments
-    g = np.random.default_rng(n_ctas)
+    g = np.random.default_rng(n_ctas + nr)
     lens = g.integers(1, 300, 40)
-    ads = g.integers(-1, 12, 40)
-    ads[1:][ads[1:] == ads[:-1]] = 12  # break equal neighbours (the planner merges runs anyway)
+    ads = g.integers(-1, 24, 40)
     seg = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     host = segments.plan_segments(seg, ads)
-    for mr in (128, 32):
-        items, ptr = segments.plan_shrink_items(host, n_ctas, max_rows=mr)
-        assert ptr[0] == 0 and ptr[-1] == len(items) and np.all(np.diff(ptr) >= 0)
-        row_ad = np.repeat(ads, lens)
-        covered = np.zeros(seg[-1], np.int32)
-        for r0, n, a, cls in items:
-            assert 1 <= n <= mr and (16 << cls) >= n and (cls == 0 or (16 << (cls - 1)) < n)
-            assert np.all(row_ad[r0:r0 + n] == a)
-            covered[r0:r0 + n] += 1
-        assert np.all(covered == 1)
-        cost = [(16 << c) + 64 if a >= 0 else 1 for _, _, a, c in items]
-        loads = [sum(cost[ptr[c]:ptr[c + 1]]) for c in range(n_ctas)]
-        assert max(loads) - min(loads) <= max(cost)
+    chunks, ptr = segments.plan_shrink_windows(host, nr, n_ctas)
+    assert ptr[0] == 0 and ptr[-1] == len(chunks) and np.all(np.diff(ptr) >= 0)
+    row_ad = np.repeat(ads, lens)
+    T = int(seg[-1])
+    covered = np.zeros(T, np.int32)
+    # every unit's parts 0..S-1 appear exactly once, with one first-chunk id per unit
+    parts = {}
+    for r0, n, a, c, S, part, c0, u in chunks:
+        parts.setdefault(u, []).append((part, S, c0))
+    for u, ps in parts.items():
+        assert sorted(p for p, _, _ in ps) == list(range(ps[0][1])) and len({c0 for *_, c0 in ps}) == 1
+    units = [tuple(ch[:4]) for ch in chunks if ch[5] == 0]
+    for r0, n, a, c in units:
+        assert r0 % 128 == 0 and n == min(128, T - r0)
+        rows = np.arange(r0, r0 + n)
+        if a < 0:
+            mine = rows[row_ad[rows] < 0]
+        else:
+            assert (1 << c) * nr <= 256 and (1 << c) <= 16
+            mine = rows[(row_ad[rows] >= a) & (row_ad[rows] < a + (1 << c))]
+            assert a in set(row_ad[rows])
+        covered[mine] += 1
+    assert np.all(covered == 1)
+    cost = [((128 + (1 << c) * nr) // S + (8 if S > 1 else 0)) if a >= 0 else 1
+            for _, _, a, c, S, *_ in chunks]
+    loads = [sum(cost[ptr[c]:ptr[c + 1]]) for c in range(n_ctas)]
+    assert max(loads) - min(loads) <= max(cost)

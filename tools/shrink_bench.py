@@ -36,9 +36,10 @@ for name, K, R, fwd, subs in (("fwd qkv", 4096, 48, True, 1), ("fwd o", 4096, 16
 
         def run(i):
             if TC:
-                ops.lora_shrink_tc(Xs[i % reps], A, plan.tc_items, plan.tc_cta_ptr, TC, scale,
-                                   ops.shrink_tc_groups(groups), R, H16=H16, Hslots=Hs,
-                                   slot_of_row=plan.slot_of_row, tile_slot_ptr=plan.tile_slot_ptr)
+                g = ops.shrink_tc_groups(groups)
+                ops.lora_shrink_tc(Xs[i % reps], A, *plan.tc_units(g[0][1]), TC, plan.row_adapter,
+                                   scale, g, R, H16=H16, Hslots=Hs, slot_of_row=plan.slot_of_row,
+                                   tile_slot_ptr=plan.tile_slot_ptr)
                 return
             ops.lora_shrink(Xs[i % reps], A, plan.shrink_tiles, plan.n_shrink_tiles, scale, groups, R,
                             H16=H16, Hslots=Hs, slot_of_row=plan.slot_of_row,
@@ -56,8 +57,9 @@ for name, K, R, fwd, subs in (("fwd qkv", 4096, 48, True, 1), ("fwd o", 4096, 16
 
         def run(i):
             if TC:
-                ops.lora_shrink_tc(Xs[i % reps], BT, tplan.tc_items, tplan.tc_cta_ptr, TC, scale,
-                                   ops.shrink_tc_groups(groups), R, a_stride=0, H16=H16, H16lo=H16lo)
+                g = ops.shrink_tc_groups(groups)
+                ops.lora_shrink_tc(Xs[i % reps], BT, *tplan.tc_units(g[0][1]), TC, tplan.row_adapter,
+                                   scale, g, R, a_stride=0, H16=H16, H16lo=H16lo)
                 return
             ops.lora_shrink(Xs[i % reps], BT, tplan.shrink_tiles, tplan.n_shrink_tiles, scale, groups,
                             R, a_stride=0, H16=H16, H16lo=H16lo)
