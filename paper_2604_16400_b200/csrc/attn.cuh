@@ -15,6 +15,7 @@
 // once) + the queries and outputs.
 #pragma once
 #include "common.cuh"
+#include "flash_attn.cuh"
 
 namespace collm {
 
@@ -203,6 +204,184 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attention_kernel(const Att
       As += f * __ldcg(b + 2 + tid);
     }
     p.out[(size_t)t * p.ldo + (h0 + g) * kAttnD + tid] = __float2bfloat16_rn(As / Ls);
+  }
+}
+
+
+// Tensor-core variant for GQA groups (G >= 2): the G query heads of a KV head are the rows of ONE
+// m16n8k16 MMA (rows G..15 zero), so each K/V element feeds G heads through the tensor pipe
+// instead of G shuffle-reduced dot products (the CUDA-core kernel above is issue-bound at G = 4:
+// 1.4 TB/s).  Each of the 4 warps stages 64 tokens of the split (K and V rows, 2 x 16 KB, cp.async
+// into XOR-swizzled shared memory, zero-filled past the split end), computes S = Q K^T (64 MMAs),
+// a local base-2 softmax per head row and O = P V (64 MMAs, P from the score fragments); the warps
+// merge in fixed order and splits combine exactly as above (deterministic).
+constexpr int kAttnTcSmem = 4 * 32768;
+
+template <int G>
+__global__ void __launch_bounds__(kAttnThreads, 1) paged_attention_tc_kernel(const AttnParams p) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  constexpr int kW = kAttnThreads / 32;  // 4 warps x 64 tokens = one 256-token split
+  extern __shared__ __align__(128) uint8_t asm_[];
+  const int t = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
+  const int pos = p.row_pos[t];
+  const int n_tok = min(pos + 1, p.max_splits * kAttnSplit);
+  const int n_splits = (n_tok + kAttnSplit - 1) / kAttnSplit;
+  if (split >= n_splits) return;
+  const int seq = p.row_seq[t];
+  const int j0 = split * kAttnSplit, j1 = min(n_tok, j0 + kAttnSplit);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  const int psz = 1 << p.page_shift;
+  const int32_t* bt = p.block_table + (size_t)seq * p.bt_stride;
+  const int h0 = kvh * G;
+  const int jw0 = j0 + warp * 64;
+  const int nvalid = max(0, min(64, j1 - jw0));
+  uint8_t* Ks = asm_ + warp * 32768;
+  uint8_t* Vs = Ks + 16384;
+  // stage this warp's 64 tokens of K and V (rows past the split end zero-filled)
+  for (int i = lane; i < 64 * 16; i += 32) {
+    const int row = i >> 4, ch = i & 15;
+    const bool ok = row < nvalid;
+    const int j = ok ? jw0 + row : j0;
+    const size_t off = (((size_t)bt[j >> p.page_shift] * p.n_kv_heads + kvh) * psz + (j & (psz - 1))) *
+                       kAttnD + ch * 8;
+    cp_async_16(Ks + fa_off(row, ch * 8), p.k_cache + off, ok);
+    cp_async_16(Vs + fa_off(row, ch * 8), p.v_cache + off, ok);
+  }
+  cp_async_commit();
+  // Q fragments: rows = the group's heads (rows >= G zero), 8 k-steps over the 128 dims
+  uint32_t qa[8][4];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const uint32_t* qp = reinterpret_cast<const uint32_t*>(p.q + (size_t)t * p.ldq + (h0 + g) * kAttnD + kk * 16 + 2 * c);
+    qa[kk][0] = g < G ? __ldg(qp) : 0u;
+    qa[kk][1] = 0u;
+    qa[kk][2] = g < G ? __ldg(qp + 4) : 0u;
+    qa[kk][3] = 0u;
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+  const uint32_t kb = smem_u32(Ks), vb = smem_u32(Vs);
+  float sc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+    for (int jn = 0; jn < 4; ++jn) {
+      uint32_t b[4];
+      fa_ldb_nk(b, kb, jn * 16, kk * 16, lane);
+      mma16816(sc[2 * jn], qa[kk], b[0], b[1]);
+      mma16816(sc[2 * jn + 1], qa[kk], b[2], b[3]);
+    }
+  // local softmax of head row g over this warp's tokens (base 2)
+  float m = -INFINITY;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const bool ok = nt * 8 + 2 * c + e < nvalid;
+      sc[nt][e] = ok ? sc[nt][e] * p.scale * kLog2e : -INFINITY;
+      m = fmaxf(m, sc[nt][e]);
+      sc[nt][2 + e] = 0.f;  // rows g+8: no head
+    }
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  float l = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float v = m == -INFINITY ? 0.f : exp2f(sc[nt][e] - m);
+      sc[nt][e] = v;
+      l += v;
+    }
+  l += __shfl_xor_sync(0xffffffffu, l, 1);
+  l += __shfl_xor_sync(0xffffffffu, l, 2);
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    uint32_t pa[4];
+    fa_c2a(pa, sc[2 * kk], sc[2 * kk + 1]);
+#pragma unroll
+    for (int jd = 0; jd < 8; ++jd) {
+      uint32_t b[4];
+      fa_ldb_kn(b, vb, jd * 16, kk * 16, lane);
+      mma16816(o[2 * jd], pa, b[0], b[1]);
+      mma16816(o[2 * jd + 1], pa, b[2], b[3]);
+    }
+  }
+  // merge the 4 warps (fixed order) through shared memory
+  __shared__ float sml[kW][kAttnMaxG][2];
+  __shared__ __align__(16) float sacc[kW][kAttnMaxG][kAttnD];
+  __shared__ bool s_last;
+  if (g < G) {
+    if (c == 0) {
+      sml[warp][g][0] = m;
+      sml[warp][g][1] = l;
+    }
+#pragma unroll
+    for (int dt = 0; dt < 16; ++dt) {
+      sacc[warp][g][dt * 8 + 2 * c] = o[dt][0];
+      sacc[warp][g][dt * 8 + 2 * c + 1] = o[dt][1];
+    }
+  }
+  __syncthreads();
+  float M[G], L[G], A[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    M[h] = -INFINITY;
+    for (int w = 0; w < kW; ++w) M[h] = fmaxf(M[h], sml[w][h][0]);
+    L[h] = 0.f;
+    A[h] = 0.f;
+    for (int w = 0; w < kW; ++w) {
+      const float ms = sml[w][h][0];
+      const float f = ms == -INFINITY ? 0.f : exp2f(ms - M[h]);
+      L[h] += f * sml[w][h][1];
+      A[h] += f * sacc[w][h][tid];
+    }
+  }
+  if (n_splits == 1) {
+#pragma unroll
+    for (int h = 0; h < G; ++h)
+      p.out[(size_t)t * p.ldo + (h0 + h) * kAttnD + tid] = __float2bfloat16_rn(A[h] / L[h]);
+    return;
+  }
+  const size_t stride_g = kAttnD + 2;
+  float* mine = p.part + (((size_t)t * p.n_kv_heads + kvh) * p.max_splits + split) * G * stride_g;
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    mine[h * stride_g + 2 + tid] = A[h];
+    if (tid == 0) {
+      mine[h * stride_g] = M[h];
+      mine[h * stride_g + 1] = L[h];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    int32_t* cn = p.counters + (size_t)t * p.n_kv_heads + kvh;
+    s_last = atomicAdd(cn, 1) == n_splits - 1;
+    if (s_last) *cn = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const float* base = p.part + ((size_t)t * p.n_kv_heads + kvh) * p.max_splits * G * stride_g;
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float Mx = -INFINITY;
+    for (int s2 = 0; s2 < n_splits; ++s2) Mx = fmaxf(Mx, __ldcg(base + ((size_t)s2 * G + h) * stride_g));
+    float Ls = 0.f, As = 0.f;
+    for (int s2 = 0; s2 < n_splits; ++s2) {
+      const float* b = base + ((size_t)s2 * G + h) * stride_g;
+      const float f = exp2f(__ldcg(b) - Mx);
+      Ls += f * __ldcg(b + 1);
+      As += f * __ldcg(b + 2 + tid);
+    }
+    p.out[(size_t)t * p.ldo + (h0 + h) * kAttnD + tid] = __float2bfloat16_rn(As / Ls);
   }
 }
 

@@ -1085,6 +1085,10 @@ int collm_preload(void) {
   COLLM_PRELOAD(paged_attention_kernel<2>);
   COLLM_PRELOAD(paged_attention_kernel<4>);
   COLLM_PRELOAD(paged_attention_kernel<8>);
+  COLLM_PRELOAD(paged_attention_tc_kernel<1>);
+  COLLM_PRELOAD(paged_attention_tc_kernel<2>);
+  COLLM_PRELOAD(paged_attention_tc_kernel<4>);
+  COLLM_PRELOAD(paged_attention_tc_kernel<8>);
   COLLM_PRELOAD((cross_entropy_kernel<0, 256>));
 #undef COLLM_PRELOAD
   return COLLM_OK;
@@ -1356,6 +1360,33 @@ int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_h
   p.part = (float*)((char*)workspace + (((size_t)T * n_kv_heads * 4 + 255) & ~(size_t)255));
   const dim3 grid(T, n_kv_heads, p.max_splits);
   cudaStream_t st = (cudaStream_t)stream;
+  // GQA groups: the tensor-core variant (K/V feed the G heads through one MMA); G = 1 keeps the
+  // CUDA-core streams (COLLM_ATTN_TC=0/1 forces either for G >= 2 / all G)
+  static const int tc_env = [] { const char* e = getenv("COLLM_ATTN_TC"); return e ? atoi(e) : -1; }();
+  const int G = n_heads / n_kv_heads;
+  if ((tc_env < 0 && G >= 2) || (tc_env == 1 && G >= 1)) {
+    static bool configured[kMaxDevices][4] = {};
+    const int dev = cur_device(), gi = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : 3;
+    auto cfg_kernel = [&](auto kern) -> int {
+      std::lock_guard<std::mutex> lk(g_state_mu);
+      if (!configured[dev][gi]) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem));
+        configured[dev][gi] = true;
+      }
+      return COLLM_OK;
+    };
+    int rc = COLLM_OK;
+    switch (G) {
+      case 1: rc = cfg_kernel(paged_attention_tc_kernel<1>); if (!rc) paged_attention_tc_kernel<1><<<grid, kAttnThreads, kAttnTcSmem, st>>>(p); break;
+      case 2: rc = cfg_kernel(paged_attention_tc_kernel<2>); if (!rc) paged_attention_tc_kernel<2><<<grid, kAttnThreads, kAttnTcSmem, st>>>(p); break;
+      case 4: rc = cfg_kernel(paged_attention_tc_kernel<4>); if (!rc) paged_attention_tc_kernel<4><<<grid, kAttnThreads, kAttnTcSmem, st>>>(p); break;
+      case 8: rc = cfg_kernel(paged_attention_tc_kernel<8>); if (!rc) paged_attention_tc_kernel<8><<<grid, kAttnThreads, kAttnTcSmem, st>>>(p); break;
+      default: return fail(COLLM_EINVAL, "GQA group %d not in {1, 2, 4, 8}", G);
+    }
+    if (rc) return rc;
+    CUDA_TRY(cudaGetLastError());
+    return COLLM_OK;
+  }
   switch (n_heads / n_kv_heads) {
     case 1: paged_attention_kernel<1><<<grid, kAttnThreads, 0, st>>>(p); break;
     case 2: paged_attention_kernel<2><<<grid, kAttnThreads, 0, st>>>(p); break;
