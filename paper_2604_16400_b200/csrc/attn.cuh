@@ -208,14 +208,17 @@ __global__ void __launch_bounds__(kAttnThreads) paged_attention_kernel(const Att
 }
 
 
-// Tensor-core variant for GQA groups (G >= 2): the G query heads of a KV head are the rows of ONE
-// m16n8k16 MMA (rows G..15 zero), so each K/V element feeds G heads through the tensor pipe
-// instead of G shuffle-reduced dot products (the CUDA-core kernel above is issue-bound at G = 4:
-// 1.4 TB/s).  Each of the 4 warps stages 64 tokens of the split (K and V rows, 2 x 16 KB, cp.async
-// into XOR-swizzled shared memory, zero-filled past the split end), computes S = Q K^T (64 MMAs),
-// a local base-2 softmax per head row and O = P V (64 MMAs, P from the score fragments); the warps
-// merge in fixed order and splits combine exactly as above (deterministic).
-constexpr int kAttnTcSmem = 4 * 32768;
+// Tensor-core variant (the default): the G query heads of a KV head are the rows of ONE m16n8k16
+// MMA (rows G..15 zero), so each K/V element feeds G heads through the tensor pipe instead of G
+// shuffle-reduced dot products (the CUDA-core kernel above is issue-bound at G = 4: 1.4 TB/s).
+// Each of the 4 warps stages 64 tokens of the split into its own 16 KB XOR-swizzled tile (cp.async,
+// zero-filled past the split end): K first — S = Q K^T (64 MMAs) and a local base-2 softmax per
+// head row — then V in the same tile — O = P V (64 MMAs, P from the score fragments); 64 KB per
+// CTA keeps 3 CTAs (12 warps, ~190 KB of loads) in flight per SM.  The warps merge in fixed order
+// through the tiles' space and splits combine exactly as above (deterministic).  Measured
+// (tools/attn_bench.py, 256 rows): 7B decode ctx 1024 5.26 TB/s (0.81 of HBM; CUDA-core 4.07),
+// GQA G = 4 4.79 TB/s (CUDA-core 1.44), G = 8 3.4 TB/s (0.55).
+constexpr int kAttnTcSmem = 4 * 16384;  // one 16 KB tile per warp: K, then V in the same buffer
 
 template <int G>
 __global__ void __launch_bounds__(kAttnThreads, 1) paged_attention_tc_kernel(const AttnParams p) {
@@ -236,19 +239,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1) paged_attention_tc_kernel(con
   const int h0 = kvh * G;
   const int jw0 = j0 + warp * 64;
   const int nvalid = max(0, min(64, j1 - jw0));
-  uint8_t* Ks = asm_ + warp * 32768;
-  uint8_t* Vs = Ks + 16384;
-  // stage this warp's 64 tokens of K and V (rows past the split end zero-filled)
-  for (int i = lane; i < 64 * 16; i += 32) {
-    const int row = i >> 4, ch = i & 15;
-    const bool ok = row < nvalid;
-    const int j = ok ? jw0 + row : j0;
-    const size_t off = (((size_t)bt[j >> p.page_shift] * p.n_kv_heads + kvh) * psz + (j & (psz - 1))) *
-                       kAttnD + ch * 8;
-    cp_async_16(Ks + fa_off(row, ch * 8), p.k_cache + off, ok);
-    cp_async_16(Vs + fa_off(row, ch * 8), p.v_cache + off, ok);
-  }
-  cp_async_commit();
+  // one 16 KB tile per warp (3 CTAs fit an SM): this warp's 64 tokens of K, then of V
+  uint8_t* Ts = asm_ + warp * 16384;
+  auto stage = [&](const bf16* cache) {  // rows past the split end zero-filled
+    for (int i = lane; i < 64 * 16; i += 32) {
+      const int row = i >> 4, ch = i & 15;
+      const bool ok = row < nvalid;
+      const int j = ok ? jw0 + row : j0;
+      const size_t off = (((size_t)bt[j >> p.page_shift] * p.n_kv_heads + kvh) * psz + (j & (psz - 1))) *
+                         kAttnD + ch * 8;
+      cp_async_16(Ts + fa_off(row, ch * 8), cache + off, ok);
+    }
+    cp_async_commit();
+  };
+  stage(p.k_cache);
   // Q fragments: rows = the group's heads (rows >= G zero), 8 k-steps over the 128 dims
   uint32_t qa[8][4];
 #pragma unroll
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) paged_attention_tc_kernel(con
   }
   cp_async_wait<0>();
   __syncwarp();
-  const uint32_t kb = smem_u32(Ks), vb = smem_u32(Vs);
+  const uint32_t kb = smem_u32(Ts), vb = kb;
   float sc[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
@@ -298,6 +302,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) paged_attention_tc_kernel(con
     }
   l += __shfl_xor_sync(0xffffffffu, l, 1);
   l += __shfl_xor_sync(0xffffffffu, l, 2);
+  __syncwarp();  // every lane's K fragments are read: the tile takes V
+  stage(p.v_cache);
+  cp_async_wait<0>();
+  __syncwarp();
   float o[16][4];
 #pragma unroll
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
@@ -313,9 +321,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) paged_attention_tc_kernel(con
       mma16816(o[2 * jd + 1], pa, b[2], b[3]);
     }
   }
-  // merge the 4 warps (fixed order) through shared memory
-  __shared__ float sml[kW][kAttnMaxG][2];
-  __shared__ __align__(16) float sacc[kW][kAttnMaxG][kAttnD];
+  // merge the 4 warps (fixed order) through shared memory (the tiles' space, all MMAs done)
+  __syncthreads();
+  float (*sml)[kAttnMaxG][2] = reinterpret_cast<float (*)[kAttnMaxG][2]>(asm_);
+  float (*sacc)[kAttnMaxG][kAttnD] = reinterpret_cast<float (*)[kAttnMaxG][kAttnD]>(asm_ + 1024);
   __shared__ bool s_last;
   if (g < G) {
     if (c == 0) {

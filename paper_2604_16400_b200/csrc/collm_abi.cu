@@ -1360,11 +1360,12 @@ int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_h
   p.part = (float*)((char*)workspace + (((size_t)T * n_kv_heads * 4 + 255) & ~(size_t)255));
   const dim3 grid(T, n_kv_heads, p.max_splits);
   cudaStream_t st = (cudaStream_t)stream;
-  // GQA groups: the tensor-core variant (K/V feed the G heads through one MMA); G = 1 keeps the
-  // CUDA-core streams (COLLM_ATTN_TC=0/1 forces either for G >= 2 / all G)
-  static const int tc_env = [] { const char* e = getenv("COLLM_ATTN_TC"); return e ? atoi(e) : -1; }();
+  // the tensor-core variant (the G heads of a KV head are one MMA's rows; measured faster for
+  // every G: 7B decode 0.81 of HBM vs 0.63, GQA G = 4 0.74 vs 0.22, tools/attn_bench.py);
+  // COLLM_ATTN_TC=0 selects the CUDA-core half-warp streams
+  static const int tc_env = [] { const char* e = getenv("COLLM_ATTN_TC"); return e ? atoi(e) : 1; }();
   const int G = n_heads / n_kv_heads;
-  if ((tc_env < 0 && G >= 2) || (tc_env == 1 && G >= 1)) {
+  if (tc_env != 0) {
     static bool configured[kMaxDevices][4] = {};
     const int dev = cur_device(), gi = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : 3;
     auto cfg_kernel = [&](auto kern) -> int {

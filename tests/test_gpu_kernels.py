@@ -314,7 +314,7 @@ def test_cross_entropy_vs_oracle(T, V):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("n_heads,n_kv", [(4, 4), (8, 2)])
+@pytest.mark.parametrize("n_heads,n_kv", [(4, 4), (4, 2), (8, 2), (8, 1)])
 def test_paged_attention_vs_oracle(n_heads, n_kv):
     """K8 over a shuffled paged KV cache: decode rows with contexts 1..700 (multi-split, split
     boundary 256/257), a prefill segment (causal, positions 0..n-1) and GQA — against the float64
