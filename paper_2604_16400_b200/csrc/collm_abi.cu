@@ -672,7 +672,7 @@ static int flash_launch(void (*kernel)(const FlashParams), int smem, dim3 grid, 
   static std::mutex mu;
   static bool done[kMaxDevices][4] = {};
   const int dev = cur_device();
-  const int slot = smem == 81920 ? 0 : smem == 99840 ? 1 : 2;
+  const int slot = smem == 81920 ? 0 : smem == 99840 ? 1 : smem == 49152 ? 3 : 2;
   {
     std::lock_guard<std::mutex> lk(mu);
     if (!done[dev][slot]) {
@@ -696,7 +696,11 @@ int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, co
   p.out = (bf16*)out; p.ldo = ldo; p.lse = lse;
   if (stat_ld > 0) p.stat_ld = stat_ld;
   CHECK_ARG(p.stat_ld >= T, "stat_ld=%d < T=%d", p.stat_ld, T);
-  return flash_launch(flash_fwd_kernel, 81920, dim3((T + kFaBM - 1) / kFaBM, n_heads), p,
+  static const int st_env = [] { const char* e = getenv("COLLM_FA_STAGES"); return e ? atoi(e) : 1; }();
+  if (st_env == 2)
+    return flash_launch(flash_fwd_kernel<2>, 81920, dim3((T + kFaBM - 1) / kFaBM, n_heads), p,
+                        (cudaStream_t)stream);
+  return flash_launch(flash_fwd_kernel<1>, 49152, dim3((T + kFaBM - 1) / kFaBM, n_heads), p,
                       (cudaStream_t)stream);
 }
 
@@ -1051,7 +1055,8 @@ int collm_preload(void) {
   COLLM_PRELOAD((lora_shrink_kernel<6, 2>));
   COLLM_PRELOAD((lora_shrink_kernel<8, 2>));
   COLLM_PRELOAD(lora_shrink_tc_kernel);
-  COLLM_PRELOAD(flash_fwd_kernel);
+  COLLM_PRELOAD(flash_fwd_kernel<1>);
+  COLLM_PRELOAD(flash_fwd_kernel<2>);
   COLLM_PRELOAD(lora_expand_rows_kernel);
   COLLM_PRELOAD(flash_delta_kernel);
   COLLM_PRELOAD(flash_bwd_dkdv_kernel);

@@ -114,7 +114,10 @@ __device__ __forceinline__ void fa_c2a(uint32_t (&a)[4], const float (&c0)[4], c
 }
 
 // ----------------------------------------------------------------------------------- forward
-__global__ void __launch_bounds__(kFaThreads) flash_fwd_kernel(const FlashParams p) {
+// ST = 2: K/V double-buffered (80 KB, 2 CTAs/SM); ST = 1: one K/V stage (48 KB, 3 CTAs/SM —
+// other CTAs hide the load latency instead of the prefetch)
+template <int ST>
+__global__ void __launch_bounds__(kFaThreads, ST == 1 ? 3 : 2) flash_fwd_kernel(const FlashParams p) {
   extern __shared__ __align__(128) uint8_t fsm[];
   // packed tiling: a CTA takes 64 consecutive rows of the batch whatever their sequences; its
   // keys run from the first row's sequence start to its last row, masked per (query, key) by
@@ -125,8 +128,8 @@ __global__ void __launch_bounds__(kFaThreads) flash_fwd_kernel(const FlashParams
   const int hk = h / (p.n_heads / p.n_kv_heads);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   uint8_t* Qs = fsm;
-  uint8_t* Ks = fsm + 16384;   // [2] stages
-  uint8_t* Vs = fsm + 49152;   // [2] stages
+  uint8_t* Ks = fsm + 16384;                     // [ST] stages
+  uint8_t* Vs = fsm + 16384 + ST * 16384;         // [ST] stages
   const uint32_t qb = smem_u32(Qs), kb0 = smem_u32(Ks), vb0 = smem_u32(Vs);
   const int nq = min(kFaBM, p.T - q0);
   const int kstart = p.row_start[q0], kend = q0 + nq;
@@ -147,15 +150,25 @@ __global__ void __launch_bounds__(kFaThreads) flash_fwd_kernel(const FlashParams
   float m_i[2] = {-INFINITY, -INFINITY}, l_i[2] = {0.f, 0.f};
 
   for (int j = 0; j < n_kt; ++j) {
-    if (j + 1 < n_kt) {
-      const int kr = kstart + (j + 1) * kFaBM;
-      fa_load_tile(Ks + ((j + 1) & 1) * 16384, p.k, p.ldk, kr, min(kFaBM, kend - kr), hk * kFaD);
-      fa_load_tile(Vs + ((j + 1) & 1) * 16384, p.v, p.ldv, kr, min(kFaBM, kend - kr), hk * kFaD);
+    if constexpr (ST == 2) {
+      if (j + 1 < n_kt) {
+        const int kr = kstart + (j + 1) * kFaBM;
+        fa_load_tile(Ks + ((j + 1) & 1) * 16384, p.k, p.ldk, kr, min(kFaBM, kend - kr), hk * kFaD);
+        fa_load_tile(Vs + ((j + 1) & 1) * 16384, p.v, p.ldv, kr, min(kFaBM, kend - kr), hk * kFaD);
+      }
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      if (j > 0) {  // every warp is done with the previous tile (the loop-end barrier)
+        const int kr = kstart + j * kFaBM;
+        fa_load_tile(Ks, p.k, p.ldk, kr, min(kFaBM, kend - kr), hk * kFaD);
+        fa_load_tile(Vs, p.v, p.ldv, kr, min(kFaBM, kend - kr), hk * kFaD);
+        cp_async_commit();
+      }
+      cp_async_wait<0>();
     }
-    cp_async_commit();
-    cp_async_wait<1>();
     __syncthreads();
-    const uint32_t kb = kb0 + (j & 1) * 16384, vb = vb0 + (j & 1) * 16384;
+    const uint32_t kb = kb0 + (ST == 2 ? (j & 1) * 16384 : 0), vb = vb0 + (ST == 2 ? (j & 1) * 16384 : 0);
     float sc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
@@ -388,6 +401,7 @@ __global__ void __launch_bounds__(kFaThreads) flash_bwd_dkdv_kernel(const FlashP
 
 // dQ of 64 query rows of one head: over the key tiles up to the diagonal, P = exp2(scale_log2 *
 // Q K^T - lse), dP = dO V^T, dS = P (dP - delta), dQ += dS K (warp w owns queries 16w..16w+15).
+// (a single K/V stage with 3 CTAs/SM, which helps the forward, measured 4-13 % slower here)
 __global__ void __launch_bounds__(kFaThreads) flash_bwd_dq_kernel(const FlashParams p) {
   extern __shared__ __align__(128) uint8_t fsm[];
   const int h = blockIdx.y;
