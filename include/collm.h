@@ -249,7 +249,10 @@ int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_h
  * Sequences are row ranges of the mixed batch (training sequences, prefill segments, decode rows)
  * given per row: row_start[t] / row_end[t] (device int32 [T]) = first / one-past-last row of row
  * t's sequence (sequences contiguous and in row order); row t attends to rows [row_start[t], t].
- * CTAs take 64 consecutive rows (packed: short sequences share a tile).  q [T, ldq] (head h at columns h*128), k / v [T, ldk/ldv]
+ * Forward: by default the tcgen05/TMEM kernel (128 query rows per CTA: TMA-fed Q K^T and P V on
+ * the tensor core, S / O accumulators in TMEM, 8 softmax warps); collm_set_flash_impl(0) (or
+ * COLLM_FA_TC=0) selects the mma.sync kernel (64 rows per CTA).  Backward: mma.sync kernels.
+ * CTAs take consecutive rows (packed: short sequences share a tile).  q [T, ldq] (head h at columns h*128), k / v [T, ldk/ldv]
  * (kv head h/G), typically column blocks of the fused q|k|v projection output.  head_dim 128; GQA with n_heads a multiple of n_kv_heads.
  * fwd: out [T, ldo] bf16, lse [n_heads, stat_ld] fp32 = base-2 log-sum-exp of
  *      scale*log2(e)*scores (kept for the backward); stat_ld <= 0 means T.
@@ -258,6 +261,8 @@ int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_h
  *      of a group summed in a fixed order).  Deterministic: no atomics (dK/dV and dQ in separate
  *      kernels, each output element owned by one CTA).  fp32 softmax and accumulation.
  * Replaces: nothing in the reference (it has no attention); SURVEY §8(f) row 1. */
+int collm_set_flash_impl(int tc); /* 1 = tcgen05 forward (default), 0 = mma.sync */
+int collm_get_flash_impl(void);
 int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
                               void* out, int ldo, float* lse, int T, int n_heads, int n_kv_heads,
                               int head_dim, const int32_t* row_start, const int32_t* row_end,

@@ -22,6 +22,7 @@
 #include "shrink.cuh"
 #include "shrink_tc.cuh"
 #include "flash_attn.cuh"
+#include "flash_tc.cuh"
 #include "expand_rows.cuh"
 
 using namespace collm;
@@ -685,6 +686,18 @@ static int flash_launch(void (*kernel)(const FlashParams), int smem, dim3 grid, 
   return COLLM_OK;
 }
 
+static std::atomic<int> g_flash_impl{[] {
+  const char* e = getenv("COLLM_FA_TC");
+  return e ? atoi(e) : 1;
+}()};
+
+int collm_set_flash_impl(int tc) {
+  CHECK_ARG(tc == 0 || tc == 1, "flash impl %d (0 = mma.sync, 1 = tcgen05)", tc);
+  g_flash_impl.store(tc);
+  return COLLM_OK;
+}
+int collm_get_flash_impl(void) { return g_flash_impl.load(); }
+
 int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
                               void* out, int ldo, float* lse, int T, int n_heads, int n_kv_heads,
                               int head_dim, const int32_t* row_start, const int32_t* row_end,
@@ -696,6 +709,28 @@ int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, co
   p.out = (bf16*)out; p.ldo = ldo; p.lse = lse;
   if (stat_ld > 0) p.stat_ld = stat_ld;
   CHECK_ARG(p.stat_ld >= T, "stat_ld=%d < T=%d", p.stat_ld, T);
+  if (collm_get_flash_impl()) {  // the tcgen05/TMEM forward (flash_tc.cuh)
+    CHECK_ARG(ldq % 8 == 0 && ldk % 8 == 0 && ldv % 8 == 0, "x8 leading dimensions");
+    FlashTcMaps maps;
+    int rc = make_tmap(&maps.q, q, ldq, T, ldq, 64, 128);
+    if (!rc) rc = make_tmap(&maps.k, k, ldk, T, ldk, 64, 128);
+    if (!rc) rc = make_tmap(&maps.v, v, ldv, T, ldv, 64, 128);
+    if (rc) return rc;
+    static bool configured[kMaxDevices] = {};
+    const int dev = cur_device();
+    {
+      std::lock_guard<std::mutex> lk(g_state_mu);
+      if (!configured[dev]) {
+        CUDA_TRY(cudaFuncSetAttribute(flash_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      FlashTcSmem::kTotal));
+        configured[dev] = true;
+      }
+    }
+    flash_fwd_tc_kernel<<<dim3((T + kFtcRows - 1) / kFtcRows, n_heads), 384, FlashTcSmem::kTotal,
+                          (cudaStream_t)stream>>>(maps, p);
+    CUDA_TRY(cudaGetLastError());
+    return COLLM_OK;
+  }
   static const int st_env = [] { const char* e = getenv("COLLM_FA_STAGES"); return e ? atoi(e) : 1; }();
   if (st_env == 2)
     return flash_launch(flash_fwd_kernel<2>, 81920, dim3((T + kFaBM - 1) / kFaBM, n_heads), p,
@@ -1056,6 +1091,7 @@ int collm_preload(void) {
   COLLM_PRELOAD((lora_shrink_kernel<8, 2>));
   COLLM_PRELOAD(lora_shrink_tc_kernel);
   COLLM_PRELOAD(flash_fwd_kernel<1>);
+  COLLM_PRELOAD(flash_fwd_tc_kernel);
   COLLM_PRELOAD(flash_fwd_kernel<2>);
   COLLM_PRELOAD(lora_expand_rows_kernel);
   COLLM_PRELOAD(flash_delta_kernel);

@@ -152,6 +152,15 @@ def set_rank_sms(n: int, device: torch.device | None = None) -> None:
     _rank_sms[d] = int(n)
 
 
+def set_flash_impl(tc: int) -> None:
+    """K9 forward kernel: 1 = tcgen05/TMEM (default), 0 = mma.sync (collm_set_flash_impl)."""
+    _lib.call("collm_set_flash_impl", int(tc))
+
+
+def flash_impl() -> int:
+    return int(_lib.load().collm_get_flash_impl())
+
+
 def rank_sms(device: torch.device | None = None) -> int:
     d = (device or torch.device("cuda", torch.cuda.current_device())).index or 0
     if d not in _rank_sms:

@@ -361,8 +361,10 @@ def test_paged_attention_vs_oracle(n_heads, n_kv):
 
 @pytest.mark.parametrize("lens,n_heads,n_kv", [([512], 4, 4), ([1, 63, 64, 65, 200], 4, 2),
                                                ([130, 7, 300], 8, 2), ([1024], 2, 1),
-                                               ([1] * 40 + [3, 17, 90] + [1] * 30, 4, 1)])
-def test_flash_attention_vs_oracle(lens, n_heads, n_kv):
+                                               ([1] * 40 + [3, 17, 90] + [1] * 30, 4, 1),
+                                               ([129, 1, 255, 384, 2], 4, 4)])
+@pytest.mark.parametrize("impl", [1, 0], ids=["tcgen05", "mma"])
+def test_flash_attention_vs_oracle(lens, n_heads, n_kv, impl):
     """K9: causal attention of packed sequences (ragged lengths incl. 1, tile boundaries 63/64/65,
     many 1-row decode sequences sharing tiles with short prefills, GQA G = 1/2/4) forward + backward against the float64 oracle; q/k/v are column views of one
     fused q|k|v buffer as in the step; the backward is bitwise repeatable."""
@@ -381,7 +383,12 @@ def test_flash_attention_vs_oracle(lens, n_heads, n_kv):
     lse = torch.zeros(n_heads, T, device="cuda")
     rows = ops.seq_rows(seq, "cuda")
     kw = dict(T=T, n_heads=n_heads, n_kv_heads=n_kv)
-    ops.flash_attention(q, k, v, out, lse, *rows, **kw)
+    prev = ops.flash_impl()
+    ops.set_flash_impl(impl)
+    try:
+        ops.flash_attention(q, k, v, out, lse, *rows, **kw)
+    finally:
+        ops.set_flash_impl(prev)
     dqkv = torch.zeros_like(qkv)
     dq, dk, dv = dqkv[:, :n_heads * D], dqkv[:, n_heads * D:(n_heads + n_kv) * D], dqkv[:, (n_heads + n_kv) * D:]
     delta = torch.zeros(n_heads, T, device="cuda")
