@@ -216,7 +216,14 @@ typedef struct {
  * an AdamW step on master/m/v (PyTorch semantics) and the bf16 copies are rewritten.  `adamw` is
  * a DEVICE pointer to 7 floats {lr, beta1, beta2, eps, weight_decay, 1-beta1^step, 1-beta2^step}
  * so a captured CUDA graph can be replayed with a changing step.  Deterministic (split-T partials
- * reduced in a fixed order by the last-arriving CTA). */
+ * reduced in a fixed order by the last-arriving CTA).
+ * Kernel: by default the persistent TMA -> tcgen05.mma -> TMEM stream (one CTA per SM, units of
+ * 128 P rows x a range of 128-row T chunks, T split into at most `tsplit` parts of whole chunks,
+ * accumulators double-buffered in TMEM so the AdamW finalize overlaps the next unit's stream);
+ * collm_set_reduce_impl(0) (or COLLM_K5_TC=0) selects the mma.sync kernel (32-row T chunks), which
+ * also serves launches with more than 40 distinct U / V tensors. */
+int collm_set_reduce_impl(int tc); /* 1 = tcgen05 (default), 0 = mma.sync */
+int collm_get_reduce_impl(void);
 size_t collm_reduce_workspace_bytes(const collm_reduce_group* groups, int n_groups, int tsplit);
 int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int mode,
                       int accum_in, float grad_scale, const float* adamw, int tsplit,

@@ -54,6 +54,8 @@ SIGNATURES: dict[str, tuple] = {
     "collm_get_rank_sms": (_I, []),
     "collm_set_flash_impl": (_I, [_I]),
     "collm_get_flash_impl": (_I, []),
+    "collm_set_reduce_impl": (_I, [_I]),
+    "collm_get_reduce_impl": (_I, []),
     "collm_plan_shrink_windows": (_I, [_IP, _I, _I, _I, _IP, _I, _IP, _IP]),
     "collm_shrink_tc_workspace_bytes": (_SZ, [_I, _I]),
     "collm_lora_shrink_tc": (_I, [_P, _I, _I, _P, _LL, _I, _I, _P, _P, _I, _I, _P, _P, _IP, _I,

@@ -24,6 +24,7 @@
 #include "flash_attn.cuh"
 #include "flash_tc.cuh"
 #include "expand_rows.cuh"
+#include "reduce_tc.cuh"
 
 using namespace collm;
 
@@ -1285,7 +1286,75 @@ static int launch_reduce(ReduceParams& p, cudaStream_t st) {
   return COLLM_OK;
 }
 
+// K5 on the tensor core (reduce_tc.cuh), used when every operand can be viewed through a TMA map
+// (<= kRtcMaxMaps distinct U / V / V2 tensors); returns 1 when the launch is not possible.
+static std::atomic<int> g_reduce_impl{[] {
+  const char* e = getenv("COLLM_K5_TC");
+  return e ? atoi(e) : 1;
+}()};
+
+static int launch_reduce_tc(const ReduceParams& p, cudaStream_t st, bool* launched) {
+  *launched = false;
+  ReduceTcMaps maps;
+  ReduceTcParams tp;
+  const void* map_ptr[kRtcMaxMaps];
+  int map_ld[kRtcMaxMaps];
+  int n_maps = 0;
+  auto map_of = [&](const void* ptr, int ld) -> int {
+    for (int i = 0; i < n_maps; ++i)
+      if (map_ptr[i] == ptr && map_ld[i] == ld) return i;
+    if (n_maps == kRtcMaxMaps) return -1;
+    if (make_tmap(&maps.m[n_maps], ptr, (uint64_t)ld, (uint64_t)p.T, (uint64_t)ld, 64, kRtcRows))
+      return -2;
+    map_ptr[n_maps] = ptr;
+    map_ld[n_maps] = ld;
+    return n_maps++;
+  };
+  for (int g = 0; g < p.n_groups; ++g) {
+    const ReduceGroup& gr = p.groups[g];
+    if (gr.Q > 64) return COLLM_OK;
+    const int iu = map_of(gr.U, gr.ldu), iv = map_of(gr.V, gr.ldv);
+    const int iv2 = gr.V2 ? map_of(gr.V2, gr.ldv) : -3;
+    if (iu == -2 || iv == -2 || iv2 == -2) return COLLM_ECUDA;  // encode failure: error set
+    if (iu < 0 || iv < 0 || iv2 == -1) return COLLM_OK;         // too many tensors: mma.sync path
+    tp.map_u[g] = (int8_t)iu;
+    tp.map_v[g] = (int8_t)iv;
+    tp.map_v2[g] = (int8_t)(gr.V2 ? iv2 : -1);
+  }
+  tp.r = p;
+  tp.n_maps = n_maps;
+  static const int no_mma = [] { const char* e = getenv("COLLM_DEBUG_K5_NO_MMA"); return e ? atoi(e) : 0; }();
+  tp.debug_no_mma = no_mma;
+  tp.n_chunks = (p.T + kRtcRows - 1) / kRtcRows;
+  const int ts = std::max(1, std::min(p.tsplit, tp.n_chunks));
+  tp.per = (tp.n_chunks + ts - 1) / ts;
+  tp.r.tsplit = (tp.n_chunks + tp.per - 1) / tp.per;  // no empty parts; <= the caller's split
+  tp.n_units = p.n_tiles * tp.r.tsplit;
+  static bool configured[kMaxDevices] = {};
+  const int dev = cur_device();
+  {
+    std::lock_guard<std::mutex> lk(g_state_mu);
+    if (!configured[dev]) {
+      CUDA_TRY(cudaFuncSetAttribute(lora_reduce_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    ReduceTcSmem::kTotal));
+      configured[dev] = true;
+    }
+  }
+  const int grid = std::min(tp.n_units, num_sms_cached());
+  lora_reduce_tc_kernel<<<grid, 256, ReduceTcSmem::kTotal, st>>>(maps, tp);
+  CUDA_TRY(cudaGetLastError());
+  *launched = true;
+  return COLLM_OK;
+}
+
 extern "C" {
+
+int collm_set_reduce_impl(int tc) {
+  CHECK_ARG(tc == 0 || tc == 1, "reduce impl %d (0 = mma.sync, 1 = tcgen05)", tc);
+  g_reduce_impl.store(tc);
+  return COLLM_OK;
+}
+int collm_get_reduce_impl(void) { return g_reduce_impl.load(); }
 
 int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int mode,
                       int accum_in, float grad_scale, const float* adamw, int tsplit,
@@ -1315,6 +1384,11 @@ int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int
     p.partials = (float*)((char*)workspace + kCounterBytes);
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if (g_reduce_impl.load()) {
+    bool launched = false;
+    rc = launch_reduce_tc(p, st, &launched);
+    if (rc || launched) return rc;
+  }
   static const int minb = [] { const char* e = getenv("COLLM_K5_MINB"); return e ? atoi(e) : 4; }();
   // 64-wide tiles (r = 64 dB, 64-rank dA chunks: each U = dY / X_tr read once per ABI group
   // instead of twice) carry 32 accumulators per thread: 3 CTAs/SM register budget

@@ -52,12 +52,6 @@ __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// MN-major SWIZZLE_128B operand descriptor: 64-element (128 B) rows along MN, 8-row atoms along
-// K (SBO = 1024 B), the next 64 MN elements `lbo` bytes further.
-__device__ __forceinline__ uint64_t umma_desc_mnmajor(uint32_t smem_addr, uint32_t lbo) {
-  return (uint64_t)((smem_addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

@@ -280,7 +280,32 @@ def lora_expand_rows(Y: torch.Tensor, H16: torch.Tensor, B: torch.Tensor, row_ad
               _lib.int_array(sub_h_col) if sub_h_col else None, _stream())
 
 
+def set_reduce_impl(tc: int) -> None:
+    """K5 kernel: 1 = TMA + tcgen05 stream (default), 0 = mma.sync (collm_set_reduce_impl)."""
+    _lib.call("collm_set_reduce_impl", int(tc))
+
+
+def reduce_impl() -> int:
+    return int(_lib.load().collm_get_reduce_impl())
+
+
 def reduce_tsplit(T: int, n_tiles: int, device: torch.device) -> int:
+    if reduce_impl():
+        # persistent, one CTA per SM: ~8 units per CTA keeps the static share balanced; parts are
+        # whole 128-row chunks
+        # (static share per CTA balanced to within ~8 %; parts of >= 8 whole 128-row chunks, so
+        # the partial round trip stays small next to the stream)
+        chunks, sms = math.ceil(T / 128), num_sms(device)
+        env = __import__("os").environ.get("COLLM_K5_TSPLIT")
+        if env:
+            return max(1, min(int(env), chunks))
+        for ts in range(1, 129):
+            if chunks < 8 * ts:
+                break
+            units = n_tiles * ts / sms
+            if math.ceil(units) <= 1.08 * units:
+                return ts
+        return 1
     # one wave: the kernel keeps 3 CTAs/SM resident; keep >= 3 32-row chunks per split
     chunks = math.ceil(T / 32)
     want = (3 * num_sms(device)) // max(1, n_tiles)

@@ -234,7 +234,49 @@ def test_shrink_tc(R, K, n_ctas, dh, n_ad):
                 assert torch.equal(got, want), (t, sl)
 
 
-def test_reduce_adamw():
+@pytest.fixture(params=[1, 0], ids=["tcgen05", "mma"])
+def reduce_impl(request):
+    from paper_2604_16400_b200 import ops
+    prev = ops.reduce_impl()
+    ops.set_reduce_impl(request.param)
+    yield request.param
+    ops.set_reduce_impl(prev)
+
+
+@pytest.mark.parametrize("T,P,Q,tsplit,v2,accum", [
+    (1, 64, 16, 1, False, False), (300, 200, 48, 1, True, False), (513, 384, 8, 4, False, True),
+    (1000, 128, 64, 8, True, True), (4096, 256, 24, 2, True, False), (129, 520, 40, 2, False, False)])
+def test_reduce_store_grad_vs_fp32(reduce_impl, T, P, Q, tsplit, v2, accum):
+    """K5 grad mode against fp32 torch: ragged T (1, 129, 513 — not whole 128-row chunks), P not
+    a multiple of the 128-row tile, Q not a multiple of 16, the V2 (bf16 lo half) operand,
+    accumulation into an existing grad, T splits; a second launch is bitwise identical."""
+    from paper_2604_16400_b200 import _lib, ops
+    g = torch.Generator().manual_seed(T + P + Q)
+    U = _bf(T, P + 16, gen=g)
+    V = _bf(T, Q + 24, gen=g)
+    V2 = (_bf(T, Q + 24, gen=g).float() * 1e-3).to(torch.bfloat16) if v2 else None
+    init = torch.randn(P, Q + 4, generator=g).cuda()
+    outs = []
+    for _ in range(2):
+        grad = init.clone() if accum else torch.zeros(P, Q + 4, device="cuda")
+        grp = ops.reduce_group(U, V, u_off=16, P=P, v_off=8, Q=Q, ldc=Q + 4, c_col_off=4, grad=grad,
+                               V2=V2)
+        ops.lora_reduce(T, [grp], _lib.MODE_STORE_GRAD, accum_in=accum, grad_scale=0.5,
+                        tsplit=tsplit)
+        torch.cuda.synchronize()
+        outs.append(grad)
+    Vf = V[:, 8:8 + Q].float() + (V2[:, 8:8 + Q].float() if v2 else 0)
+    ref = 0.5 * U[:, 16:16 + P].float().t() @ Vf
+    got = outs[0][:, 4:]
+    if accum:
+        ref = ref + init[:, 4:]
+    assert torch.equal(outs[0][:, :4], init[:, :4] if accum else torch.zeros_like(init[:, :4]))
+    rel = ((got - ref).norm() / ref.norm()).item()
+    assert rel < 1e-5, rel
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_reduce_adamw(reduce_impl):
     from paper_2604_16400_b200 import _lib, ops
     g = torch.Generator().manual_seed(5)
     T, P, Q = 300, 200, 48
