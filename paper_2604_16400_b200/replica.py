@@ -267,6 +267,14 @@ class ReplicaStack:
             p.apply_optimizer(self.opt)
 
     # ------------------------------------------------------------------ plans
+    def _shrink_tc_ctas(self) -> tuple[int | None, int | None]:
+        """CTAs of the K1' (TMA + tcgen05) shrink for the forward and the dH pass: the rank-space
+        partition when one is set (None: DevicePlan takes collm_get_rank_sms), else the
+        whole-GPU override COLLM_SHRINK_TC_FWD / COLLM_SHRINK_TC_DH (0 = the mma.sync K1)."""
+        env = os.environ
+        return tuple(int(env[k]) if env.get(k) else None
+                     for k in ("COLLM_SHRINK_TC_FWD", "COLLM_SHRINK_TC_DH"))
+
     def plan(self, train: TrainItem | None, items: list[InferenceItem]) -> StepPlan:
         for it in items:
             if it.adapter >= self.cfg.n_adapters:
@@ -275,7 +283,8 @@ class ReplicaStack:
                     f"(n_adapters={self.cfg.n_adapters})")
         mb = build_mixed_batch(train, items)
         hp = plan_segments(mb.seg_start, mb.seg_adapter)
-        dp = DevicePlan(hp, self.device, expand=False)
+        fwd_ctas, dh_ctas = self._shrink_tc_ctas()
+        dp = DevicePlan(hp, self.device, expand=False, tc_ctas=fwd_ctas)
         th = td = None
         if mb.n_train_rows:
             if mb.train_adapter != self.train_slot:
@@ -283,7 +292,7 @@ class ReplicaStack:
                     f"training rows use adapter {mb.train_adapter}, the replica trains "
                     f"{self.train_slot}")
             th = uniform_plan(mb.n_train_rows, mb.train_adapter)
-            td = DevicePlan(th, self.device)
+            td = DevicePlan(th, self.device, tc_ctas=dh_ctas)
         sp = StepPlan(mb, hp, dp, th, td)
         if self.attention:
             # sequences: training sequences of seq_len rows, then maximal runs of one request

@@ -114,6 +114,7 @@ def plan_segments(seg_start, seg_adapter) -> HostPlan:
     return HostPlan(ss, sa, tsp, slots[: ns.value].copy(), tiles[: nt.value].copy())
 
 
+SHRINK_TC_MIN_ROWS = int(os.environ.get("COLLM_SHRINK_TC_MIN_ROWS", "4096"))
 TC_RANKS = (16, 32, 48, 64, 96, 128, 192, 256)  # group widths the K1' units are planned for
 
 
@@ -148,9 +149,17 @@ class DevicePlan:
         self.n_rows = int(host.seg_start[-1])
         self.n_tiles_m = (self.n_rows + TILE_M - 1) // TILE_M
         dev = torch.device(device)
-        if tc_ctas is None:  # the rank-space partition of this device (collm_set_rank_sms)
+        if tc_ctas is None:
+            # the rank-space partition of this device (collm_set_rank_sms); without one, passes of
+            # >= SHRINK_TC_MIN_ROWS rows take K1' on the whole GPU (the TMA + tcgen05 shrink
+            # streams the large X near HBM rate; small passes are MMA-latency-bound there and
+            # keep the mma.sync K1)
             from . import ops
-            tc_ctas = ops.rank_sms(dev) if dev.type == "cuda" else 0
+            tc_ctas = 0
+            if dev.type == "cuda":
+                tc_ctas = ops.rank_sms(dev)
+                if not tc_ctas and self.n_rows >= SHRINK_TC_MIN_ROWS:
+                    tc_ctas = ops.num_sms(dev) // 2 * 2
         self.tc_ctas = int(tc_ctas)
         # K1' units per group width (the rank-space partition, collm_set_rank_sms)
         tc_plans = [plan_shrink_windows(host, nr, self.tc_ctas) for nr in TC_RANKS] \

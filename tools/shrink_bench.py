@@ -11,11 +11,11 @@ from paper_2604_16400_b200.configs import CONFIGS  # noqa: E402
 
 cfg = CONFIGS[os.environ.get("CFG", "llama2-7b")]
 TC = int(os.environ.get("TC", "0"))  # rank-space partition size: collm_lora_shrink_tc
-if TC:
+if TC and TC <= 64:
     ops.set_rank_sms(TC)
 mb = segments.build_mixed_batch(*cfg.batch(0))
-plan = segments.DevicePlan(segments.plan_segments(mb.seg_start, mb.seg_adapter))
-tplan = segments.DevicePlan(segments.uniform_plan(mb.n_train_rows, mb.train_adapter))
+plan = segments.DevicePlan(segments.plan_segments(mb.seg_start, mb.seg_adapter), tc_ctas=TC)
+tplan = segments.DevicePlan(segments.uniform_plan(mb.n_train_rows, mb.train_adapter), tc_ctas=TC)
 T, Ttr = mb.n_rows, mb.n_train_rows
 scale = torch.full((cfg.n_adapters,), 2.0, device="cuda")
 res = []
