@@ -23,6 +23,7 @@
 #include "shrink_tc.cuh"
 #include "flash_attn.cuh"
 #include "flash_tc.cuh"
+#include "flash_bwd_tc.cuh"
 #include "expand_rows.cuh"
 #include "reduce_tc.cuh"
 
@@ -763,6 +764,38 @@ int collm_flash_attention_bwd(const void* q, int ldq, const void* k, int ldk, co
   const int warps = T * n_heads;
   flash_delta_kernel<<<(warps + 7) / 8, 256, 0, st>>>(p);
   CUDA_TRY(cudaGetLastError());
+  if (collm_get_flash_impl() && lddq % 8 == 0 && lddk % 8 == 0 && lddv % 8 == 0 && aligned16(dq) &&
+      aligned16(dk) && aligned16(dv)) {
+    // tcgen05/TMEM backward (flash_bwd_tc.cuh)
+    FlashBwdTcMaps maps;
+    int rc2 = make_tmap(&maps.q64, q, ldq, T, ldq, 64, 64);
+    if (!rc2) rc2 = make_tmap(&maps.o64, dout, lddo, T, lddo, 64, 64);
+    if (!rc2) rc2 = make_tmap(&maps.k128, k, ldk, T, ldk, 64, 128);
+    if (!rc2) rc2 = make_tmap(&maps.v128, v, ldv, T, ldv, 64, 128);
+    if (!rc2) rc2 = make_tmap(&maps.q128, q, ldq, T, ldq, 64, 128);
+    if (!rc2) rc2 = make_tmap(&maps.o128, dout, lddo, T, lddo, 64, 128);
+    if (!rc2) rc2 = make_tmap(&maps.k64, k, ldk, T, ldk, 64, 64);
+    if (!rc2) rc2 = make_tmap(&maps.v64, v, ldv, T, ldv, 64, 64);
+    if (rc2) return rc2;
+    static bool configured[kMaxDevices] = {};
+    const int dev = cur_device();
+    {
+      std::lock_guard<std::mutex> lk(g_state_mu);
+      if (!configured[dev]) {
+        CUDA_TRY(cudaFuncSetAttribute(flash_bwd_dkdv_tc_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, FbDkdvSmem::kTotal));
+        CUDA_TRY(cudaFuncSetAttribute(flash_bwd_dq_tc_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, FbDqSmem::kTotal));
+        configured[dev] = true;
+      }
+    }
+    const int t128 = (T + 127) / 128;
+    flash_bwd_dkdv_tc_kernel<<<dim3(t128, n_kv_heads), 384, FbDkdvSmem::kTotal, st>>>(maps, p);
+    CUDA_TRY(cudaGetLastError());
+    flash_bwd_dq_tc_kernel<<<dim3(t128, n_heads), 384, FbDqSmem::kTotal, st>>>(maps, p);
+    CUDA_TRY(cudaGetLastError());
+    return COLLM_OK;
+  }
   const int tiles = (T + kFaBM - 1) / kFaBM;
   rc = flash_launch(flash_bwd_dkdv_kernel, 99840, dim3(tiles, n_kv_heads), p, st);
   if (rc) return rc;

@@ -1,0 +1,439 @@
+// flash_bwd_tc.cuh — K9 backward on tcgen05/TMEM (the training sequences' attention gradients).
+//
+// Same contract and math as flash_bwd_dkdv_kernel / flash_bwd_dq_kernel (flash_attn.cuh): P is
+// recomputed from the forward's base-2 LSE, delta = rowsum(dO o O) (flash_delta_kernel),
+// dS = P (dP - delta), dV = P^T dO, dK = scale dS^T Q, dQ = scale dS K; every output element is
+// owned by one CTA and accumulated in a fixed order (no atomics: bitwise repeatable).
+//
+// dK/dV kernel — CTA = 128 keys x one kv head; loops over the G query heads of the group and the
+// 64-query steps from the first key to the last key's sequence end.  Per step:
+//   S^T  = K Q^T    tcgen05.mma M = 128 keys x N = 64 queries x K = 128 dims (A = K, B = Q, K-major)
+//   dP^T = V dO^T   same shape (A = V, B = dO)            -> TMEM, double-buffered (next step's
+//                                                            MMAs overlap this step's elementwise)
+//   8 elementwise warps (thread = 32 queries of one key row): P^T = exp2(S^T c - lse[q]) masked
+//   (k <= q < row_end[k]), dS^T = P^T (dP^T - delta[q]), both bf16 into K-major swizzled tiles;
+//   dV  += P^T dO   M = 128 keys x N = 128 dims x K = 64 queries (B = dO MN-major)
+//   dK  += dS^T Q   same (B = Q MN-major)                -> TMEM accumulators for the whole loop.
+// Q / dO steps stream through a 2-stage TMA ring; warp 3 stages the step's lse / delta.
+//
+// dQ kernel — CTA = 128 queries x one head; loops over 64-key steps from the first row's
+// sequence start to the tile's last row:
+//   S = Q K^T, dP = dO V^T (M = 128 queries x N = 64 keys), dS = P (dP - delta) per query row,
+//   dQ += dS K (N = 128 dims, B = K MN-major) in TMEM.
+//
+// Roles (384 threads, 1 CTA/SM): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator,
+// warp 3 statistics (dK/dV), warps 4-11 elementwise + epilogue (warps w and w+4 share a TMEM
+// lane quarter and take the two 32-column halves of a step).
+#pragma once
+#include "common.cuh"
+#include "flash_attn.cuh"
+#include "flash_tc.cuh"
+
+namespace collm {
+
+constexpr uint32_t kFbBox64 = 64 * 128;    // [64 rows][64 dims] bf16 TMA box, 8 KB
+constexpr uint32_t kFbBox128 = 128 * 128;  // [128 rows][64 dims] bf16 TMA box, 16 KB
+
+struct FlashBwdTcMaps {
+  CUtensorMap q64, o64, k128, v128;  // dK/dV kernel: Q / dO steps of 64 rows, K / V tiles of 128
+  CUtensorMap q128, o128, k64, v64;  // dQ kernel: Q / dO tiles of 128 rows, K / V steps of 64
+};
+
+struct FbDkdvSmem {
+  static constexpr uint32_t kK = 0;                   // 2 boxes [128 keys][64 dims]
+  static constexpr uint32_t kV = 2 * kFbBox128;
+  static constexpr uint32_t kQO = 4 * kFbBox128;      // [2 stages] Q (2 boxes), dO (2 boxes)
+  static constexpr uint32_t kPS = kQO + 2 * 4 * kFbBox64;  // [2] P^T tile, dS^T tile [128][64]
+  static constexpr uint32_t kStat = kPS + 2 * 2 * kFbBox128;  // [2 stages][lse 64 | delta 64]
+  static constexpr uint32_t kBar = kStat + 2 * 128 * 4;
+  static constexpr uint32_t kTotal = kBar + 256 + 1024;
+};
+
+struct FbDqSmem {
+  static constexpr uint32_t kQ = 0;                    // 2 boxes [128 q][64 dims]
+  static constexpr uint32_t kO = 2 * kFbBox128;        // dO
+  static constexpr uint32_t kKV = 4 * kFbBox128;       // [2 stages] K (2 boxes [64][64]), V
+  static constexpr uint32_t kS = kKV + 2 * 4 * kFbBox64;  // [2] dS tile [128 q][64 keys]
+  static constexpr uint32_t kBar = kS + 2 * kFbBox128;
+  static constexpr uint32_t kTotal = kBar + 256 + 1024;
+};
+
+// 32 bf16 (this thread's 32 columns of a 64-column K-major SWIZZLE_128B row) into its row
+__device__ __forceinline__ void fb_store_row32(uint8_t* tile, int row, int half, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int piece = half * 4 + i;
+    *reinterpret_cast<uint4*>(tile + row * 128 + ((piece ^ (row & 7)) << 4)) =
+        make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                   pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+  }
+}
+
+// write 64 fp32 accumulator columns [c0, c0+64) of TMEM row `lane_base` to bf16 dst, times mul
+__device__ __forceinline__ void fb_store_acc64(uint32_t taddr, bf16* dst, float mul, bool ok) {
+#pragma unroll
+  for (int ch = 0; ch < 2; ++ch) {
+    uint32_t o[32];
+    tmem_ld_32x32b_x32(taddr + ch * 32, o);
+    tmem_wait_ld();
+    if (ok) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 8)
+        *reinterpret_cast<uint4*>(dst + ch * 32 + e) =
+            make_uint4(pack_bf16x2(__uint_as_float(o[e]) * mul, __uint_as_float(o[e + 1]) * mul),
+                       pack_bf16x2(__uint_as_float(o[e + 2]) * mul, __uint_as_float(o[e + 3]) * mul),
+                       pack_bf16x2(__uint_as_float(o[e + 4]) * mul, __uint_as_float(o[e + 5]) * mul),
+                       pack_bf16x2(__uint_as_float(o[e + 6]) * mul, __uint_as_float(o[e + 7]) * mul));
+    }
+  }
+}
+
+// ================================================================== dK / dV
+__global__ void __launch_bounds__(384, 1)
+    flash_bwd_dkdv_tc_kernel(const __grid_constant__ FlashBwdTcMaps maps, const FlashParams p) {
+  using L = FbDkdvSmem;
+  extern __shared__ uint8_t fbraw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fbraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* kv_full = bar;        // K, V tiles loaded
+  uint64_t* qd_full = bar + 1;    // [2] Q / dO step + its lse / delta staged
+  uint64_t* s_full = bar + 3;     // [2] S^T, dP^T of the step in TMEM buffer b
+  uint64_t* s_free = bar + 5;     // [2] elementwise warps done reading TMEM buffer b
+  uint64_t* p_full = bar + 7;     // [2] P^T / dS^T tiles b written
+  uint64_t* mm_done = bar + 9;    // [2] dV / dK MMAs of the step done (stage + tiles b free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+
+  const int hk = blockIdx.y;
+  const int k0 = (gridDim.x - 1 - blockIdx.x) * 128;  // long (early-key) tiles first
+  if (k0 >= p.T) return;
+  const int G = p.n_heads / p.n_kv_heads;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = min(128, p.T - k0);
+  const int qend = p.row_end[k0 + nk - 1];  // queries that see these keys: [k0, qend)
+  const int per_head = (qend - k0 + 63) / 64, total = G * per_head;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&qd_full[b], 2);
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 8);
+      mbar_init(&p_full[b], 8);
+      mbar_init(&mm_done[b], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512, 1>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S^T [0,128), dP^T [128,256), dV [256,384), dK [384,512)
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (elect_one()) {
+      tma_prefetch_desc(&maps.q64);
+      tma_prefetch_desc(&maps.o64);
+      mbar_arrive_expect_tx(kv_full, 4 * kFbBox128);
+      tma_load_2d(smem + L::kK, &maps.k128, kv_full, hk * kFaD, k0);
+      tma_load_2d(smem + L::kK + kFbBox128, &maps.k128, kv_full, hk * kFaD + 64, k0);
+      tma_load_2d(smem + L::kV, &maps.v128, kv_full, hk * kFaD, k0);
+      tma_load_2d(smem + L::kV + kFbBox128, &maps.v128, kv_full, hk * kFaD + 64, k0);
+      for (int it = 0; it < total; ++it) {
+        const int s = it & 1;
+        if (it >= 2) ftc_wait(&mm_done[s], ((it >> 1) - 1) & 1, 21, it);
+        const int hq = hk * G + it / per_head, qr = k0 + (it % per_head) * 64;
+        uint8_t* st = smem + L::kQO + s * 4 * kFbBox64;
+        mbar_arrive_expect_tx(&qd_full[s], 4 * kFbBox64);
+        tma_load_2d(st, &maps.q64, &qd_full[s], hq * kFaD, qr);
+        tma_load_2d(st + kFbBox64, &maps.q64, &qd_full[s], hq * kFaD + 64, qr);
+        tma_load_2d(st + 2 * kFbBox64, &maps.o64, &qd_full[s], hq * kFaD, qr);
+        tma_load_2d(st + 3 * kFbBox64, &maps.o64, &qd_full[s], hq * kFaD + 64, qr);
+      }
+    }
+  } else if (warp == 3) {
+    // ===================== statistics of each step: lse, delta of its 64 queries =====================
+    for (int it = 0; it < total; ++it) {
+      const int s = it & 1;
+      if (it >= 2) ftc_wait(&mm_done[s], ((it >> 1) - 1) & 1, 22, it);
+      const int hq = hk * G + it / per_head, qr = k0 + (it % per_head) * 64;
+      float* stat = reinterpret_cast<float*>(smem + L::kStat) + s * 128;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int q = qr + h2 * 32 + lane;
+        const bool ok = q < qend;
+        stat[h2 * 32 + lane] = ok ? p.lse[(size_t)hq * p.stat_ld + q] : 0.f;
+        stat[64 + h2 * 32 + lane] = ok ? p.delta[(size_t)hq * p.stat_ld + q] : 0.f;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qd_full[s]);
+    }
+  } else if (warp == 1) {
+    // ===================== tcgen05.mma issuer =====================
+    const uint32_t idesc_s = umma_idesc_bf16(128, 64);
+    const uint32_t idesc_g = umma_idesc_bf16(128, 128) | (1u << 16);  // B (dO / Q) MN-major
+    const uint32_t sk = smem_u32(smem + L::kK), sv = smem_u32(smem + L::kV);
+    ftc_wait(kv_full, 0, 23, 0);
+    auto issue_s = [&](int j) {
+      const int s = j & 1;
+      ftc_wait(&qd_full[s], (j >> 1) & 1, 24, j);
+      if (j >= 2) ftc_wait(&s_free[s], ((j >> 1) - 1) & 1, 25, j);
+      tc_fence_after();
+      const uint32_t sq = smem_u32(smem + L::kQO + s * 4 * kFbBox64), so = sq + 2 * kFbBox64;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t offa = (kk >> 2) * kFbBox128 + (kk & 3) * 32;
+          const uint32_t offb = (kk >> 2) * kFbBox64 + (kk & 3) * 32;
+          umma_bf16(tmem + s * 64, umma_desc_kmajor(sk + offa, 128), umma_desc_kmajor(sq + offb, 128),
+                    idesc_s, kk ? 1u : 0u);
+          umma_bf16(tmem + 128 + s * 64, umma_desc_kmajor(sv + offa, 128),
+                    umma_desc_kmajor(so + offb, 128), idesc_s, kk ? 1u : 0u);
+        }
+        umma_commit(&s_full[s]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < total; ++j) {
+      if (j + 1 < total) issue_s(j + 1);  // the next step's scores overlap this step's elementwise
+      const int s = j & 1;
+      ftc_wait(&p_full[s], (j >> 1) & 1, 26, j);
+      tc_fence_after();
+      const uint32_t sq = smem_u32(smem + L::kQO + s * 4 * kFbBox64), so = sq + 2 * kFbBox64;
+      const uint32_t sp = smem_u32(smem + L::kPS + s * 2 * kFbBox128), sds = sp + kFbBox128;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // 16 queries per MMA
+          const uint32_t acc = (j | kk) ? 1u : 0u;
+          umma_bf16(tmem + 256, umma_desc_kmajor(sp + kk * 32, 128),
+                    umma_desc_mnmajor(so + kk * 2048, kFbBox64), idesc_g, acc);
+          umma_bf16(tmem + 384, umma_desc_kmajor(sds + kk * 32, 128),
+                    umma_desc_mnmajor(sq + kk * 2048, kFbBox64), idesc_g, acc);
+        }
+        umma_commit(&mm_done[s]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ===================== elementwise: thread = 32 queries of one key row =====================
+    const int ew = warp & 3, half = (warp - 4) >> 2;
+    const int r = ew * 32 + lane, key = k0 + r;
+    const bool key_ok = key < p.T;
+    const int kend = key_ok ? p.row_end[key] : 0;
+    const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+    const bool tile_full = nk == 128;
+    const int kend0 = p.row_end[k0];  // the smallest sequence end of the tile's keys
+    const float c = p.scale_log2;
+    for (int j = 0; j < total; ++j) {
+      const int s = j & 1;
+      const int qr = k0 + (j % per_head) * 64;
+      const int q0 = qr + half * 32;
+      ftc_wait(&s_full[s], (j >> 1) & 1, 27, j);
+      tc_fence_after();
+      uint32_t sr[32], dp[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + s * 64 + half * 32, sr);
+      tmem_ld_32x32b_x32(tmem + lane_base + 128 + s * 64 + half * 32, dp);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[s]);
+      ftc_wait(&qd_full[s], (j >> 1) & 1, 28, j);  // the step's lse / delta (staged by warp 3)
+      const float* stat = reinterpret_cast<const float*>(smem + L::kStat) + s * 128 + half * 32;
+      float pv[32], dsv[32];
+      const bool interior = tile_full && q0 >= k0 + 127 && q0 + 31 < kend0;
+#pragma unroll
+      for (int e4 = 0; e4 < 8; ++e4) {
+        const float4 ls = *reinterpret_cast<const float4*>(stat + e4 * 4);
+        const float4 dl = *reinterpret_cast<const float4*>(stat + 64 + e4 * 4);
+        const float lsv[4] = {ls.x, ls.y, ls.z, ls.w}, dlv[4] = {dl.x, dl.y, dl.z, dl.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = e4 * 4 + i, q = q0 + e;
+          const bool ok = interior || (key_ok && q >= key && q < kend);
+          const float pe = ok ? ex2_approx(fmaf(__uint_as_float(sr[e]), c, -lsv[i])) : 0.f;
+          pv[e] = pe;
+          dsv[e] = pe * (__uint_as_float(dp[e]) - dlv[i]);
+        }
+      }
+      if (j >= 2) ftc_wait(&mm_done[s], ((j >> 1) - 1) & 1, 29, j);
+      uint8_t* ps = smem + L::kPS + s * 2 * kFbBox128;
+      fb_store_row32(ps, r, half, pv);
+      fb_store_row32(ps + kFbBox128, r, half, dsv);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[s]);
+    }
+    ftc_wait(&mm_done[(total - 1) & 1], ((total - 1) >> 1) & 1, 30, total);
+    tc_fence_after();
+    fb_store_acc64(tmem + lane_base + 256 + half * 64,
+                   p.dv + (size_t)key * p.lddv + hk * kFaD + half * 64, 1.f, key_ok);
+    fb_store_acc64(tmem + lane_base + 384 + half * 64,
+                   p.dk + (size_t)key * p.lddk + hk * kFaD + half * 64, p.scale, key_ok);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512, 1>(tmem);
+  }
+}
+
+// ================================================================== dQ
+__global__ void __launch_bounds__(384, 1)
+    flash_bwd_dq_tc_kernel(const __grid_constant__ FlashBwdTcMaps maps, const FlashParams p) {
+  using L = FbDqSmem;
+  extern __shared__ uint8_t fbraw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fbraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* q_full = bar;         // Q, dO tiles loaded
+  uint64_t* kv_full = bar + 1;    // [2] K / V step loaded
+  uint64_t* s_full = bar + 3;     // [2]
+  uint64_t* s_free = bar + 5;     // [2]
+  uint64_t* p_full = bar + 7;     // [2] dS tile b written
+  uint64_t* mm_done = bar + 9;    // [2] dQ MMAs of the step done (K/V stage + dS tile b free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+
+  const int h = blockIdx.y;
+  const int q0 = (gridDim.x - 1 - blockIdx.x) * 128;  // late (long) query tiles first
+  if (q0 >= p.T) return;
+  const int hk = h / (p.n_heads / p.n_kv_heads);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nq = min(128, p.T - q0);
+  const int kstart = p.row_start[q0], kend = q0 + nq;
+  const int n_steps = (kend - kstart + 63) / 64;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&kv_full[b], 1);
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 8);
+      mbar_init(&p_full[b], 8);
+      mbar_init(&mm_done[b], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512, 1>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S [0,128), dP [128,256), dQ [256,384)
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&maps.k64);
+      tma_prefetch_desc(&maps.v64);
+      mbar_arrive_expect_tx(q_full, 4 * kFbBox128);
+      tma_load_2d(smem + L::kQ, &maps.q128, q_full, h * kFaD, q0);
+      tma_load_2d(smem + L::kQ + kFbBox128, &maps.q128, q_full, h * kFaD + 64, q0);
+      tma_load_2d(smem + L::kO, &maps.o128, q_full, h * kFaD, q0);
+      tma_load_2d(smem + L::kO + kFbBox128, &maps.o128, q_full, h * kFaD + 64, q0);
+      for (int j = 0; j < n_steps; ++j) {
+        const int s = j & 1;
+        if (j >= 2) ftc_wait(&mm_done[s], ((j >> 1) - 1) & 1, 41, j);
+        const int kr = kstart + j * 64;
+        uint8_t* st = smem + L::kKV + s * 4 * kFbBox64;
+        mbar_arrive_expect_tx(&kv_full[s], 4 * kFbBox64);
+        tma_load_2d(st, &maps.k64, &kv_full[s], hk * kFaD, kr);
+        tma_load_2d(st + kFbBox64, &maps.k64, &kv_full[s], hk * kFaD + 64, kr);
+        tma_load_2d(st + 2 * kFbBox64, &maps.v64, &kv_full[s], hk * kFaD, kr);
+        tma_load_2d(st + 3 * kFbBox64, &maps.v64, &kv_full[s], hk * kFaD + 64, kr);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc_s = umma_idesc_bf16(128, 64);
+    const uint32_t idesc_g = umma_idesc_bf16(128, 128) | (1u << 16);  // B (K) MN-major
+    const uint32_t sq = smem_u32(smem + L::kQ), so = smem_u32(smem + L::kO);
+    ftc_wait(q_full, 0, 42, 0);
+    auto issue_s = [&](int j) {
+      const int s = j & 1;
+      ftc_wait(&kv_full[s], (j >> 1) & 1, 43, j);
+      if (j >= 2) ftc_wait(&s_free[s], ((j >> 1) - 1) & 1, 44, j);
+      tc_fence_after();
+      const uint32_t sk = smem_u32(smem + L::kKV + s * 4 * kFbBox64), sv = sk + 2 * kFbBox64;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t offa = (kk >> 2) * kFbBox128 + (kk & 3) * 32;
+          const uint32_t offb = (kk >> 2) * kFbBox64 + (kk & 3) * 32;
+          umma_bf16(tmem + s * 64, umma_desc_kmajor(sq + offa, 128), umma_desc_kmajor(sk + offb, 128),
+                    idesc_s, kk ? 1u : 0u);
+          umma_bf16(tmem + 128 + s * 64, umma_desc_kmajor(so + offa, 128),
+                    umma_desc_kmajor(sv + offb, 128), idesc_s, kk ? 1u : 0u);
+        }
+        umma_commit(&s_full[s]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < n_steps; ++j) {
+      if (j + 1 < n_steps) issue_s(j + 1);
+      const int s = j & 1;
+      ftc_wait(&p_full[s], (j >> 1) & 1, 45, j);
+      tc_fence_after();
+      const uint32_t sk = smem_u32(smem + L::kKV + s * 4 * kFbBox64);
+      const uint32_t sds = smem_u32(smem + L::kS + s * kFbBox128);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // 16 keys per MMA
+          umma_bf16(tmem + 256, umma_desc_kmajor(sds + kk * 32, 128),
+                    umma_desc_mnmajor(sk + kk * 2048, kFbBox64), idesc_g, (j | kk) ? 1u : 0u);
+        umma_commit(&mm_done[s]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ===================== elementwise: thread = 32 keys of one query row =====================
+    const int ew = warp & 3, half = (warp - 4) >> 2;
+    const int r = ew * 32 + lane, qr = q0 + r;
+    const bool row_ok = qr < p.T;
+    const int qs = row_ok ? p.row_start[qr] : 0x7fffffff;
+    const float lse = row_ok ? p.lse[(size_t)h * p.stat_ld + qr] : 0.f;
+    const float dl = row_ok ? p.delta[(size_t)h * p.stat_ld + qr] : 0.f;
+    const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+    const int qs_last = p.row_start[q0 + nq - 1];
+    const float c = p.scale_log2;
+    for (int j = 0; j < n_steps; ++j) {
+      const int s = j & 1;
+      const int key0 = kstart + j * 64 + half * 32;
+      ftc_wait(&s_full[s], (j >> 1) & 1, 46, j);
+      tc_fence_after();
+      uint32_t sr[32], dp[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + s * 64 + half * 32, sr);
+      tmem_ld_32x32b_x32(tmem + lane_base + 128 + s * 64 + half * 32, dp);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[s]);
+      const bool interior = nq == 128 && key0 + 31 <= q0 && key0 >= qs_last;
+      float dsv[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int key = key0 + e;
+        const bool ok = interior || (row_ok && key <= qr && key >= qs);
+        const float pe = ok ? ex2_approx(fmaf(__uint_as_float(sr[e]), c, -lse)) : 0.f;
+        dsv[e] = pe * (__uint_as_float(dp[e]) - dl);
+      }
+      if (j >= 2) ftc_wait(&mm_done[s], ((j >> 1) - 1) & 1, 47, j);
+      fb_store_row32(smem + L::kS + s * kFbBox128, r, half, dsv);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[s]);
+    }
+    ftc_wait(&mm_done[(n_steps - 1) & 1], ((n_steps - 1) >> 1) & 1, 48, n_steps);
+    tc_fence_after();
+    fb_store_acc64(tmem + lane_base + 256 + half * 64,
+                   p.dq + (size_t)qr * p.lddq + h * kFaD + half * 64, p.scale, row_ok);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512, 1>(tmem);
+  }
+}
+
+}  // namespace collm

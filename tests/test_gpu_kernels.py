@@ -429,17 +429,18 @@ def test_flash_attention_vs_oracle(lens, n_heads, n_kv, impl):
     ops.set_flash_impl(impl)
     try:
         ops.flash_attention(q, k, v, out, lse, *rows, **kw)
+        dqkv = torch.zeros_like(qkv)
+        dq, dk, dv = (dqkv[:, :n_heads * D], dqkv[:, n_heads * D:(n_heads + n_kv) * D],
+                      dqkv[:, (n_heads + n_kv) * D:])
+        delta = torch.zeros(n_heads, T, device="cuda")
+        ops.flash_attention_bwd(q, k, v, out, dout, lse, delta, dq, dk, dv, *rows, **kw)
+        dqkv2 = torch.zeros_like(qkv)
+        ops.flash_attention_bwd(q, k, v, out, dout, lse, delta, dqkv2[:, :n_heads * D],
+                                dqkv2[:, n_heads * D:(n_heads + n_kv) * D],
+                                dqkv2[:, (n_heads + n_kv) * D:], *rows, **kw)
+        torch.cuda.synchronize()
     finally:
         ops.set_flash_impl(prev)
-    dqkv = torch.zeros_like(qkv)
-    dq, dk, dv = dqkv[:, :n_heads * D], dqkv[:, n_heads * D:(n_heads + n_kv) * D], dqkv[:, (n_heads + n_kv) * D:]
-    delta = torch.zeros(n_heads, T, device="cuda")
-    ops.flash_attention_bwd(q, k, v, out, dout, lse, delta, dq, dk, dv, *rows, **kw)
-    dqkv2 = torch.zeros_like(qkv)
-    ops.flash_attention_bwd(q, k, v, out, dout, lse, delta, dqkv2[:, :n_heads * D],
-                            dqkv2[:, n_heads * D:(n_heads + n_kv) * D],
-                            dqkv2[:, (n_heads + n_kv) * D:], *rows, **kw)
-    torch.cuda.synchronize()
     assert torch.equal(dqkv, dqkv2)
     f = lambda t: t.float().cpu().numpy()  # noqa: E731
     ref, lse_ref, (dq_r, dk_r, dv_r) = oracle.causal_attention(f(q), f(k), f(v), seq, n_heads, n_kv,
