@@ -768,14 +768,14 @@ int collm_flash_attention_bwd(const void* q, int ldq, const void* k, int ldk, co
       aligned16(dk) && aligned16(dv)) {
     // tcgen05/TMEM backward (flash_bwd_tc.cuh)
     FlashBwdTcMaps maps;
-    int rc2 = make_tmap(&maps.q64, q, ldq, T, ldq, 64, 64);
-    if (!rc2) rc2 = make_tmap(&maps.o64, dout, lddo, T, lddo, 64, 64);
+    int rc2 = make_tmap_kblocks(&maps.q64, q, T, ldq, ldq / 64, 64, 2);
+    if (!rc2) rc2 = make_tmap_kblocks(&maps.o64, dout, T, lddo, lddo / 64, 64, 2);
     if (!rc2) rc2 = make_tmap(&maps.k128, k, ldk, T, ldk, 64, 128);
     if (!rc2) rc2 = make_tmap(&maps.v128, v, ldv, T, ldv, 64, 128);
     if (!rc2) rc2 = make_tmap(&maps.q128, q, ldq, T, ldq, 64, 128);
     if (!rc2) rc2 = make_tmap(&maps.o128, dout, lddo, T, lddo, 64, 128);
-    if (!rc2) rc2 = make_tmap(&maps.k64, k, ldk, T, ldk, 64, 64);
-    if (!rc2) rc2 = make_tmap(&maps.v64, v, ldv, T, ldv, 64, 64);
+    if (!rc2) rc2 = make_tmap_kblocks(&maps.k64, k, T, ldk, ldk / 64, 64, 2);
+    if (!rc2) rc2 = make_tmap_kblocks(&maps.v64, v, T, ldv, ldv / 64, 64, 2);
     if (rc2) return rc2;
     static bool configured[kMaxDevices] = {};
     const int dev = cur_device();
@@ -789,6 +789,8 @@ int collm_flash_attention_bwd(const void* q, int ldq, const void* k, int ldk, co
         configured[dev] = true;
       }
     }
+    static const int fb_debug = [] { const char* e = getenv("COLLM_DEBUG_FB"); return e ? atoi(e) : 0; }();
+    if (fb_debug) CUDA_TRY(cudaMemcpyToSymbolAsync(g_fb_debug, &fb_debug, sizeof(int), 0, cudaMemcpyHostToDevice, st));
     const int t128 = (T + 127) / 128;
     flash_bwd_dkdv_tc_kernel<<<dim3(t128, n_kv_heads), 384, FbDkdvSmem::kTotal, st>>>(maps, p);
     CUDA_TRY(cudaGetLastError());

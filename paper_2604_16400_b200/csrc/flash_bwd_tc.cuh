@@ -14,7 +14,8 @@
 //   (k <= q < row_end[k]), dS^T = P^T (dP^T - delta[q]), both bf16 into K-major swizzled tiles;
 //   dV  += P^T dO   M = 128 keys x N = 128 dims x K = 64 queries (B = dO MN-major)
 //   dK  += dS^T Q   same (B = Q MN-major)                -> TMEM accumulators for the whole loop.
-// Q / dO steps stream through a 2-stage TMA ring; warp 3 stages the step's lse / delta.
+// Q / dO steps stream through a 3-stage TMA ring; warp 3 stages the step's lse / delta.  (dQ:
+// K / V steps through a 4-stage ring.)
 //
 // dQ kernel — CTA = 128 queries x one head; loops over 64-key steps from the first row's
 // sequence start to the tile's last row:
@@ -33,27 +34,35 @@ namespace collm {
 
 constexpr uint32_t kFbBox64 = 64 * 128;    // [64 rows][64 dims] bf16 TMA box, 8 KB
 constexpr uint32_t kFbBox128 = 128 * 128;  // [128 rows][64 dims] bf16 TMA box, 16 KB
+constexpr int kFbQStages = 3;   // dK/dV: Q / dO step ring depth
+constexpr int kFbKVStages = 4;  // dQ: K / V step ring depth
+// timing experiments only (COLLM_DEBUG_FB): 1 = skip the MMAs (commit only), 2 = skip the
+// elementwise math (barriers only)
+__device__ int g_fb_debug;
 
 struct FlashBwdTcMaps {
-  CUtensorMap q64, o64, k128, v128;  // dK/dV kernel: Q / dO steps of 64 rows, K / V tiles of 128
-  CUtensorMap q128, o128, k64, v64;  // dQ kernel: Q / dO tiles of 128 rows, K / V steps of 64
+  // dK/dV kernel: Q / dO steps of 64 rows as ONE 3-D box each ([2 dim blocks][64 rows][64 dims],
+  // k-block view), K / V tiles of 128 rows (2-D boxes)
+  CUtensorMap q64, o64, k128, v128;
+  // dQ kernel: Q / dO tiles of 128 rows (2-D), K / V steps of 64 rows (3-D, one box each)
+  CUtensorMap q128, o128, k64, v64;
 };
 
 struct FbDkdvSmem {
   static constexpr uint32_t kK = 0;                   // 2 boxes [128 keys][64 dims]
   static constexpr uint32_t kV = 2 * kFbBox128;
-  static constexpr uint32_t kQO = 4 * kFbBox128;      // [2 stages] Q (2 boxes), dO (2 boxes)
-  static constexpr uint32_t kPS = kQO + 2 * 4 * kFbBox64;  // [2] P^T tile, dS^T tile [128][64]
-  static constexpr uint32_t kStat = kPS + 2 * 2 * kFbBox128;  // [2 stages][lse 64 | delta 64]
-  static constexpr uint32_t kBar = kStat + 2 * 128 * 4;
+  static constexpr uint32_t kQO = 4 * kFbBox128;      // [stages] Q (2 boxes), dO (2 boxes)
+  static constexpr uint32_t kPS = kQO + kFbQStages * 4 * kFbBox64;  // [2] P^T, dS^T tiles [128][64]
+  static constexpr uint32_t kStat = kPS + 2 * 2 * kFbBox128;  // [stages][lse 64 | delta 64]
+  static constexpr uint32_t kBar = kStat + kFbQStages * 128 * 4;
   static constexpr uint32_t kTotal = kBar + 256 + 1024;
 };
 
 struct FbDqSmem {
   static constexpr uint32_t kQ = 0;                    // 2 boxes [128 q][64 dims]
   static constexpr uint32_t kO = 2 * kFbBox128;        // dO
-  static constexpr uint32_t kKV = 4 * kFbBox128;       // [2 stages] K (2 boxes [64][64]), V
-  static constexpr uint32_t kS = kKV + 2 * 4 * kFbBox64;  // [2] dS tile [128 q][64 keys]
+  static constexpr uint32_t kKV = 4 * kFbBox128;       // [stages] K (2 boxes [64][64]), V
+  static constexpr uint32_t kS = kKV + kFbKVStages * 4 * kFbBox64;  // [2] dS tile [128 q][64 keys]
   static constexpr uint32_t kBar = kS + 2 * kFbBox128;
   static constexpr uint32_t kTotal = kBar + 256 + 1024;
 };
@@ -96,12 +105,13 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fbraw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* kv_full = bar;        // K, V tiles loaded
-  uint64_t* qd_full = bar + 1;    // [2] Q / dO step + its lse / delta staged
-  uint64_t* s_full = bar + 3;     // [2] S^T, dP^T of the step in TMEM buffer b
-  uint64_t* s_free = bar + 5;     // [2] elementwise warps done reading TMEM buffer b
-  uint64_t* p_full = bar + 7;     // [2] P^T / dS^T tiles b written
-  uint64_t* mm_done = bar + 9;    // [2] dV / dK MMAs of the step done (stage + tiles b free)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+  uint64_t* s_full = bar + 1;     // [2] S^T, dP^T of the step in TMEM buffer b
+  uint64_t* s_free = bar + 3;     // [2] elementwise warps done reading TMEM buffer b
+  uint64_t* p_full = bar + 5;     // [2] P^T / dS^T tiles b written
+  uint64_t* mm_done = bar + 7;    // [2] dV / dK MMAs of the step done (tiles b free)
+  uint64_t* qd_full = bar + 9;    // [stages] Q / dO step + its lse / delta staged
+  uint64_t* qd_empty = bar + 9 + kFbQStages;  // [stages] the step's MMAs done (stage free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 2 * kFbQStages);
 
   const int hk = blockIdx.y;
   const int k0 = (gridDim.x - 1 - blockIdx.x) * 128;  // long (early-key) tiles first
@@ -114,8 +124,11 @@ __global__ void __launch_bounds__(384, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kFbQStages; ++b) {
       mbar_init(&qd_full[b], 2);
+      mbar_init(&qd_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&s_free[b], 8);
       mbar_init(&p_full[b], 8);
@@ -140,33 +153,49 @@ __global__ void __launch_bounds__(384, 1)
       tma_load_2d(smem + L::kV, &maps.v128, kv_full, hk * kFaD, k0);
       tma_load_2d(smem + L::kV + kFbBox128, &maps.v128, kv_full, hk * kFaD + 64, k0);
       for (int it = 0; it < total; ++it) {
-        const int s = it & 1;
-        if (it >= 2) ftc_wait(&mm_done[s], ((it >> 1) - 1) & 1, 21, it);
+        const int s = it % kFbQStages, u = it / kFbQStages;
+        if (it >= kFbQStages) ftc_wait(&qd_empty[s], (u - 1) & 1, 21, it);
         const int hq = hk * G + it / per_head, qr = k0 + (it % per_head) * 64;
         uint8_t* st = smem + L::kQO + s * 4 * kFbBox64;
         mbar_arrive_expect_tx(&qd_full[s], 4 * kFbBox64);
-        tma_load_2d(st, &maps.q64, &qd_full[s], hq * kFaD, qr);
-        tma_load_2d(st + kFbBox64, &maps.q64, &qd_full[s], hq * kFaD + 64, qr);
-        tma_load_2d(st + 2 * kFbBox64, &maps.o64, &qd_full[s], hq * kFaD, qr);
-        tma_load_2d(st + 3 * kFbBox64, &maps.o64, &qd_full[s], hq * kFaD + 64, qr);
+        tma_load_3d(st, &maps.q64, &qd_full[s], 0, qr, hq * 2);
+        tma_load_3d(st + 2 * kFbBox64, &maps.o64, &qd_full[s], 0, qr, hq * 2);
       }
     }
   } else if (warp == 3) {
     // ===================== statistics of each step: lse, delta of its 64 queries =====================
-    for (int it = 0; it < total; ++it) {
-      const int s = it & 1;
-      if (it >= 2) ftc_wait(&mm_done[s], ((it >> 1) - 1) & 1, 22, it);
-      const int hq = hk * G + it / per_head, qr = k0 + (it % per_head) * 64;
-      float* stat = reinterpret_cast<float*>(smem + L::kStat) + s * 128;
+    // 8 steps' loads in flight at once (a load round trip per step would pace the whole kernel)
+    constexpr int D = 8;
+    for (int base = 0; base < total; base += D) {
+      float v[D][4];
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int q = qr + h2 * 32 + lane;
-        const bool ok = q < qend;
-        stat[h2 * 32 + lane] = ok ? p.lse[(size_t)hq * p.stat_ld + q] : 0.f;
-        stat[64 + h2 * 32 + lane] = ok ? p.delta[(size_t)hq * p.stat_ld + q] : 0.f;
+      for (int d = 0; d < D; ++d) {
+        const int it = base + d;
+        if (it >= total) break;
+        const int hq = hk * G + it / per_head, qr = k0 + (it % per_head) * 64;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int q = qr + h2 * 32 + lane;
+          const bool ok = q < qend;
+          v[d][h2] = ok ? p.lse[(size_t)hq * p.stat_ld + q] : 0.f;
+          v[d][2 + h2] = ok ? p.delta[(size_t)hq * p.stat_ld + q] : 0.f;
+        }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&qd_full[s]);
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int it = base + d;
+        if (it >= total) break;
+        const int s = it % kFbQStages, u = it / kFbQStages;
+        if (it >= kFbQStages) ftc_wait(&qd_empty[s], (u - 1) & 1, 22, it);
+        float* stat = reinterpret_cast<float*>(smem + L::kStat) + s * 128;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          stat[h2 * 32 + lane] = v[d][h2];
+          stat[64 + h2 * 32 + lane] = v[d][2 + h2];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&qd_full[s]);
+      }
     }
   } else if (warp == 1) {
     // ===================== tcgen05.mma issuer =====================
@@ -175,12 +204,13 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t sk = smem_u32(smem + L::kK), sv = smem_u32(smem + L::kV);
     ftc_wait(kv_full, 0, 23, 0);
     auto issue_s = [&](int j) {
-      const int s = j & 1;
-      ftc_wait(&qd_full[s], (j >> 1) & 1, 24, j);
+      const int s = j & 1, qs = j % kFbQStages;
+      ftc_wait(&qd_full[qs], (j / kFbQStages) & 1, 24, j);
       if (j >= 2) ftc_wait(&s_free[s], ((j >> 1) - 1) & 1, 25, j);
       tc_fence_after();
-      const uint32_t sq = smem_u32(smem + L::kQO + s * 4 * kFbBox64), so = sq + 2 * kFbBox64;
+      const uint32_t sq = smem_u32(smem + L::kQO + qs * 4 * kFbBox64), so = sq + 2 * kFbBox64;
       if (elect_one()) {
+        if (!(g_fb_debug & 1))
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t offa = (kk >> 2) * kFbBox128 + (kk & 3) * 32;
@@ -200,9 +230,11 @@ __global__ void __launch_bounds__(384, 1)
       const int s = j & 1;
       ftc_wait(&p_full[s], (j >> 1) & 1, 26, j);
       tc_fence_after();
-      const uint32_t sq = smem_u32(smem + L::kQO + s * 4 * kFbBox64), so = sq + 2 * kFbBox64;
+      const int qs = j % kFbQStages;
+      const uint32_t sq = smem_u32(smem + L::kQO + qs * 4 * kFbBox64), so = sq + 2 * kFbBox64;
       const uint32_t sp = smem_u32(smem + L::kPS + s * 2 * kFbBox128), sds = sp + kFbBox128;
       if (elect_one()) {
+        if (!(g_fb_debug & 1))
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // 16 queries per MMA
           const uint32_t acc = (j | kk) ? 1u : 0u;
@@ -212,6 +244,7 @@ __global__ void __launch_bounds__(384, 1)
                     umma_desc_mnmajor(sq + kk * 2048, kFbBox64), idesc_g, acc);
         }
         umma_commit(&mm_done[s]);
+        umma_commit(&qd_empty[qs]);
       }
       __syncwarp();
     }
@@ -231,6 +264,11 @@ __global__ void __launch_bounds__(384, 1)
       const int q0 = qr + half * 32;
       ftc_wait(&s_full[s], (j >> 1) & 1, 27, j);
       tc_fence_after();
+      if (g_fb_debug & 2) {
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(&s_free[s]); mbar_arrive(&p_full[s]); }
+        continue;
+      }
       uint32_t sr[32], dp[32];
       tmem_ld_32x32b_x32(tmem + lane_base + s * 64 + half * 32, sr);
       tmem_ld_32x32b_x32(tmem + lane_base + 128 + s * 64 + half * 32, dp);
@@ -238,8 +276,9 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[s]);
-      ftc_wait(&qd_full[s], (j >> 1) & 1, 28, j);  // the step's lse / delta (staged by warp 3)
-      const float* stat = reinterpret_cast<const float*>(smem + L::kStat) + s * 128 + half * 32;
+      const int qs = j % kFbQStages;
+      ftc_wait(&qd_full[qs], (j / kFbQStages) & 1, 28, j);  // the step's lse / delta (warp 3)
+      const float* stat = reinterpret_cast<const float*>(smem + L::kStat) + qs * 128 + half * 32;
       float pv[32], dsv[32];
       const bool interior = tile_full && q0 >= k0 + 127 && q0 + 31 < kend0;
 #pragma unroll
@@ -288,12 +327,13 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fbraw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* q_full = bar;         // Q, dO tiles loaded
-  uint64_t* kv_full = bar + 1;    // [2] K / V step loaded
-  uint64_t* s_full = bar + 3;     // [2]
-  uint64_t* s_free = bar + 5;     // [2]
-  uint64_t* p_full = bar + 7;     // [2] dS tile b written
-  uint64_t* mm_done = bar + 9;    // [2] dQ MMAs of the step done (K/V stage + dS tile b free)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+  uint64_t* s_full = bar + 1;     // [2]
+  uint64_t* s_free = bar + 3;     // [2]
+  uint64_t* p_full = bar + 5;     // [2] dS tile b written
+  uint64_t* mm_done = bar + 7;    // [2] dQ MMAs of the step done (dS tile b free)
+  uint64_t* kv_full = bar + 9;    // [stages] K / V step loaded
+  uint64_t* kv_empty = bar + 9 + kFbKVStages;  // [stages] the step's MMAs done (stage free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 2 * kFbKVStages);
 
   const int h = blockIdx.y;
   const int q0 = (gridDim.x - 1 - blockIdx.x) * 128;  // late (long) query tiles first
@@ -306,8 +346,11 @@ __global__ void __launch_bounds__(384, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kFbKVStages; ++b) {
       mbar_init(&kv_full[b], 1);
+      mbar_init(&kv_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&s_free[b], 8);
       mbar_init(&p_full[b], 8);
@@ -331,15 +374,13 @@ __global__ void __launch_bounds__(384, 1)
       tma_load_2d(smem + L::kO, &maps.o128, q_full, h * kFaD, q0);
       tma_load_2d(smem + L::kO + kFbBox128, &maps.o128, q_full, h * kFaD + 64, q0);
       for (int j = 0; j < n_steps; ++j) {
-        const int s = j & 1;
-        if (j >= 2) ftc_wait(&mm_done[s], ((j >> 1) - 1) & 1, 41, j);
+        const int s = j % kFbKVStages, u = j / kFbKVStages;
+        if (j >= kFbKVStages) ftc_wait(&kv_empty[s], (u - 1) & 1, 41, j);
         const int kr = kstart + j * 64;
         uint8_t* st = smem + L::kKV + s * 4 * kFbBox64;
         mbar_arrive_expect_tx(&kv_full[s], 4 * kFbBox64);
-        tma_load_2d(st, &maps.k64, &kv_full[s], hk * kFaD, kr);
-        tma_load_2d(st + kFbBox64, &maps.k64, &kv_full[s], hk * kFaD + 64, kr);
-        tma_load_2d(st + 2 * kFbBox64, &maps.v64, &kv_full[s], hk * kFaD, kr);
-        tma_load_2d(st + 3 * kFbBox64, &maps.v64, &kv_full[s], hk * kFaD + 64, kr);
+        tma_load_3d(st, &maps.k64, &kv_full[s], 0, kr, hk * 2);
+        tma_load_3d(st + 2 * kFbBox64, &maps.v64, &kv_full[s], 0, kr, hk * 2);
       }
     }
   } else if (warp == 1) {
@@ -348,12 +389,13 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t sq = smem_u32(smem + L::kQ), so = smem_u32(smem + L::kO);
     ftc_wait(q_full, 0, 42, 0);
     auto issue_s = [&](int j) {
-      const int s = j & 1;
-      ftc_wait(&kv_full[s], (j >> 1) & 1, 43, j);
+      const int s = j & 1, ks = j % kFbKVStages;
+      ftc_wait(&kv_full[ks], (j / kFbKVStages) & 1, 43, j);
       if (j >= 2) ftc_wait(&s_free[s], ((j >> 1) - 1) & 1, 44, j);
       tc_fence_after();
-      const uint32_t sk = smem_u32(smem + L::kKV + s * 4 * kFbBox64), sv = sk + 2 * kFbBox64;
+      const uint32_t sk = smem_u32(smem + L::kKV + ks * 4 * kFbBox64), sv = sk + 2 * kFbBox64;
       if (elect_one()) {
+        if (!(g_fb_debug & 1))
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t offa = (kk >> 2) * kFbBox128 + (kk & 3) * 32;
@@ -373,14 +415,17 @@ __global__ void __launch_bounds__(384, 1)
       const int s = j & 1;
       ftc_wait(&p_full[s], (j >> 1) & 1, 45, j);
       tc_fence_after();
-      const uint32_t sk = smem_u32(smem + L::kKV + s * 4 * kFbBox64);
+      const int ks = j % kFbKVStages;
+      const uint32_t sk = smem_u32(smem + L::kKV + ks * 4 * kFbBox64);
       const uint32_t sds = smem_u32(smem + L::kS + s * kFbBox128);
       if (elect_one()) {
+        if (!(g_fb_debug & 1))
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // 16 keys per MMA
           umma_bf16(tmem + 256, umma_desc_kmajor(sds + kk * 32, 128),
                     umma_desc_mnmajor(sk + kk * 2048, kFbBox64), idesc_g, (j | kk) ? 1u : 0u);
         umma_commit(&mm_done[s]);
+        umma_commit(&kv_empty[ks]);
       }
       __syncwarp();
     }
@@ -400,6 +445,11 @@ __global__ void __launch_bounds__(384, 1)
       const int key0 = kstart + j * 64 + half * 32;
       ftc_wait(&s_full[s], (j >> 1) & 1, 46, j);
       tc_fence_after();
+      if (g_fb_debug & 2) {
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(&s_free[s]); mbar_arrive(&p_full[s]); }
+        continue;
+      }
       uint32_t sr[32], dp[32];
       tmem_ld_32x32b_x32(tmem + lane_base + s * 64 + half * 32, sr);
       tmem_ld_32x32b_x32(tmem + lane_base + 128 + s * 64 + half * 32, dp);
