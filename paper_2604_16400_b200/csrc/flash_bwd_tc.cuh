@@ -289,8 +289,9 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int e = e4 * 4 + i, q = q0 + e;
-          const bool ok = interior || (key_ok && q >= key && q < kend);
-          const float pe = ok ? ex2_approx(fmaf(__uint_as_float(sr[e]), c, -lsv[i])) : 0.f;
+          // branch-free mask (select before the exp: ex2(-inf) = 0)
+          const bool ok = interior | (key_ok & (q >= key) & (q < kend));
+          const float pe = ex2_approx(ok ? fmaf(__uint_as_float(sr[e]), c, -lsv[i]) : -INFINITY);
           pv[e] = pe;
           dsv[e] = pe * (__uint_as_float(dp[e]) - dlv[i]);
         }
@@ -462,8 +463,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
         const int key = key0 + e;
-        const bool ok = interior || (row_ok && key <= qr && key >= qs);
-        const float pe = ok ? ex2_approx(fmaf(__uint_as_float(sr[e]), c, -lse)) : 0.f;
+        const bool ok = interior | (row_ok & (key <= qr) & (key >= qs));  // branch-free
+        const float pe = ex2_approx(ok ? fmaf(__uint_as_float(sr[e]), c, -lse) : -INFINITY);
         dsv[e] = pe * (__uint_as_float(dp[e]) - dl);
       }
       if (j >= 2) ftc_wait(&mm_done[s], ((j >> 1) - 1) & 1, 47, j);
