@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const int key = key0 + ch * 32 + e;
-            const bool ok = row_ok && key <= qr && key >= qs;
+            const bool ok = row_ok & (key <= qr) & (key >= qs);  // branch-free
             const float v = ok ? __uint_as_float(sr[ch][e]) : -INFINITY;
             sr[ch][e] = __float_as_uint(v);
             hmax = fmaxf(hmax, v);
