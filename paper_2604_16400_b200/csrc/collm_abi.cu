@@ -413,7 +413,8 @@ int collm_lora_shrink(const void* X, int ldx, const void* A, long long a_stride,
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (g_reduce_lean[cur_device()]) {
+  static const int carve_env = [] { const char* e = getenv("COLLM_SHRINK_CARVEOUT"); return e ? atoi(e) : 0; }();
+  if (g_reduce_lean[cur_device()] || carve_env) {
     // next to a GEMM ask for the max-shared carveout: an SM this kernel reaches first must
     // still fit a GEMM CTA; alone, keep the default (more L1)
     attr[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;

@@ -26,14 +26,31 @@ st.run_step(plan)
 torch.cuda.synchronize()
 a = st._acts
 lib = _lib.load()
-lib.collm_set_gemm_lean(1)
+GRAPH = os.environ.get("GRAPH", "0") == "1"  # replay the pairs from a CUDA graph (no CPU gaps)
+lib.collm_set_gemm_lean(0 if (GRAPH and pdl) else 1)
 proj = [p for p in st.layers[0] if p.spec.name == want][0]
 X = a["X"][0] if want in ENTRY else (a["Xo"][0] if want == "o" else a["Xd"][0])
 Y = a["X"][1] if want == "down" else a["Y"][want]
-for _ in range(4):
-    prev = [q for q in st.layers[0] if q.spec.name != want][0]  # a GEMM before, as in the step
-    cache = proj.forward_lora(X, plan.device, n_train=plan.n_train)
-    proj.forward_gemm(cache, plan.device, Y, pdl=pdl)
+
+
+def pairs():
+    for _ in range(4):
+        cache = proj.forward_lora(X, plan.device, n_train=plan.n_train)
+        proj.forward_gemm(cache, plan.device, Y, pdl=pdl)
+
+
+if GRAPH:
+    pairs()
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s), torch.cuda.graph(gr, stream=s):
+        pairs()
+    torch.cuda.current_stream().wait_stream(s)
+    gr.replay()
+else:
+    pairs()
 torch.cuda.synchronize()
 sh = (ctypes.c_uint64 * (4096 * 2))()
 assert lib.collm_shrink_debug_copy(ctypes.byref(sh), ctypes.c_size_t(4096 * 16)) == 0
