@@ -276,6 +276,26 @@ def test_reduce_store_grad_vs_fp32(reduce_impl, T, P, Q, tsplit, v2, accum):
     assert torch.equal(outs[0], outs[1])
 
 
+def test_reduce_many_tensors_falls_back(reduce_impl):
+    """More distinct U / V tensors than the tcgen05 K5 maps in one launch (16 groups, 48 tensors):
+    the launch still runs (mma.sync kernel) and matches fp32 torch."""
+    from paper_2604_16400_b200 import _lib, ops
+    g = torch.Generator().manual_seed(11)
+    T = 200
+    groups, refs, grads, keep = [], [], [], []
+    for i in range(16):
+        U, V, V2 = _bf(T, 64, gen=g), _bf(T, 16, gen=g), _bf(T, 16, scale=1e-3, gen=g)
+        keep += [U, V, V2]  # the group table holds raw pointers
+        grad = torch.zeros(64, 16, device="cuda")
+        groups.append(ops.reduce_group(U, V, P=64, Q=16, ldc=16, grad=grad, V2=V2))
+        refs.append(U.float().t() @ (V.float() + V2.float()))
+        grads.append(grad)
+    ops.lora_reduce(T, groups, _lib.MODE_STORE_GRAD)
+    torch.cuda.synchronize()
+    for got, ref in zip(grads, refs):
+        assert ((got - ref).norm() / ref.norm()).item() < 1e-5
+
+
 def test_reduce_adamw(reduce_impl):
     from paper_2604_16400_b200 import _lib, ops
     g = torch.Generator().manual_seed(5)
@@ -404,7 +424,8 @@ def test_paged_attention_vs_oracle(n_heads, n_kv):
 @pytest.mark.parametrize("lens,n_heads,n_kv", [([512], 4, 4), ([1, 63, 64, 65, 200], 4, 2),
                                                ([130, 7, 300], 8, 2), ([1024], 2, 1),
                                                ([1] * 40 + [3, 17, 90] + [1] * 30, 4, 1),
-                                               ([129, 1, 255, 384, 2], 4, 4)])
+                                               ([129, 1, 255, 384, 2], 4, 4),
+                                               ([300, 5, 700], 8, 1)])
 @pytest.mark.parametrize("impl", [1, 0], ids=["tcgen05", "mma"])
 def test_flash_attention_vs_oracle(lens, n_heads, n_kv, impl):
     """K9: causal attention of packed sequences (ragged lengths incl. 1, tile boundaries 63/64/65,
