@@ -11,11 +11,16 @@
 //   dP^T = V dO^T   same shape (A = V, B = dO)            -> TMEM, double-buffered (next step's
 //                                                            MMAs overlap this step's elementwise)
 //   8 elementwise warps (thread = 32 queries of one key row): P^T = exp2(S^T c - lse[q]) masked
-//   (k <= q < row_end[k]), dS^T = P^T (dP^T - delta[q]), both bf16 into K-major swizzled tiles;
-//   dV  += P^T dO   M = 128 keys x N = 128 dims x K = 64 queries (B = dO MN-major)
-//   dK  += dS^T Q   same (B = Q MN-major)                -> TMEM accumulators for the whole loop.
-// Q / dO steps stream through a 3-stage TMA ring; warp 3 stages the step's lse / delta.  (dQ:
-// K / V steps through a 4-stage ring.)
+//   (k <= q < row_end[k]), dS^T = P^T (dP^T - delta[q]), both packed bf16 back into TMEM in
+//   place of the S^T / dP^T columns the thread read (tcgen05.st);
+//   dV  += P^T dO   M = 128 keys x N = 128 dims x K = 64 queries, A = P^T FROM TMEM, B = dO
+//                   (MN-major smem)
+//   dK  += dS^T Q   same (A = dS^T from TMEM, B = Q)     -> TMEM accumulators for the whole loop.
+// Q / dO steps stream through a 4-stage TMA ring; warp 3 stages the step's lse / delta.  (dQ:
+// K / V steps through a 5-stage ring; dS from TMEM as the A operand of dQ += dS K.)
+// Measured limits (13B, `COLLM_DEBUG_FB`): the Q / dO (dQ: K / V) re-reads per tile are L2-bound
+// (~6 TB/s L2 -> SM), then the N = 64 MMAs (~34 ns each, smem operand bandwidth), then the
+// elementwise work; a CTA pair multicasting the steps would halve the first.
 //
 // dQ kernel — CTA = 128 queries x one head; loops over 64-key steps from the first row's
 // sequence start to the tile's last row:
@@ -34,8 +39,8 @@ namespace collm {
 
 constexpr uint32_t kFbBox64 = 64 * 128;    // [64 rows][64 dims] bf16 TMA box, 8 KB
 constexpr uint32_t kFbBox128 = 128 * 128;  // [128 rows][64 dims] bf16 TMA box, 16 KB
-constexpr int kFbQStages = 3;   // dK/dV: Q / dO step ring depth
-constexpr int kFbKVStages = 4;  // dQ: K / V step ring depth
+constexpr int kFbQStages = 4;   // dK/dV: Q / dO step ring depth
+constexpr int kFbKVStages = 5;  // dQ: K / V step ring depth
 // timing experiments only (COLLM_DEBUG_FB): 1 = skip the MMAs (commit only), 2 = skip the
 // elementwise math (barriers only)
 __device__ int g_fb_debug;
@@ -52,8 +57,7 @@ struct FbDkdvSmem {
   static constexpr uint32_t kK = 0;                   // 2 boxes [128 keys][64 dims]
   static constexpr uint32_t kV = 2 * kFbBox128;
   static constexpr uint32_t kQO = 4 * kFbBox128;      // [stages] Q (2 boxes), dO (2 boxes)
-  static constexpr uint32_t kPS = kQO + kFbQStages * 4 * kFbBox64;  // [2] P^T, dS^T tiles [128][64]
-  static constexpr uint32_t kStat = kPS + 2 * 2 * kFbBox128;  // [stages][lse 64 | delta 64]
+  static constexpr uint32_t kStat = kQO + kFbQStages * 4 * kFbBox64;  // [stages][lse | delta]
   static constexpr uint32_t kBar = kStat + kFbQStages * 128 * 4;
   static constexpr uint32_t kTotal = kBar + 256 + 1024;
 };
@@ -62,20 +66,39 @@ struct FbDqSmem {
   static constexpr uint32_t kQ = 0;                    // 2 boxes [128 q][64 dims]
   static constexpr uint32_t kO = 2 * kFbBox128;        // dO
   static constexpr uint32_t kKV = 4 * kFbBox128;       // [stages] K (2 boxes [64][64]), V
-  static constexpr uint32_t kS = kKV + kFbKVStages * 4 * kFbBox64;  // [2] dS tile [128 q][64 keys]
-  static constexpr uint32_t kBar = kS + 2 * kFbBox128;
+  static constexpr uint32_t kBar = kKV + kFbKVStages * 4 * kFbBox64;
   static constexpr uint32_t kTotal = kBar + 256 + 1024;
 };
 
-// 32 bf16 (this thread's 32 columns of a 64-column K-major SWIZZLE_128B row) into its row
-__device__ __forceinline__ void fb_store_row32(uint8_t* tile, int row, int half, const float* v) {
+// 32 lanes x 16 consecutive 32-bit TMEM columns per thread (32x32b shape, x16)
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem desc]^T: the A operand read from tensor memory (M = 128 rows in
+// the lanes, two bf16 per 32-bit column, K = 16 -> 8 columns per instruction)
+__device__ __forceinline__ void umma_bf16_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// this thread's 32 values as 16 packed bf16 pairs at TMEM row `taddr` (the first half of the
+// 32 fp32 columns the thread read them from: no other thread touches those columns)
+__device__ __forceinline__ void fb_store_tmem32(uint32_t taddr, const float* v) {
+  uint32_t pk[16];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int piece = half * 4 + i;
-    *reinterpret_cast<uint4*>(tile + row * 128 + ((piece ^ (row & 7)) << 4)) =
-        make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                   pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
-  }
+  for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+  tmem_st_32x32b_x16(taddr, pk);
 }
 
 // write 64 fp32 accumulator columns [c0, c0+64) of TMEM row `lane_base` to bf16 dst, times mul
@@ -232,16 +255,16 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       const int qs = j % kFbQStages;
       const uint32_t sq = smem_u32(smem + L::kQO + qs * 4 * kFbBox64), so = sq + 2 * kFbBox64;
-      const uint32_t sp = smem_u32(smem + L::kPS + s * 2 * kFbBox128), sds = sp + kFbBox128;
       if (elect_one()) {
         if (!(g_fb_debug & 1))
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // 16 queries per MMA
           const uint32_t acc = (j | kk) ? 1u : 0u;
-          umma_bf16(tmem + 256, umma_desc_kmajor(sp + kk * 32, 128),
-                    umma_desc_mnmajor(so + kk * 2048, kFbBox64), idesc_g, acc);
-          umma_bf16(tmem + 384, umma_desc_kmajor(sds + kk * 32, 128),
-                    umma_desc_mnmajor(sq + kk * 2048, kFbBox64), idesc_g, acc);
+          // P^T / dS^T packed in TMEM: queries 32h..32h+31 at columns 32h..32h+15 of buffer s
+          const uint32_t col = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+          umma_bf16_ta(tmem + 256, tmem + col, umma_desc_mnmajor(so + kk * 2048, kFbBox64), idesc_g, acc);
+          umma_bf16_ta(tmem + 384, tmem + 128 + col, umma_desc_mnmajor(sq + kk * 2048, kFbBox64),
+                       idesc_g, acc);
         }
         umma_commit(&mm_done[s]);
         umma_commit(&qd_empty[qs]);
@@ -296,11 +319,11 @@ __global__ void __launch_bounds__(384, 1)
           dsv[e] = pe * (__uint_as_float(dp[e]) - dlv[i]);
         }
       }
-      if (j >= 2) ftc_wait(&mm_done[s], ((j >> 1) - 1) & 1, 29, j);
-      uint8_t* ps = smem + L::kPS + s * 2 * kFbBox128;
-      fb_store_row32(ps, r, half, pv);
-      fb_store_row32(ps + kFbBox128, r, half, dsv);
-      fence_proxy_async_smem();
+      // P^T and dS^T packed in place of the S^T / dP^T columns this thread read (the MMAs that
+      // read the previous step's P^T in this buffer completed before S^T(j) did: in order)
+      fb_store_tmem32(tmem + lane_base + s * 64 + half * 32, pv);
+      fb_store_tmem32(tmem + lane_base + 128 + s * 64 + half * 32, dsv);
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[s]);
@@ -418,13 +441,12 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       const int ks = j % kFbKVStages;
       const uint32_t sk = smem_u32(smem + L::kKV + ks * 4 * kFbBox64);
-      const uint32_t sds = smem_u32(smem + L::kS + s * kFbBox128);
       if (elect_one()) {
         if (!(g_fb_debug & 1))
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // 16 keys per MMA
-          umma_bf16(tmem + 256, umma_desc_kmajor(sds + kk * 32, 128),
-                    umma_desc_mnmajor(sk + kk * 2048, kFbBox64), idesc_g, (j | kk) ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk)  // 16 keys per MMA; dS packed in TMEM (dP buffer s)
+          umma_bf16_ta(tmem + 256, tmem + 128 + s * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
+                       umma_desc_mnmajor(sk + kk * 2048, kFbBox64), idesc_g, (j | kk) ? 1u : 0u);
         umma_commit(&mm_done[s]);
         umma_commit(&kv_empty[ks]);
       }
@@ -467,9 +489,8 @@ __global__ void __launch_bounds__(384, 1)
         const float pe = ex2_approx(ok ? fmaf(__uint_as_float(sr[e]), c, -lse) : -INFINITY);
         dsv[e] = pe * (__uint_as_float(dp[e]) - dl);
       }
-      if (j >= 2) ftc_wait(&mm_done[s], ((j >> 1) - 1) & 1, 47, j);
-      fb_store_row32(smem + L::kS + s * kFbBox128, r, half, dsv);
-      fence_proxy_async_smem();
+      fb_store_tmem32(tmem + lane_base + 128 + s * 64 + half * 32, dsv);
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[s]);
