@@ -222,7 +222,7 @@ typedef struct {
  * accumulators double-buffered in TMEM so the AdamW finalize overlaps the next unit's stream);
  * collm_set_reduce_impl(0) (or COLLM_K5_TC=0) selects the mma.sync kernel (32-row T chunks), which
  * also serves launches with more than 40 distinct U / V tensors. */
-int collm_set_reduce_impl(int tc); /* 1 = tcgen05 (default), 0 = mma.sync */
+int collm_set_reduce_impl(int tc); /* 1 = tcgen05 (default), 0 = mma.sync; caller's current device */
 int collm_get_reduce_impl(void);
 size_t collm_reduce_workspace_bytes(const collm_reduce_group* groups, int n_groups, int tsplit);
 int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int mode,
@@ -268,7 +268,7 @@ int collm_paged_attention(const void* q, int ldq, int T, int n_heads, int n_kv_h
  *      of a group summed in a fixed order).  Deterministic: no atomics (dK/dV and dQ in separate
  *      kernels, each output element owned by one CTA).  fp32 softmax and accumulation.
  * Replaces: nothing in the reference (it has no attention); SURVEY §8(f) row 1. */
-int collm_set_flash_impl(int tc); /* 1 = tcgen05 forward (default), 0 = mma.sync */
+int collm_set_flash_impl(int tc); /* 1 = tcgen05 (default), 0 = mma.sync; caller's current device */
 int collm_get_flash_impl(void);
 int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
                               void* out, int ldo, float* lse, int T, int n_heads, int n_kv_heads,

@@ -689,17 +689,22 @@ static int flash_launch(void (*kernel)(const FlashParams), int smem, dim3 grid, 
   return COLLM_OK;
 }
 
-static std::atomic<int> g_flash_impl{[] {
-  const char* e = getenv("COLLM_FA_TC");
-  return e ? atoi(e) : 1;
-}()};
+// Kernel selection per device (like the other mode switches): -1 = not set (the env default)
+static std::atomic<int> g_flash_impl[kMaxDevices];
+static std::atomic<int> g_reduce_impl[kMaxDevices];
+static int impl_of(std::atomic<int>* per_dev, const char* env) {
+  const int v = per_dev[cur_device()].load();
+  if (v > 0) return v - 1;
+  const char* e = getenv(env);
+  return e ? (atoi(e) != 0) : 1;
+}
 
 int collm_set_flash_impl(int tc) {
   CHECK_ARG(tc == 0 || tc == 1, "flash impl %d (0 = mma.sync, 1 = tcgen05)", tc);
-  g_flash_impl.store(tc);
+  g_flash_impl[cur_device()].store(tc + 1);
   return COLLM_OK;
 }
-int collm_get_flash_impl(void) { return g_flash_impl.load(); }
+int collm_get_flash_impl(void) { return impl_of(g_flash_impl, "COLLM_FA_TC"); }
 
 int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
                               void* out, int ldo, float* lse, int T, int n_heads, int n_kv_heads,
@@ -1324,11 +1329,6 @@ static int launch_reduce(ReduceParams& p, cudaStream_t st) {
 
 // K5 on the tensor core (reduce_tc.cuh), used when every operand can be viewed through a TMA map
 // (<= kRtcMaxMaps distinct U / V / V2 tensors); returns 1 when the launch is not possible.
-static std::atomic<int> g_reduce_impl{[] {
-  const char* e = getenv("COLLM_K5_TC");
-  return e ? atoi(e) : 1;
-}()};
-
 static int launch_reduce_tc(const ReduceParams& p, cudaStream_t st, bool* launched) {
   *launched = false;
   ReduceTcMaps maps;
@@ -1387,10 +1387,10 @@ extern "C" {
 
 int collm_set_reduce_impl(int tc) {
   CHECK_ARG(tc == 0 || tc == 1, "reduce impl %d (0 = mma.sync, 1 = tcgen05)", tc);
-  g_reduce_impl.store(tc);
+  g_reduce_impl[cur_device()].store(tc + 1);
   return COLLM_OK;
 }
-int collm_get_reduce_impl(void) { return g_reduce_impl.load(); }
+int collm_get_reduce_impl(void) { return impl_of(g_reduce_impl, "COLLM_K5_TC"); }
 
 int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int mode,
                       int accum_in, float grad_scale, const float* adamw, int tsplit,
@@ -1420,7 +1420,7 @@ int collm_lora_reduce(int T, const collm_reduce_group* groups, int n_groups, int
     p.partials = (float*)((char*)workspace + kCounterBytes);
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (g_reduce_impl.load()) {
+  if (collm_get_reduce_impl()) {
     bool launched = false;
     rc = launch_reduce_tc(p, st, &launched);
     if (rc || launched) return rc;
