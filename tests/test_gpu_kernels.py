@@ -152,7 +152,10 @@ def test_shrink(R, K):
 @pytest.mark.parametrize("R,K,n_ctas,dh,n_ad", [(16, 512, 2, False, 5), (48, 4096, 16, False, 5),
                                                 (96, 1024, 8, False, 5), (192, 5120, 16, False, 5),
                                                 (16, 1024, 8, False, 40), (48, 2048, 16, False, 40),
-                                                (48, 11008, 8, True, 5), (192, 2048, 4, True, 5)])
+                                                (48, 11008, 8, True, 5), (192, 2048, 4, True, 5),
+                                                # the whole GPU (large passes): many split-K parts
+                                                (48, 4096, 148, False, 5), (16, 1024, 148, False, 40),
+                                                (192, 2048, 148, True, 5)])
 def test_shrink_tc(R, K, n_ctas, dh, n_ad):
     """K1 on the rank-space partition (collm_lora_shrink_tc: TMA k-block boxes -> tcgen05 ->
     TMEM): items of <= 128 rows merged from ragged 16-row tiles (1-row tile, a base-only
