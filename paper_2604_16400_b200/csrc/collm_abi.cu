@@ -734,7 +734,9 @@ int collm_flash_attention_fwd(const void* q, int ldq, const void* k, int ldk, co
         configured[dev] = true;
       }
     }
-    flash_fwd_tc_kernel<<<dim3((T + kFtcRows - 1) / kFtcRows, n_heads), 384, FlashTcSmem::kTotal,
+    // persistent: one CTA per SM walks (query tile, head) items
+    const int n_items = (T + kFtcRows - 1) / kFtcRows * n_heads;
+    flash_fwd_tc_kernel<<<std::min(n_items, num_sms_cached()), 384, FlashTcSmem::kTotal,
                           (cudaStream_t)stream>>>(maps, p);
     CUDA_TRY(cudaGetLastError());
     return COLLM_OK;
