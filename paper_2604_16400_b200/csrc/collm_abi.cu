@@ -802,7 +802,7 @@ int collm_flash_attention_bwd(const void* q, int ldq, const void* k, int ldk, co
     const int t128 = (T + 127) / 128;
     flash_bwd_dkdv_tc_kernel<<<dim3(t128, n_kv_heads), 384, FbDkdvSmem::kTotal, st>>>(maps, p);
     CUDA_TRY(cudaGetLastError());
-    flash_bwd_dq_tc_kernel<<<dim3(t128, n_heads), 384, FbDqSmem::kTotal, st>>>(maps, p);
+    flash_bwd_dq_tc_kernel<<<std::min(t128 * n_heads, num_sms_cached()), 384, FbDqSmem::kTotal, st>>>(maps, p);
     CUDA_TRY(cudaGetLastError());
     return COLLM_OK;
   }

@@ -17,7 +17,7 @@
 //                   (MN-major smem)
 //   dK  += dS^T Q   same (A = dS^T from TMEM, B = Q)     -> TMEM accumulators for the whole loop.
 // Q / dO steps stream through a 4-stage TMA ring; warp 3 stages the step's lse / delta.  (dQ:
-// K / V steps through a 5-stage ring; dS from TMEM as the A operand of dQ += dS K.)
+// K / V steps through a 3-stage ring; dS from TMEM as the A operand of dQ += dS K; persistent.)
 // Measured limits (13B, `COLLM_DEBUG_FB`): the Q / dO (dQ: K / V) re-reads per tile are L2-bound
 // (~6 TB/s L2 -> SM), then the N = 64 MMAs (~34 ns each, smem operand bandwidth), then the
 // elementwise work; a CTA pair multicasting the steps would halve the first.
@@ -40,7 +40,7 @@ namespace collm {
 constexpr uint32_t kFbBox64 = 64 * 128;    // [64 rows][64 dims] bf16 TMA box, 8 KB
 constexpr uint32_t kFbBox128 = 128 * 128;  // [128 rows][64 dims] bf16 TMA box, 16 KB
 constexpr int kFbQStages = 4;   // dK/dV: Q / dO step ring depth
-constexpr int kFbKVStages = 5;  // dQ: K / V step ring depth
+constexpr int kFbKVStages = 3;  // dQ: K / V step ring depth
 // timing experiments only (COLLM_DEBUG_FB): 1 = skip the MMAs (commit only), 2 = skip the
 // elementwise math (barriers only)
 __device__ int g_fb_debug;
@@ -63,9 +63,8 @@ struct FbDkdvSmem {
 };
 
 struct FbDqSmem {
-  static constexpr uint32_t kQ = 0;                    // 2 boxes [128 q][64 dims]
-  static constexpr uint32_t kO = 2 * kFbBox128;        // dO
-  static constexpr uint32_t kKV = 4 * kFbBox128;       // [stages] K (2 boxes [64][64]), V
+  static constexpr uint32_t kQO = 0;                   // [2 items] Q (2 boxes [128][64]), dO
+  static constexpr uint32_t kKV = 2 * 4 * kFbBox128;   // [stages] K (2 boxes [64][64]), V
   static constexpr uint32_t kBar = kKV + kFbKVStages * 4 * kFbBox64;
   static constexpr uint32_t kTotal = kBar + 256 + 1024;
 };
@@ -322,41 +321,56 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // ================================================================== dQ
+// Persistent: one CTA per SM walks (query tile, head) items (late tiles first, heads fastest);
+// Q / dO double-buffered per item in smem, dQ double-buffered in TMEM, so the next item's loads
+// and first scores overlap this item's last steps and the previous item's dQ write-out.
+struct FbDqItem {
+  int h, q0, nq, kstart, n_steps;
+};
+__device__ __forceinline__ bool fb_dq_item(const FlashParams& p, int i, FbDqItem& it) {
+  const int n_qt = (p.T + 127) / 128;
+  if (i >= n_qt * p.n_heads) return false;
+  it.h = i % p.n_heads;
+  it.q0 = (n_qt - 1 - i / p.n_heads) * 128;
+  it.nq = min(128, p.T - it.q0);
+  it.kstart = p.row_start[it.q0];
+  it.n_steps = (it.q0 + it.nq - it.kstart + 63) / 64;
+  return true;
+}
+
 __global__ void __launch_bounds__(384, 1)
     flash_bwd_dq_tc_kernel(const __grid_constant__ FlashBwdTcMaps maps, const FlashParams p) {
   using L = FbDqSmem;
   extern __shared__ uint8_t fbraw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fbraw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t* q_full = bar;         // Q, dO tiles loaded
-  uint64_t* s_full = bar + 1;     // [2]
-  uint64_t* s_free = bar + 3;     // [2]
-  uint64_t* p_full = bar + 5;     // [2] dS tile b written
-  uint64_t* mm_done = bar + 7;    // [2] dQ MMAs of the step done (dS tile b free)
-  uint64_t* kv_full = bar + 9;    // [stages] K / V step loaded
-  uint64_t* kv_empty = bar + 9 + kFbKVStages;  // [stages] the step's MMAs done (stage free)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 2 * kFbKVStages);
+  uint64_t* q_full = bar;          // [2] Q, dO of item k in buffer k & 1
+  uint64_t* q_empty = bar + 2;     // [2] the item's last S / dP MMAs done (buffer free)
+  uint64_t* s_full = bar + 4;      // [2]
+  uint64_t* s_free = bar + 6;      // [2]
+  uint64_t* p_full = bar + 8;      // [2] dS (packed into the dP buffer) written
+  uint64_t* dq_full = bar + 10;    // [2] the item's dQ (TMEM buffer k & 1) complete
+  uint64_t* dq_empty = bar + 12;   // [2] dQ buffer read out
+  uint64_t* kv_full = bar + 14;    // [stages] K / V step loaded
+  uint64_t* kv_empty = bar + 14 + kFbKVStages;  // [stages] the step's MMAs done (stage free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14 + 2 * kFbKVStages);
 
-  const int h = blockIdx.y;
-  const int q0 = (gridDim.x - 1 - blockIdx.x) * 128;  // late (long) query tiles first
-  if (q0 >= p.T) return;
-  const int hk = h / (p.n_heads / p.n_kv_heads);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nq = min(128, p.T - q0);
-  const int kstart = p.row_start[q0], kend = q0 + nq;
-  const int n_steps = (kend - kstart + 63) / 64;
+  const int G = gridDim.x, Gh = p.n_heads / p.n_kv_heads;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
     for (int b = 0; b < kFbKVStages; ++b) {
       mbar_init(&kv_full[b], 1);
       mbar_init(&kv_empty[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], 1);
       mbar_init(&s_full[b], 1);
       mbar_init(&s_free[b], 8);
       mbar_init(&p_full[b], 8);
-      mbar_init(&mm_done[b], 1);
+      mbar_init(&dq_full[b], 1);
+      mbar_init(&dq_empty[b], 8);
     }
     fence_mbar_init();
   }
@@ -364,37 +378,45 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S [0,128), dP [128,256), dQ [256,384)
+  const uint32_t tmem = *tmem_slot;  // S [0,128), dP / dS [128,256), dQ [256,512) (2 buffers)
 
   if (warp == 0) {
     if (elect_one()) {
       tma_prefetch_desc(&maps.k64);
       tma_prefetch_desc(&maps.v64);
-      mbar_arrive_expect_tx(q_full, 4 * kFbBox128);
-      tma_load_2d(smem + L::kQ, &maps.q128, q_full, h * kFaD, q0);
-      tma_load_2d(smem + L::kQ + kFbBox128, &maps.q128, q_full, h * kFaD + 64, q0);
-      tma_load_2d(smem + L::kO, &maps.o128, q_full, h * kFaD, q0);
-      tma_load_2d(smem + L::kO + kFbBox128, &maps.o128, q_full, h * kFaD + 64, q0);
-      for (int j = 0; j < n_steps; ++j) {
-        const int s = j % kFbKVStages, u = j / kFbKVStages;
-        if (j >= kFbKVStages) ftc_wait(&kv_empty[s], (u - 1) & 1, 41, j);
-        const int kr = kstart + j * 64;
-        uint8_t* st = smem + L::kKV + s * 4 * kFbBox64;
-        mbar_arrive_expect_tx(&kv_full[s], 4 * kFbBox64);
-        tma_load_3d(st, &maps.k64, &kv_full[s], 0, kr, hk * 2);
-        tma_load_3d(st + 2 * kFbBox64, &maps.v64, &kv_full[s], 0, kr, hk * 2);
+      FbDqItem it;
+      int g = 0;
+      for (int k = 0; fb_dq_item(p, blockIdx.x + k * G, it); ++k) {
+        const int qb = k & 1, hk = it.h / Gh;
+        if (k >= 2) ftc_wait(&q_empty[qb], ((k >> 1) - 1) & 1, 40, k);
+        uint8_t* qo = smem + L::kQO + qb * 4 * kFbBox128;
+        mbar_arrive_expect_tx(&q_full[qb], 4 * kFbBox128);
+        tma_load_2d(qo, &maps.q128, &q_full[qb], it.h * kFaD, it.q0);
+        tma_load_2d(qo + kFbBox128, &maps.q128, &q_full[qb], it.h * kFaD + 64, it.q0);
+        tma_load_2d(qo + 2 * kFbBox128, &maps.o128, &q_full[qb], it.h * kFaD, it.q0);
+        tma_load_2d(qo + 3 * kFbBox128, &maps.o128, &q_full[qb], it.h * kFaD + 64, it.q0);
+        for (int j = 0; j < it.n_steps; ++j, ++g) {
+          const int s = g % kFbKVStages, u = g / kFbKVStages;
+          if (g >= kFbKVStages) ftc_wait(&kv_empty[s], (u - 1) & 1, 41, g);
+          const int kr = it.kstart + j * 64;
+          uint8_t* st = smem + L::kKV + s * 4 * kFbBox64;
+          mbar_arrive_expect_tx(&kv_full[s], 4 * kFbBox64);
+          tma_load_3d(st, &maps.k64, &kv_full[s], 0, kr, hk * 2);
+          tma_load_3d(st + 2 * kFbBox64, &maps.v64, &kv_full[s], 0, kr, hk * 2);
+        }
       }
     }
   } else if (warp == 1) {
     const uint32_t idesc_s = umma_idesc_bf16(128, 64);
     const uint32_t idesc_g = umma_idesc_bf16(128, 128) | (1u << 16);  // B (K) MN-major
-    const uint32_t sq = smem_u32(smem + L::kQ), so = smem_u32(smem + L::kO);
-    ftc_wait(q_full, 0, 42, 0);
-    auto issue_s = [&](int j) {
-      const int s = j & 1, ks = j % kFbKVStages;
-      ftc_wait(&kv_full[ks], (j / kFbKVStages) & 1, 43, j);
-      if (j >= 2) ftc_wait(&s_free[s], ((j >> 1) - 1) & 1, 44, j);
+    // S = Q K^T, dP = dO V^T of item k's step j (global step g)
+    auto issue_s = [&](int k, const FbDqItem& it, int j, int g) {
+      const int s = g & 1, ks = g % kFbKVStages, qb = k & 1;
+      if (j == 0) ftc_wait(&q_full[qb], (k >> 1) & 1, 42, k);
+      ftc_wait(&kv_full[ks], (g / kFbKVStages) & 1, 43, g);
+      if (g >= 2) ftc_wait(&s_free[s], ((g >> 1) - 1) & 1, 44, g);
       tc_fence_after();
+      const uint32_t sq = smem_u32(smem + L::kQO + qb * 4 * kFbBox128), so = sq + 2 * kFbBox128;
       const uint32_t sk = smem_u32(smem + L::kKV + ks * 4 * kFbBox64), sv = sk + 2 * kFbBox64;
       if (elect_one()) {
         if (!(g_fb_debug & 1))
@@ -408,75 +430,96 @@ __global__ void __launch_bounds__(384, 1)
                     umma_desc_kmajor(sv + offb, 128), idesc_s, kk ? 1u : 0u);
         }
         umma_commit(&s_full[s]);
+        if (j == it.n_steps - 1) umma_commit(&q_empty[qb]);
       }
       __syncwarp();
     };
-    issue_s(0);
-    for (int j = 0; j < n_steps; ++j) {
-      if (j + 1 < n_steps) issue_s(j + 1);
-      const int s = j & 1;
-      ftc_wait(&p_full[s], (j >> 1) & 1, 45, j);
-      tc_fence_after();
-      const int ks = j % kFbKVStages;
-      const uint32_t sk = smem_u32(smem + L::kKV + ks * 4 * kFbBox64);
-      if (elect_one()) {
-        if (!(g_fb_debug & 1))
+    FbDqItem it, nx;
+    if (fb_dq_item(p, blockIdx.x, it)) {
+      issue_s(0, it, 0, 0);
+      int g = 0;
+      for (int k = 0;; ++k) {
+        const bool has_next = fb_dq_item(p, blockIdx.x + (k + 1) * G, nx);
+        const int ob = k & 1;
+        for (int j = 0; j < it.n_steps; ++j, ++g) {
+          if (j + 1 < it.n_steps) issue_s(k, it, j + 1, g + 1);
+          else if (has_next) issue_s(k + 1, nx, 0, g + 1);
+          const int s = g & 1, ks = g % kFbKVStages;
+          ftc_wait(&p_full[s], (g >> 1) & 1, 45, g);
+          if (j == 0 && k >= 2) ftc_wait(&dq_empty[ob], ((k >> 1) - 1) & 1, 49, k);
+          tc_fence_after();
+          const uint32_t sk = smem_u32(smem + L::kKV + ks * 4 * kFbBox64);
+          if (elect_one()) {
+            if (!(g_fb_debug & 1))
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // 16 keys per MMA; dS packed in TMEM (dP buffer s)
-          umma_bf16_ta(tmem + 256, tmem + 128 + s * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
-                       umma_desc_mnmajor(sk + kk * 2048, kFbBox64), idesc_g, (j | kk) ? 1u : 0u);
-        umma_commit(&mm_done[s]);
-        umma_commit(&kv_empty[ks]);
+            for (int kk = 0; kk < 4; ++kk)  // 16 keys per MMA; dS packed in TMEM (dP buffer s)
+              umma_bf16_ta(tmem + 256 + ob * 128, tmem + 128 + s * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
+                           umma_desc_mnmajor(sk + kk * 2048, kFbBox64), idesc_g, (j | kk) ? 1u : 0u);
+            umma_commit(&kv_empty[ks]);
+            if (j == it.n_steps - 1) umma_commit(&dq_full[ob]);
+          }
+          __syncwarp();
+        }
+        if (!has_next) break;
+        it = nx;
       }
-      __syncwarp();
     }
   } else if (warp >= 4) {
     // ===================== elementwise: thread = 32 keys of one query row =====================
     const int ew = warp & 3, half = (warp - 4) >> 2;
-    const int r = ew * 32 + lane, qr = q0 + r;
-    const bool row_ok = qr < p.T;
-    const int qs = row_ok ? p.row_start[qr] : 0x7fffffff;
-    const float lse = row_ok ? p.lse[(size_t)h * p.stat_ld + qr] : 0.f;
-    const float dl = row_ok ? p.delta[(size_t)h * p.stat_ld + qr] : 0.f;
+    const int r = ew * 32 + lane;
     const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-    const int qs_last = p.row_start[q0 + nq - 1];
     const float c = p.scale_log2;
-    for (int j = 0; j < n_steps; ++j) {
-      const int s = j & 1;
-      const int key0 = kstart + j * 64 + half * 32;
-      ftc_wait(&s_full[s], (j >> 1) & 1, 46, j);
-      tc_fence_after();
-      if (g_fb_debug & 2) {
+    FbDqItem it;
+    int g = 0;
+    for (int k = 0; fb_dq_item(p, blockIdx.x + k * G, it); ++k) {
+      const int ob = k & 1;
+      const int qr = it.q0 + r;
+      const bool row_ok = qr < p.T;
+      const int qs = row_ok ? p.row_start[qr] : 0x7fffffff;
+      const float lse = row_ok ? p.lse[(size_t)it.h * p.stat_ld + qr] : 0.f;
+      const float dl = row_ok ? p.delta[(size_t)it.h * p.stat_ld + qr] : 0.f;
+      const int qs_last = p.row_start[it.q0 + it.nq - 1];
+      for (int j = 0; j < it.n_steps; ++j, ++g) {
+        const int s = g & 1;
+        const int key0 = it.kstart + j * 64 + half * 32;
+        ftc_wait(&s_full[s], (g >> 1) & 1, 46, g);
+        tc_fence_after();
+        if (g_fb_debug & 2) {
+          __syncwarp();
+          if (lane == 0) { mbar_arrive(&s_free[s]); mbar_arrive(&p_full[s]); }
+          continue;
+        }
+        uint32_t sr[32], dp[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + s * 64 + half * 32, sr);
+        tmem_ld_32x32b_x32(tmem + lane_base + 128 + s * 64 + half * 32, dp);
+        tmem_wait_ld();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) { mbar_arrive(&s_free[s]); mbar_arrive(&p_full[s]); }
-        continue;
-      }
-      uint32_t sr[32], dp[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + s * 64 + half * 32, sr);
-      tmem_ld_32x32b_x32(tmem + lane_base + 128 + s * 64 + half * 32, dp);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[s]);
-      const bool interior = nq == 128 && key0 + 31 <= q0 && key0 >= qs_last;
-      float dsv[32];
+        if (lane == 0) mbar_arrive(&s_free[s]);
+        const bool interior = it.nq == 128 && key0 + 31 <= it.q0 && key0 >= qs_last;
+        float dsv[32];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const int key = key0 + e;
-        const bool ok = interior | (row_ok & (key <= qr) & (key >= qs));  // branch-free
-        const float pe = ex2_approx(ok ? fmaf(__uint_as_float(sr[e]), c, -lse) : -INFINITY);
-        dsv[e] = pe * (__uint_as_float(dp[e]) - dl);
+        for (int e = 0; e < 32; ++e) {
+          const int key = key0 + e;
+          const bool ok = interior | (row_ok & (key <= qr) & (key >= qs));  // branch-free
+          const float pe = ex2_approx(ok ? fmaf(__uint_as_float(sr[e]), c, -lse) : -INFINITY);
+          dsv[e] = pe * (__uint_as_float(dp[e]) - dl);
+        }
+        fb_store_tmem32(tmem + lane_base + 128 + s * 64 + half * 32, dsv);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[s]);
       }
-      fb_store_tmem32(tmem + lane_base + 128 + s * 64 + half * 32, dsv);
-      tmem_wait_st();
+      ftc_wait(&dq_full[ob], (k >> 1) & 1, 48, k);
+      tc_fence_after();
+      fb_store_acc64(tmem + lane_base + 256 + ob * 128 + half * 64,
+                     p.dq + (size_t)qr * p.lddq + it.h * kFaD + half * 64, p.scale, row_ok);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[s]);
+      if (lane == 0) mbar_arrive(&dq_empty[ob]);
     }
-    ftc_wait(&mm_done[(n_steps - 1) & 1], ((n_steps - 1) >> 1) & 1, 48, n_steps);
-    tc_fence_after();
-    fb_store_acc64(tmem + lane_base + 256 + half * 64,
-                   p.dq + (size_t)qr * p.lddq + h * kFaD + half * 64, p.scale, row_ok);
   }
   tc_fence_before();
   __syncthreads();
