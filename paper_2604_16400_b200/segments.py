@@ -115,6 +115,15 @@ def plan_segments(seg_start, seg_adapter) -> HostPlan:
 
 
 SHRINK_TC_MIN_ROWS = int(os.environ.get("COLLM_SHRINK_TC_MIN_ROWS", "4096"))
+
+
+def default_tc_ctas(n_rows: int, rank_sms: int, num_sms: int) -> int:
+    """CTAs of the K1' shrink for a pass of n_rows rows (0 = the mma.sync K1): the rank-space
+    partition when one is set, else the whole GPU (even: TPC pairs) for passes of
+    >= SHRINK_TC_MIN_ROWS rows."""
+    if rank_sms:
+        return rank_sms
+    return num_sms // 2 * 2 if n_rows >= SHRINK_TC_MIN_ROWS else 0
 TC_RANKS = (16, 32, 48, 64, 96, 128, 192, 256)  # group widths the K1' units are planned for
 
 
@@ -157,9 +166,7 @@ class DevicePlan:
             from . import ops
             tc_ctas = 0
             if dev.type == "cuda":
-                tc_ctas = ops.rank_sms(dev)
-                if not tc_ctas and self.n_rows >= SHRINK_TC_MIN_ROWS:
-                    tc_ctas = ops.num_sms(dev) // 2 * 2
+                tc_ctas = default_tc_ctas(self.n_rows, ops.rank_sms(dev), ops.num_sms(dev))
         self.tc_ctas = int(tc_ctas)
         # K1' units per group width (the rank-space partition, collm_set_rank_sms)
         tc_plans = [plan_shrink_windows(host, nr, self.tc_ctas) for nr in TC_RANKS] \

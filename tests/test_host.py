@@ -189,3 +189,39 @@ def test_plan_shrink_windows(lib, n_ctas, nr):
             for _, _, a, c, S, *_ in chunks]
     loads = [sum(cost[ptr[c]:ptr[c + 1]]) for c in range(n_ctas)]
     assert max(loads) - min(loads) <= max(cost)
+
+
+def test_reduce_tsplit_rules(monkeypatch):
+    """K5 split choice (host side of collm_lora_reduce): the tcgen05 stream splits T only when the
+    static share per CTA would be unbalanced by > 8 % and every part keeps >= 8 whole 128-row
+    chunks (BASELINE shapes: 7B / 8B whole tiles, 13B two parts); the mma.sync kernel fills one
+    wave of 3 CTAs per SM."""
+    import torch
+
+    from paper_2604_16400_b200 import ops
+    monkeypatch.setattr(ops, "num_sms", lambda device=None: 148)
+    dev = torch.device("cpu")
+    monkeypatch.setattr(ops, "reduce_impl", lambda: 1)
+    assert ops.reduce_tsplit(512, 514, dev) == 1        # 7B: 4 chunks per tile
+    assert ops.reduce_tsplit(8192, 576, dev) == 1       # 8B: 3.89 tiles per CTA, balanced
+    assert ops.reduce_tsplit(16384, 644, dev) == 2      # 13B: 4.35 -> 8.70 units per CTA
+    assert ops.reduce_tsplit(100, 3, dev) == 1          # one chunk
+    for T, tiles in ((4096, 10), (70000, 300), (2048, 148)):
+        ts = ops.reduce_tsplit(T, tiles, dev)
+        chunks = -(-T // 128)
+        assert 1 <= ts <= chunks and (ts == 1 or chunks >= 8 * ts)
+    monkeypatch.setattr(ops, "reduce_impl", lambda: 0)
+    assert ops.reduce_tsplit(512, 514, dev) == 1
+    assert ops.reduce_tsplit(4096, 8, dev) == min(3 * 148 // 8, 4096 // 32 // 3, 128)
+
+
+def test_shrink_tc_selection_by_rows():
+    """Passes of >= SHRINK_TC_MIN_ROWS rows take K1' on the whole GPU, smaller passes keep the
+    mma.sync K1, a rank-space partition always takes K1' on its SMs (BASELINE: 7B 1024 rows -> K1,
+    8B 26985 / 13B 16640 rows -> K1' on 148 CTAs)."""
+    from paper_2604_16400_b200 import segments
+    m = segments.SHRINK_TC_MIN_ROWS
+    assert segments.default_tc_ctas(1024, 0, 148) == (148 if m <= 1024 else 0)
+    assert segments.default_tc_ctas(max(m, 16640), 0, 148) == 148
+    assert segments.default_tc_ctas(max(m, 16640), 0, 147) == 146
+    assert segments.default_tc_ctas(100, 16, 148) == 16
