@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 2 * kFbQStages);
 
   const int hk = blockIdx.y;
-  const int k0 = (gridDim.x - 1 - blockIdx.x) * 128;  // long (early-key) tiles first
+  const int k0 = blockIdx.x * 128;  // early keys (the most queries) first
   if (k0 >= p.T) return;
   const int G = p.n_heads / p.n_kv_heads;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
