@@ -428,7 +428,10 @@ def test_paged_attention_vs_oracle(n_heads, n_kv):
                                                ([130, 7, 300], 8, 2), ([1024], 2, 1),
                                                ([1] * 40 + [3, 17, 90] + [1] * 30, 4, 1),
                                                ([129, 1, 255, 384, 2], 4, 4),
-                                               ([300, 5, 700], 8, 1), ([2048, 1000], 4, 1)])
+                                               ([300, 5, 700], 8, 1), ([2048, 1000], 4, 1),
+                                               # > 2 x 148 (tile, head) items: every persistent
+                                               # CTA walks several items (Q / O / dQ buffers wrap)
+                                               ([1500, 7, 1200, 1389], 16, 4)])
 @pytest.mark.parametrize("impl", [1, 0], ids=["tcgen05", "mma"])
 def test_flash_attention_vs_oracle(lens, n_heads, n_kv, impl):
     """K9: causal attention of packed sequences (ragged lengths incl. 1, tile boundaries 63/64/65,

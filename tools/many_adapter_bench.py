@@ -50,7 +50,9 @@ for n_distinct, expand_rows in ((1, True), (32, True), (256, False), (256, True)
     os.environ["COLLM_EXPAND_ROWS_SLOTS"] = "32" if expand_rows else "100000"
     items = [InferenceItem(i, i * n_distinct // T, 1, RowRole.DECODE) for i in range(T)]
     mb = segments.build_mixed_batch(None, items)
-    plan = segments.DevicePlan(segments.plan_segments(mb.seg_start, mb.seg_adapter))
+    tc = int(os.environ.get("TC", "0"))  # K1' on this many CTAs (0: the default selection)
+    plan = segments.DevicePlan(segments.plan_segments(mb.seg_start, mb.seg_adapter),
+                               tc_ctas=tc or None)
     torch.cuda.synchronize()
     tag = f"{n_distinct} adapters" + (" [per-row expand]" if plan.n_expand_tiles else "")
     res[f"{tag}: shrink+GEMM"] = timed(lambda: proj.forward(X, plan, Y))
